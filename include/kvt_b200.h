@@ -1,0 +1,311 @@
+/*
+ * kvt_b200.h — C ABI of the B200 EvicPress hot path.
+ *
+ * This is the drop-in boundary. The reference (`kvtier`, a C++20 library)
+ * exposes its hot path as free functions in namespace kvtier
+ * (proj/include/kvtier/utility.hpp, proj/include/kvtier/placement.hpp).
+ * Every entry point below names the reference function it replaces.
+ * Signatures use plain pointers, sizes and POD structs only: no torch,
+ * no std:: types, no CUDA types. Three implementations share this ABI:
+ *
+ *   kvt_*   libkvt_b200.so      sm_100a CUDA (the product)
+ *   orc_*   oracle/liboracle.so  CPU restatement (test infrastructure only)
+ *   ref_*   oracle/_ref/libkvtier_ref.so  the reference library itself,
+ *                                built from /root/reference sources
+ *
+ * Conventions
+ *  - Contexts are identified by their index in byte-lexicographic order
+ *    of ContextId (the iteration order of kvtier::ProfileMap, a
+ *    std::map<std::string,...>). Tie-breaks "smaller context id" in the
+ *    reference therefore become "smaller index".
+ *  - Methods are identified by their index in the CandidateSpace's
+ *    MethodSet insertion order (proj/src/utility.cpp:102,136).
+ *  - Ratios are identified by their index in CandidateSpace order:
+ *    sorted descending, de-duplicated (proj/src/utility.cpp:31-32).
+ *  - Tiers are validated and stable-sorted by tier_id exactly like
+ *    validate_hierarchy (proj/src/core.cpp:86-121); "tier index" is the
+ *    position after sorting, actions report tier_id.
+ *  - Every call returns a kvt_status; on failure kvt_last_error() (or
+ *    orc_/ref_ equivalent) holds the message. KVT_EVALIDATION maps back to
+ *    kvtier::ValidationError (proj/include/kvtier/core.hpp:18-20).
+ *  - Functions are re-entrant per handle; one handle per thread/stream
+ *    (the reference runs independent stores concurrently under
+ *    `compare --jobs`, proj/tools/kvtier_main.cpp:206-235).
+ */
+#ifndef KVT_B200_H
+#define KVT_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVT_ABI_VERSION 1
+
+/* Hard limits of the device kernels (kernel-parameter structs). */
+#define KVT_MAX_TIERS 8
+#define KVT_MAX_METHODS 16
+#define KVT_MAX_RATIOS 32
+
+typedef enum {
+  KVT_OK = 0,
+  KVT_EVALIDATION = 1, /* kvtier::ValidationError */
+  KVT_ETRACE = 2,      /* kvtier::TraceError */
+  KVT_ECUDA = 3,       /* CUDA runtime / launch failure */
+  KVT_EINVAL = 4,      /* bad ABI argument (null pointer, limits) */
+  KVT_ENOMEM = 5
+} kvt_status;
+
+typedef enum { KVT_RULE_UTILITY = 0, KVT_RULE_QUALITY_FIRST = 1 } kvt_rule;
+/* proj/include/kvtier/utility.hpp:87 SelectionRule */
+
+typedef enum { KVT_INSERT = 0, KVT_RECOMPRESS = 1, KVT_EVICT = 2 } kvt_action_kind;
+/* proj/include/kvtier/core.hpp:96-103 PlacementAction::Kind */
+
+/* proj/include/kvtier/core.hpp:63-71 TierSpec (name dropped: only used in
+ * error text). */
+typedef struct {
+  int32_t tier_id;
+  int32_t unlimited; /* 1 = capacity_bytes is nullopt */
+  int64_t capacity_bytes;
+  double read_bandwidth;       /* bytes per second, > 0 */
+  double fixed_access_latency; /* seconds, >= 0 */
+} kvt_tier;
+
+/* proj/include/kvtier/utility.hpp:31-46 CandidateSpace +
+ * proj/include/kvtier/core.hpp:28-47 MethodSet. */
+typedef struct {
+  int32_t n_methods;
+  const char* const* method_names;      /* insertion order */
+  const double* decompression_overhead; /* seconds per byte, >= 0 */
+  int32_t n_ratios;
+  const double* ratios; /* any order; sorted desc + de-duplicated inside */
+} kvt_space;
+
+/* proj/include/kvtier/core.hpp:74-79 UtilityParams (prefill terms are not on
+ * the placement path). */
+typedef struct {
+  double alpha;
+} kvt_params;
+
+/* A set of kvtier::ContextProfile (proj/include/kvtier/quality.hpp:20-29),
+ * struct-of-arrays over contexts in ProfileMap order. Quality rows are
+ * stored per *space* method (methods absent from the space are dropped,
+ * they can never be enumerated; methods of the space absent from the
+ * profile have has_method = 0 and are unscorable,
+ * proj/src/utility.cpp:13-17). */
+typedef struct {
+  int32_t n_ctx;
+  int32_t n_methods;                  /* == space n_methods */
+  const int64_t* original_size_bytes; /* [n_ctx] */
+  const double* frequency;            /* [n_ctx] profile frequency (utility.cpp:76) */
+  const int32_t* grid_offset;         /* [n_ctx+1] CSR into grid */
+  const double* grid;                 /* ascending ratio grid per context */
+  const double* quality;  /* [grid_offset[c]*n_methods + m*len_c + i] */
+  const uint8_t* has_method; /* [n_ctx*n_methods] */
+} kvt_profiles;
+
+/* proj/include/kvtier/core.hpp:96-103 PlacementAction. */
+typedef struct {
+  int32_t kind;    /* kvt_action_kind */
+  int32_t ctx;     /* context index */
+  int32_t tier_id; /* target tier id (current tier for Recompress) */
+  int32_t method;  /* space method index */
+  double ratio;
+} kvt_action;
+
+/* proj/include/kvtier/placement.hpp:75-81 UpdateCandidate with its
+ * ConfigCandidate target (proj/include/kvtier/utility.hpp:17-26). */
+typedef struct {
+  int32_t ctx;
+  int32_t kind; /* KVT_RECOMPRESS or KVT_EVICT */
+  int32_t tier_index;
+  int32_t tier_id;
+  int32_t method;
+  int32_t pad_;
+  double ratio;
+  int64_t size_bytes;
+  double quality;
+  double ttft;
+  double utility;
+  double utility_drop;
+  int64_t bytes_freed;
+} kvt_update;
+
+/* Dense candidate tables (the all_candidates cross product,
+ * proj/src/utility.cpp:129-145) laid out for the device:
+ *   size    [n_ctx][R]          compressed_size(orig, ratio_r)
+ *   quality [n_ctx][M][R]       quality_of; valid = scorable
+ *   valid   [n_ctx][M][R]
+ *   ttft    [n_ctx][T][M][R]    load_time
+ *   utility [n_ctx][T][M][R]    utility_score
+ * Any output pointer may be NULL. */
+
+/* Per-context winner of best_config (proj/src/utility.cpp:159-172). */
+typedef struct {
+  int32_t status; /* 0 ok, 1 no scorable configuration (ValidationError) */
+  int32_t tier_index;
+  int32_t tier_id;
+  int32_t method;
+  int32_t ratio_index;
+  int32_t pad_;
+  double ratio;
+  int64_t size_bytes;
+  double quality;
+  double ttft;
+  double utility;
+} kvt_best;
+
+/* Resident snapshot of one context (proj/include/kvtier/core.hpp:84-93
+ * CacheEntry). tier_index = -1 when not resident. seq orders arrival
+ * within a tier (StoreState keeps per-tier vectors in arrival order). */
+typedef struct {
+  int32_t tier_index;
+  int32_t method;
+  double ratio;
+  int64_t original_size_bytes;
+  int64_t frequency;
+  int64_t last_access;
+  int64_t seq;
+} kvt_entry;
+
+typedef struct kvt_handle kvt_handle;   /* device, stream, scratch */
+typedef struct kvt_pset kvt_pset;       /* uploaded profile set */
+typedef struct kvt_store kvt_store;     /* StoreState */
+
+#define KVT_DECLARE_API(P)                                                         \
+  const char* P##last_error(void);                                                 \
+  int P##abi_version(void);                                                        \
+  /* handle: device ordinal, CUDA stream (NULL = default); CPU impls ignore */     \
+  int P##create(int device, void* stream, kvt_handle** out);                       \
+  int P##destroy(kvt_handle* h);                                                   \
+  int P##pset_create(kvt_handle* h, const kvt_profiles* profiles, kvt_pset** out); \
+  int P##pset_destroy(kvt_pset* p);                                                \
+  /* utility.cpp:129-145 all_candidates (dense, all contexts) */                   \
+  int P##score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, \
+                          int32_t n_tiers, const kvt_space* space,                 \
+                          const kvt_params* params, int64_t* size, double* quality, \
+                          uint8_t* valid, double* ttft, double* utility);          \
+  /* utility.cpp:159-172 best_config (every context) */                            \
+  int P##best_config(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers,      \
+                     int32_t n_tiers, const kvt_space* space,                      \
+                     const kvt_params* params, int32_t rule, kvt_best* out);       \
+  /* placement.cpp:44-159 StoreState */                                            \
+  int P##store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_tiers,       \
+                      int32_t n_ctx, kvt_store** out);                             \
+  int P##store_destroy(kvt_store* s);                                              \
+  /* names entry method indices (store_add before any placement call) */          \
+  int P##store_bind_space(kvt_store* s, const kvt_space* space);                   \
+  int P##store_add(kvt_store* s, int32_t ctx, const kvt_entry* e);                 \
+  int P##store_remove(kvt_store* s, int32_t ctx, kvt_entry* removed);              \
+  int P##store_reconfigure(kvt_store* s, int32_t ctx, int32_t method, double ratio); \
+  int P##store_touch(kvt_store* s, int32_t ctx, int64_t stamp);                    \
+  int P##store_clear(kvt_store* s);                                                \
+  int P##store_occupancy(kvt_store* s, int64_t* occ);                              \
+  int P##store_snapshot(kvt_store* s, kvt_entry* entries);                         \
+  /* placement.cpp:174-204 least_drop_update (does not apply it) */                \
+  int P##least_drop_update(kvt_store* s, const kvt_pset* p, const kvt_space* space, \
+                           const kvt_params* params, int32_t tier_index,           \
+                           kvt_update* out);                                       \
+  /* placement.cpp:206-223 resolve_overflow. Actions of every mutating call   \
+   * are buffered inside the store; *n_actions returns how many, fetch them  \
+   * with store_actions. */                                                    \
+  int P##resolve_overflow(kvt_store* s, const kvt_pset* p, const kvt_space* space, \
+                          const kvt_params* params, int64_t* n_actions);           \
+  /* placement.cpp:225-250 insert_joint, batched: ops applied in order, the    \
+   * action list is the concatenation of the per-op lists. On error *n_done   \
+   * tells how many ops completed (the failing op may be half applied, as in  \
+   * the reference, which mutates before it throws). */                        \
+  int P##insert_joint(kvt_store* s, const kvt_pset* p, const kvt_space* space,     \
+                      const kvt_params* params, int32_t rule, const int32_t* ctx,  \
+                      const int64_t* frequency, const int64_t* stamp, int64_t n_ops, \
+                      int64_t* n_actions, int64_t* n_done);                        \
+  /* placement.cpp:252-283 rearrange */                                            \
+  int P##rearrange(kvt_store* s, const kvt_pset* p, const kvt_space* space,        \
+                   const kvt_params* params, int32_t rule, int64_t* n_actions);    \
+  /* copy the first n buffered actions of the last mutating call */               \
+  int P##store_actions(kvt_store* s, kvt_action* out, int64_t n);                  \
+  /* placement.cpp:285-298 placement_utility */                                    \
+  int P##placement_utility(kvt_store* s, const kvt_pset* p, const kvt_space* space, \
+                           const kvt_params* params, double* out);
+
+KVT_DECLARE_API(kvt_)
+
+/* ------------------------------------------------------------------------
+ * KV codec (builder-defined; the reference has no codec, SPEC.md:15 —
+ * parity unpinned). All pointers are device
+ * pointers for kvt_*, host pointers for orc_*. Layout: K and V are bf16
+ * [L][H][T][D] with D == 128.
+ * ------------------------------------------------------------------------ */
+typedef enum { KVT_SCORER_KNORM = 0, KVT_SCORER_KEYDIFF = 1, KVT_SCORER_SNAPKV = 2 } kvt_scorer;
+
+typedef struct {
+  int32_t L, H, T, D; /* D must be 128 */
+} kvt_kv_shape;
+
+/* One codec configuration resolved from a (method label, ratio) pair. */
+typedef struct {
+  int32_t scorer;     /* kvt_scorer */
+  int32_t bits;       /* 2, 4, 8 or 16 (16 = bf16, token drop only) */
+  int32_t keep;       /* tokens kept per (layer, kv head), 1..T */
+  int32_t window;     /* snapkv observation window W (always kept) */
+  int32_t q_heads;    /* snapkv query heads per kv head (GQA group) */
+  int32_t pool;       /* snapkv max-pool kernel (odd) */
+  uint64_t q_seed;    /* snapkv synthetic query seed */
+} kvt_codec_cfg;
+
+/* Layout of one compressed chunk (all offsets in bytes from blob start). */
+typedef struct {
+  int64_t idx_off, idx_bytes;       /* int32 [L][H][keep] ascending */
+  int64_t kcode_off, kcode_bytes;   /* u32 words, [L][H][keep][D*bits/32] */
+  int64_t kscale_off, kzero_off, kparam_bytes; /* fp16 [L][H][ceil(keep/G)][D] each */
+  int64_t vcode_off, vcode_bytes;   /* u32 words, [L][H][keep][D*bits/32] */
+  int64_t vscale_off, vzero_off, vparam_bytes; /* fp16 [L][H][keep] each */
+  int64_t total_bytes;
+} kvt_blob_map;
+
+#define KVT_QGROUP 128 /* K per-channel quant group (kept tokens) */
+
+#define KVT_DECLARE_CODEC(P)                                                          \
+  /* resolve "<scorer>[-q<bits>]" + retained-size ratio into a codec config */      \
+  int P##codec_plan(const char* method, double ratio, const kvt_kv_shape* shape,     \
+                    kvt_codec_cfg* out);                                             \
+  int P##blob_layout(const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,            \
+                     kvt_blob_map* out);                                          \
+  /* synthetic KV: counter hash of (seed, ctx, layer, head, token, dim) */          \
+  int P##kv_generate(kvt_handle* h, const kvt_kv_shape* shape, uint64_t seed,        \
+                     uint64_t ctx, uint16_t* k, uint16_t* v);                        \
+  /* per-(layer, head, token) float scores; larger = more important */              \
+  int P##token_scores(kvt_handle* h, const kvt_kv_shape* shape,                      \
+                      const kvt_codec_cfg* cfg, const uint16_t* k, float* scores);   \
+  /* per (layer, head): `keep` largest scores, ties -> lower index, ascending */    \
+  int P##topk(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,    \
+              const float* scores, int32_t* idx);                                    \
+  /* gather kept tokens, quantise, pack into blob */                                 \
+  int P##pack(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,    \
+              const uint16_t* k, const uint16_t* v, const int32_t* idx, void* blob); \
+  /* unpack + dequantise into bf16 [L][H][keep][D] */                                \
+  int P##unpack(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,  \
+                const void* blob, uint16_t* k_out, uint16_t* v_out);                 \
+  /* scores + topk + pack in one call (workspace: scores + idx, see below) */      \
+  int P##compress(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg, \
+                  const uint16_t* k, const uint16_t* v, void* workspace, void* blob); \
+  int64_t P##compress_workspace_bytes(const kvt_kv_shape* shape, const kvt_codec_cfg* cfg);
+
+KVT_DECLARE_CODEC(kvt_)
+
+/* Device-pointer variants and timing helpers used by the bench. */
+/* Synchronise the handle's stream. */
+int kvt_sync(kvt_handle* h);
+/* Set the stream used by subsequent launches on this handle. */
+int kvt_set_stream(kvt_handle* h, void* stream);
+/* Number of kernels this handle launched so far (evidence for gpu_launches). */
+int64_t kvt_launch_count(kvt_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVT_B200_H */
