@@ -1,0 +1,1535 @@
+// Placement hot path on sm_100a: candidate scoring (K1, fused best_config)
+// and the least-utility-drop greedy (K2 per-resident best update + K3
+// persistent single-warp resolver) behind the kvt_* C ABI.
+//
+// Reference: proj/src/utility.cpp (scoring), proj/src/placement.cpp (store +
+// greedy). Results are bit-identical to the reference library (tests/).
+//
+// Greedy design. A resident's update options depend only on
+// its own (tier, config, profile) (utility.cpp:81-127), so each resident
+// caches its best option key (drop, bytes_freed, enumeration index) and a
+// per-tier 32-ary tournament tree keeps the tier-wide argmin under the
+// reference's total order (drop asc, bytes_freed desc, context asc;
+// placement.cpp:165-170). One step = read root, apply, recompute one
+// resident with one warp, update <= 2 tree paths of depth log32(N). The
+// whole insert/resolve sequence runs in ONE persistent warp: the
+// dependency chain is strictly sequential, so the kernel is built for
+// latency (no block barriers, no host round trips between steps).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "kvt_common.cuh"
+
+namespace kvt {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+}  // namespace kvt
+
+using namespace kvt;
+
+
+
+extern "C" const char* kvt_last_error(void) { return g_err.c_str(); }
+extern "C" int kvt_abi_version(void) { return KVT_ABI_VERSION; }
+
+static int ensure_scratch(kvt_handle* h, size_t bytes) {
+  if (h->scratch_bytes >= bytes) return KVT_OK;
+  if (h->scratch) cudaFree(h->scratch);
+  h->scratch = nullptr;
+  h->scratch_bytes = 0;
+  KVT_CUDA_TRY(cudaMalloc(&h->scratch, bytes));
+  h->scratch_bytes = bytes;
+  return KVT_OK;
+}
+
+extern "C" int kvt_create(int device, void* stream, kvt_handle** out) {
+  if (!out) return set_error(KVT_EINVAL, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_error(KVT_ECUDA, std::string("no CUDA device visible: ") + cudaGetErrorString(e));
+  KVT_CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  KVT_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return set_error(KVT_ECUDA, std::string("libkvt_b200 is built for sm_100a, device is ") + prop.name);
+  auto* h = new kvt_handle();
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  *out = h;
+  return KVT_OK;
+}
+
+extern "C" int kvt_destroy(kvt_handle* h) {
+  if (!h) return KVT_OK;
+  if (h->scratch) cudaFree(h->scratch);
+  delete h;
+  return KVT_OK;
+}
+
+extern "C" int kvt_sync(kvt_handle* h) {
+  KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return KVT_OK;
+}
+
+extern "C" int kvt_set_stream(kvt_handle* h, void* stream) {
+  h->stream = static_cast<cudaStream_t>(stream);
+  return KVT_OK;
+}
+
+extern "C" int64_t kvt_launch_count(kvt_handle* h) { return h->launches; }
+
+// ------------------------------------------------------------ host resolve
+
+// CandidateSpace ctor proj/src/utility.cpp:21-33, MethodSet ctor
+// proj/src/core.cpp:10-27.
+static int resolve_space(const kvt_space* sp, DevSpace* s) {
+  if (!sp) return set_error(KVT_EINVAL, "null space");
+  if (sp->n_methods <= 0) return set_error(KVT_EVALIDATION, "method set must not be empty");
+  if (sp->n_methods > KVT_MAX_METHODS) return set_error(KVT_EINVAL, "too many methods for the device kernels");
+  if (sp->n_ratios <= 0) return set_error(KVT_EVALIDATION, "candidate ratio grid must not be empty");
+  if (sp->n_ratios > KVT_MAX_RATIOS) return set_error(KVT_EINVAL, "too many ratios for the device kernels");
+  std::memset(s, 0, sizeof(*s));
+  s->M = sp->n_methods;
+  for (int m = 0; m < s->M; ++m) {
+    const char* nm = sp->method_names[m];
+    if (!nm || !nm[0]) return set_error(KVT_EVALIDATION, "compression method name must not be empty");
+    for (int j = 0; j < m; ++j)
+      if (std::strcmp(sp->method_names[j], nm) == 0)
+        return set_error(KVT_EVALIDATION, std::string("duplicate compression method name: ") + nm);
+    if (sp->decompression_overhead[m] < 0.0)
+      return set_error(KVT_EVALIDATION, std::string("negative decompression overhead for method ") + nm);
+    s->ovh[m] = sp->decompression_overhead[m];
+  }
+  for (int m = 0; m < s->M; ++m) {  // byte-lexicographic rank (std::string operator<)
+    int rank = 0;
+    for (int j = 0; j < s->M; ++j)
+      if (std::strcmp(sp->method_names[j], sp->method_names[m]) < 0) ++rank;
+    s->name_rank[m] = rank;
+  }
+  std::vector<double> r(sp->ratios, sp->ratios + sp->n_ratios);
+  for (double v : r)
+    if (!(v > 0.0) || v > 1.0 || !std::isfinite(v))
+      return set_error(KVT_EVALIDATION, "candidate ratio out of (0, 1]");
+  std::sort(r.begin(), r.end(), [](double a, double b) { return a > b; });
+  r.erase(std::unique(r.begin(), r.end()), r.end());
+  s->R = static_cast<int>(r.size());
+  for (int i = 0; i < s->R; ++i) s->ratio[i] = r[i];
+  return KVT_OK;
+}
+
+// validate_hierarchy proj/src/core.cpp:86-121
+static int resolve_tiers(const kvt_tier* in, int n, DevTiers* o) {
+  if (n <= 0) return set_error(KVT_EVALIDATION, "hierarchy must have at least one tier");
+  if (n > KVT_MAX_TIERS) return set_error(KVT_EINVAL, "too many tiers for the device kernels");
+  std::vector<kvt_tier> t(in, in + n);
+  std::stable_sort(t.begin(), t.end(), [](const kvt_tier& a, const kvt_tier& b) { return a.tier_id < b.tier_id; });
+  std::memset(o, 0, sizeof(*o));
+  o->T = n;
+  for (int i = 0; i < n; ++i) {
+    const std::string tid = std::to_string(t[i].tier_id);
+    if (i + 1 < n && t[i + 1].tier_id == t[i].tier_id)
+      return set_error(KVT_EVALIDATION, "duplicate tier_id " + tid);
+    if (t[i].unlimited && i + 1 != n)
+      return set_error(KVT_EVALIDATION, "unlimited capacity is only allowed on the bottom tier (tier " + tid + ")");
+    if (!t[i].unlimited && t[i].capacity_bytes < 0)
+      return set_error(KVT_EVALIDATION, "negative capacity on tier " + tid);
+    if (!(t[i].read_bandwidth > 0.0) || !std::isfinite(t[i].read_bandwidth))
+      return set_error(KVT_EVALIDATION, "read bandwidth must be > 0 on tier " + tid);
+    if (t[i].fixed_access_latency < 0.0 || !std::isfinite(t[i].fixed_access_latency))
+      return set_error(KVT_EVALIDATION, "fixed access latency must be >= 0 on tier " + tid);
+    o->id[i] = t[i].tier_id;
+    o->unlimited[i] = t[i].unlimited ? 1 : 0;
+    o->cap[i] = t[i].capacity_bytes;
+    o->bw[i] = t[i].read_bandwidth;
+    o->lat[i] = t[i].fixed_access_latency;
+  }
+  return KVT_OK;
+}
+
+static uint64_t fnv(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// ----------------------------------------------------------------- profiles
+
+struct kvt_pset {
+  kvt_handle* h = nullptr;
+  DevProfiles dev{};
+  void* buf = nullptr;
+  uint64_t id = 0;
+};
+
+static uint64_t g_pset_counter = 0;
+
+extern "C" int kvt_pset_create(kvt_handle* h, const kvt_profiles* pr, kvt_pset** out) {
+  if (!h || !pr || !out) return set_error(KVT_EINVAL, "null argument");
+  if (pr->n_ctx < 0 || pr->n_methods <= 0 || pr->n_methods > KVT_MAX_METHODS)
+    return set_error(KVT_EINVAL, "bad profile set dimensions");
+  const int n = pr->n_ctx, M = pr->n_methods;
+  const int G = pr->grid_offset[n];
+  for (int c = 0; c < n; ++c) {
+    if (pr->grid_offset[c + 1] <= pr->grid_offset[c])
+      return set_error(KVT_EVALIDATION, "profile ratio grid is empty for context " + std::to_string(c));
+    if (pr->original_size_bytes[c] <= 0)
+      return set_error(KVT_EVALIDATION, "original size must be > 0");
+  }
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_orig = 0;
+  const size_t o_freq = o_orig + align(sizeof(long long) * (n + 1));
+  const size_t o_goff = o_freq + align(sizeof(double) * (n + 1));
+  const size_t o_grid = o_goff + align(sizeof(int) * (n + 1));
+  const size_t o_qual = o_grid + align(sizeof(double) * (G + 1));
+  const size_t o_has = o_qual + align(sizeof(double) * (static_cast<size_t>(G) * M + 1));
+  const size_t total = o_has + align(static_cast<size_t>(n) * M + 1);
+  auto* p = new kvt_pset();
+  p->h = h;
+  cudaError_t e = cudaMalloc(&p->buf, total);
+  if (e != cudaSuccess) {
+    delete p;
+    return set_error(KVT_ECUDA, std::string("cudaMalloc profiles: ") + cudaGetErrorString(e));
+  }
+  char* b = static_cast<char*>(p->buf);
+  cudaStream_t s = h->stream;
+  cudaMemcpyAsync(b + o_orig, pr->original_size_bytes, sizeof(long long) * n, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_freq, pr->frequency, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_goff, pr->grid_offset, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_grid, pr->grid, sizeof(double) * G, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_qual, pr->quality, sizeof(double) * static_cast<size_t>(G) * M, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_has, pr->has_method, static_cast<size_t>(n) * M, cudaMemcpyHostToDevice, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(p->buf);
+    delete p;
+    return set_error(KVT_ECUDA, std::string("profile upload: ") + cudaGetErrorString(e));
+  }
+  p->dev.n = n;
+  p->dev.M = M;
+  p->dev.orig = reinterpret_cast<const long long*>(b + o_orig);
+  p->dev.freq = reinterpret_cast<const double*>(b + o_freq);
+  p->dev.goff = reinterpret_cast<const int*>(b + o_goff);
+  p->dev.grid = reinterpret_cast<const double*>(b + o_grid);
+  p->dev.qual = reinterpret_cast<const double*>(b + o_qual);
+  p->dev.has = reinterpret_cast<const unsigned char*>(b + o_has);
+  p->id = ++g_pset_counter;
+  *out = p;
+  return KVT_OK;
+}
+
+extern "C" int kvt_pset_destroy(kvt_pset* p) {
+  if (!p) return KVT_OK;
+  cudaFree(p->buf);
+  delete p;
+  return KVT_OK;
+}
+
+// ------------------------------------------------------------- K1 scoring
+
+struct Tables {  // dense candidate tables, see include/kvt_b200.h
+  long long* size;      // [n][R]
+  double* q;            // [n][M][R]
+  unsigned char* valid; // [n][M][R]
+  double* ttft;         // [n][T][M][R] (nullable)
+  double* u;            // [n][T][M][R]
+  kvt_best* best;       // [n] (nullable)
+};
+
+// candidate_preferred proj/src/utility.cpp:147-157; j = enumeration index
+struct CandKey {
+  double u, q, ratio;
+  int tier_id, name_rank, j;
+};
+
+__device__ __forceinline__ bool cand_better(const CandKey& a, const CandKey& b, int rule) {
+  if (a.j < 0) return false;
+  if (b.j < 0) return true;
+  if (rule == KVT_RULE_QUALITY_FIRST && a.q != b.q) return a.q > b.q;
+  if (a.u != b.u) return a.u > b.u;
+  if (a.q != b.q) return a.q > b.q;
+  if (a.tier_id != b.tier_id) return a.tier_id < b.tier_id;
+  if (a.ratio != b.ratio) return a.ratio > b.ratio;
+  if (a.name_rank != b.name_rank) return a.name_rank < b.name_rank;
+  return a.j < b.j;  // first enumerated wins exact ties (utility.cpp:167-170)
+}
+
+__device__ __forceinline__ CandKey shfl_cand(const CandKey& k, int lane_mask) {
+  CandKey o;
+  o.u = __shfl_xor_sync(0xffffffffu, k.u, lane_mask);
+  o.q = __shfl_xor_sync(0xffffffffu, k.q, lane_mask);
+  o.ratio = __shfl_xor_sync(0xffffffffu, k.ratio, lane_mask);
+  o.tier_id = __shfl_xor_sync(0xffffffffu, k.tier_id, lane_mask);
+  o.name_rank = __shfl_xor_sync(0xffffffffu, k.name_rank, lane_mask);
+  o.j = __shfl_xor_sync(0xffffffffu, k.j, lane_mask);
+  return o;
+}
+
+constexpr int kScoreWarps = 4;
+
+// One warp per context: quality_of per (method, ratio) once, then the
+// tier x method x ratio cross product (all_candidates order, utility.cpp:
+// 129-145) with the best_config argmax fused in.
+__global__ void __launch_bounds__(kScoreWarps * 32)
+k_score(DevProfiles P, DevSpace S, DevTiers TT, double alpha, int rule, Tables out) {
+  __shared__ double sq[kScoreWarps][KVT_MAX_METHODS * KVT_MAX_RATIOS];
+  __shared__ unsigned char sv[kScoreWarps][KVT_MAX_METHODS * KVT_MAX_RATIOS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kScoreWarps + warp;
+  if (c >= P.n) return;
+  const int M = S.M, R = S.R, T = TT.T, MR = M * R;
+  const long long orig = P.orig[c];
+  const double f = P.freq[c];
+  for (int k = lane; k < MR; k += 32) {
+    const int m = k / R, r = k - m * R;
+    const double ratio = S.ratio[r];
+    double q = 0.0;
+    bool ok = scorable(P, c, m, ratio);
+    if (ok) ok = quality_of(P, c, m, ratio, &q);
+    sq[warp][k] = ok ? q : 0.0;
+    sv[warp][k] = ok ? 1 : 0;
+    out.q[static_cast<size_t>(c) * MR + k] = ok ? q : 0.0;
+    out.valid[static_cast<size_t>(c) * MR + k] = ok ? 1 : 0;
+  }
+  for (int r = lane; r < R; r += 32) out.size[static_cast<size_t>(c) * R + r] = csize(orig, S.ratio[r]);
+  __syncwarp();
+  CandKey best;
+  best.j = -1;
+  best.u = best.q = best.ratio = 0.0;
+  best.tier_id = best.name_rank = 0;
+  const size_t ubase = static_cast<size_t>(c) * T * MR;
+  for (int j = lane; j < T * MR; j += 32) {
+    const int t = j / MR, k = j - t * MR;
+    const int m = k / R, r = k - m * R;
+    if (!sv[warp][k]) {
+      out.u[ubase + j] = 0.0;
+      if (out.ttft) out.ttft[ubase + j] = 0.0;
+      continue;
+    }
+    const long long sz = csize(orig, S.ratio[r]);
+    const double tt = load_time(sz, TT.lat[t], TT.bw[t], S.ovh[m]);
+    const double u = utility_score(sq[warp][k], tt, f, alpha);
+    out.u[ubase + j] = u;
+    if (out.ttft) out.ttft[ubase + j] = tt;
+    CandKey cand{u, sq[warp][k], S.ratio[r], TT.id[t], S.name_rank[m], j};
+    if (cand_better(cand, best, rule)) best = cand;
+  }
+  if (!out.best) return;
+  for (int off = 16; off > 0; off >>= 1) {
+    CandKey o = shfl_cand(best, off);
+    if (cand_better(o, best, rule)) best = o;
+  }
+  if (lane == 0) {
+    kvt_best b = {};
+    if (best.j < 0) {
+      b.status = 1;
+    } else {
+      const int t = best.j / MR, k = best.j - t * MR;
+      const int m = k / R, r = k - m * R;
+      b.tier_index = t;
+      b.tier_id = TT.id[t];
+      b.method = m;
+      b.ratio_index = r;
+      b.ratio = S.ratio[r];
+      b.size_bytes = csize(orig, S.ratio[r]);
+      b.quality = best.q;
+      b.ttft = load_time(b.size_bytes, TT.lat[t], TT.bw[t], S.ovh[m]);
+      b.utility = best.u;
+    }
+    out.best[c] = b;
+  }
+}
+
+static int launch_score(kvt_handle* h, const DevProfiles& P, const DevSpace& S, const DevTiers& T,
+                        double alpha, int rule, const Tables& out) {
+  if (P.n == 0) return KVT_OK;
+  const int blocks = (P.n + kScoreWarps - 1) / kScoreWarps;
+  k_score<<<blocks, kScoreWarps * 32, 0, h->stream>>>(P, S, T, alpha, rule, out);
+  h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  return KVT_OK;
+}
+
+extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
+                                    const kvt_space* space, const kvt_params* params, int64_t* size,
+                                    double* quality, uint8_t* valid, double* ttft, double* utility) {
+  DevSpace S;
+  DevTiers T;
+  int rc;
+  if ((rc = resolve_space(space, &S))) return rc;
+  if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
+  if (p->dev.M != S.M) return set_error(KVT_EINVAL, "profile set / space method count mismatch");
+  const size_t n = p->dev.n, R = S.R, MR = S.M * S.R, TMR = T.T * MR;
+  const size_t b_size = n * R * 8, b_q = n * MR * 8, b_v = (n * MR + 255) & ~size_t(255), b_u = n * TMR * 8;
+  if ((rc = ensure_scratch(h, b_size + b_q + b_v + 2 * b_u + 1024))) return rc;
+  char* b = static_cast<char*>(h->scratch);
+  Tables t{reinterpret_cast<long long*>(b), reinterpret_cast<double*>(b + b_size),
+           reinterpret_cast<unsigned char*>(b + b_size + b_q),
+           reinterpret_cast<double*>(b + b_size + b_q + b_v),
+           reinterpret_cast<double*>(b + b_size + b_q + b_v + b_u), nullptr};
+  if ((rc = launch_score(h, p->dev, S, T, params->alpha, KVT_RULE_UTILITY, t))) return rc;
+  cudaStream_t s = h->stream;
+  if (size) KVT_CUDA_TRY(cudaMemcpyAsync(size, t.size, b_size, cudaMemcpyDeviceToHost, s));
+  if (quality) KVT_CUDA_TRY(cudaMemcpyAsync(quality, t.q, b_q, cudaMemcpyDeviceToHost, s));
+  if (valid) KVT_CUDA_TRY(cudaMemcpyAsync(valid, t.valid, n * MR, cudaMemcpyDeviceToHost, s));
+  if (ttft) KVT_CUDA_TRY(cudaMemcpyAsync(ttft, t.ttft, b_u, cudaMemcpyDeviceToHost, s));
+  if (utility) KVT_CUDA_TRY(cudaMemcpyAsync(utility, t.u, b_u, cudaMemcpyDeviceToHost, s));
+  KVT_CUDA_TRY(cudaStreamSynchronize(s));
+  return KVT_OK;
+}
+
+extern "C" int kvt_best_config(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
+                               const kvt_space* space, const kvt_params* params, int32_t rule, kvt_best* out) {
+  DevSpace S;
+  DevTiers T;
+  int rc;
+  if ((rc = resolve_space(space, &S))) return rc;
+  if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
+  if (p->dev.M != S.M) return set_error(KVT_EINVAL, "profile set / space method count mismatch");
+  const size_t n = p->dev.n, R = S.R, MR = S.M * S.R, TMR = T.T * MR;
+  const size_t b_size = n * R * 8, b_q = n * MR * 8, b_v = (n * MR + 255) & ~size_t(255), b_u = n * TMR * 8;
+  const size_t b_best = n * sizeof(kvt_best);
+  if ((rc = ensure_scratch(h, b_size + b_q + b_v + b_u + b_best + 1024))) return rc;
+  char* b = static_cast<char*>(h->scratch);
+  Tables t{reinterpret_cast<long long*>(b), reinterpret_cast<double*>(b + b_size),
+           reinterpret_cast<unsigned char*>(b + b_size + b_q), nullptr,
+           reinterpret_cast<double*>(b + b_size + b_q + b_v),
+           reinterpret_cast<kvt_best*>(b + b_size + b_q + b_v + b_u)};
+  if ((rc = launch_score(h, p->dev, S, T, params->alpha, rule, t))) return rc;
+  KVT_CUDA_TRY(cudaMemcpyAsync(out, t.best, b_best, cudaMemcpyDeviceToHost, h->stream));
+  KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return KVT_OK;
+}
+
+// ------------------------------------------------------------------- store
+
+enum : int {
+  ST_OK = 0,
+  ST_NEED_SPACE = 1,
+  ST_ERR_RESIDENT = 2,     // already resident
+  ST_ERR_NO_CONFIG = 3,    // best_config threw
+  ST_ERR_NO_OPTION = 4,    // least_drop_update threw (no option)
+  ST_ERR_QUALITY = 5,      // quality_of threw for a resident's current config
+  ST_ERR_NOT_RESIDENT = 6,
+  ST_ERR_TIER = 7,
+};
+
+struct Ctl {
+  long long occ[KVT_MAX_TIERS];
+  int errcount[KVT_MAX_TIERS];
+  long long seq;
+  long long n_act;
+  long long cap_act;
+  long long n_ops;
+  long long resume_op;
+  int in_resolve;
+  int status;
+  int err_ctx;
+  int err_tier;
+  int n_saved;
+  int pad;
+};
+
+struct DevStore {
+  int n;
+  DevTiers TT;
+  int* tier;       // tier index or -1
+  int* meth;
+  int* ridx;       // space ratio index or -1 (off grid)
+  double* ratio;
+  long long* orig;
+  long long* freq;
+  long long* last;
+  long long* seq;
+  // cached best update per resident (K2)
+  double* cdrop;
+  long long* cbytes;
+  int* copt;       // enumeration index relative to the resident's tier; -1 none, -2 error
+  int* mem;        // tree membership: tier index if in that tier's tree, else -1
+  // 32-ary tournament trees, one per tier: tree[t*tree_stride + lvl_off[k] + node]
+  int* tree;
+  int tree_stride;
+  int nlev;
+  int lvl_off[8];
+  int lvl_size[8];
+  kvt_action* act;
+  Ctl* ctl;
+  int* saved;      // rearrange order
+};
+
+struct StepCtx {
+  DevStore st;
+  DevProfiles P;
+  DevSpace S;
+  double alpha;
+  Tables tb;
+};
+
+struct Key {
+  double drop;
+  long long bytes;
+  int idx;
+};
+
+// update_preferred proj/src/placement.cpp:165-170 + enumeration order
+__device__ __forceinline__ bool key_better(const Key& a, const Key& b) {
+  if (a.idx < 0) return false;
+  if (b.idx < 0) return true;
+  if (a.drop != b.drop) return a.drop < b.drop;
+  if (a.bytes != b.bytes) return a.bytes > b.bytes;
+  return a.idx < b.idx;
+}
+
+__device__ __forceinline__ Key warp_min(Key k) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Key o;
+    o.drop = __shfl_xor_sync(0xffffffffu, k.drop, off);
+    o.bytes = __shfl_xor_sync(0xffffffffu, k.bytes, off);
+    o.idx = __shfl_xor_sync(0xffffffffu, k.idx, off);
+    if (key_better(o, k)) k = o;
+  }
+  return k;
+}
+
+// score_candidate proj/src/utility.cpp:65-79 for an arbitrary ratio.
+__device__ __forceinline__ bool score_fly(const StepCtx& X, int c, int t, int m, double ratio, double* u,
+                                          long long* size, double* q_out = nullptr, double* tt_out = nullptr) {
+  double q;
+  if (!quality_of(X.P, c, m, ratio, &q)) return false;
+  const long long sz = csize(X.P.orig[c], ratio);
+  const double tt = load_time(sz, X.st.TT.lat[t], X.st.TT.bw[t], X.S.ovh[m]);
+  *u = utility_score(q, tt, X.P.freq[c], X.alpha);
+  *size = sz;
+  if (q_out) *q_out = q;
+  if (tt_out) *tt_out = tt;
+  return true;
+}
+
+// K2: best update of one resident (enumerate_updates proj/src/utility.cpp:
+// 81-127 scored against its current candidate, placement.cpp:179-197).
+// Whole warp; lane 0 writes the cache. Returns the tree membership.
+__device__ int compute_cache(const StepCtx& X, int c, int cur, int me, int re, double rate, long long eorig) {
+  const int lane = threadIdx.x & 31;
+  const int M = X.S.M, R = X.S.R, T = X.st.TT.T, MR = M * R;
+  const size_t qb = static_cast<size_t>(c) * MR;
+  double ucur;
+  long long scur;
+  bool ok;
+  const bool covered = re >= 0 && X.tb.valid[qb + static_cast<size_t>(me) * R + re];
+  if (covered) {
+    ucur = X.tb.u[(static_cast<size_t>(c) * T + cur) * MR + static_cast<size_t>(me) * R + re];
+    scur = X.tb.size[static_cast<size_t>(c) * R + re];
+    ok = true;
+  } else {
+    ok = score_fly(X, c, cur, me, rate, &ucur, &scur);
+  }
+  if (!ok) {
+    if (lane == 0) {
+      X.st.copt[c] = -2;
+      X.st.mem[c] = -1;
+      atomicAdd(&X.st.ctl->errcount[cur], 1);
+    }
+    __syncwarp();
+    return -1;
+  }
+  const long long cur_bytes = csize(eorig, rate);
+  const bool keep_ok = scorable(X.P, c, me, rate);
+  const int per = MR + 1;
+  const int nopt = (T - cur) * per;
+  Key best{0.0, 0, -1};
+  for (int e = lane; e < nopt; e += 32) {
+    const int j = e / per, w = e - j * per, ti = cur + j;
+    double uo;
+    long long so;
+    bool v;
+    if (w < MR) {
+      const int m = w / R, r = w - m * R;
+      v = X.tb.valid[qb + w] != 0;
+      if (v && ti == cur) v = csize(eorig, X.S.ratio[r]) < cur_bytes;
+      if (v) {
+        uo = X.tb.u[(static_cast<size_t>(c) * T + ti) * MR + w];
+        so = X.tb.size[static_cast<size_t>(c) * R + r];
+      }
+    } else {
+      v = ti != cur && !covered && keep_ok;
+      if (v) v = score_fly(X, c, ti, me, rate, &uo, &so);
+    }
+    if (v) {
+      Key k{__dsub_rn(ucur, uo), ti == cur ? scur - so : scur, e};
+      if (key_better(k, best)) best = k;
+    }
+  }
+  best = warp_min(best);
+  const int member = best.idx >= 0 ? cur : -1;
+  if (lane == 0) {
+    X.st.cdrop[c] = best.drop;
+    X.st.cbytes[c] = best.bytes;
+    X.st.copt[c] = best.idx;
+    X.st.mem[c] = member;
+  }
+  __syncwarp();
+  return member;
+}
+
+__device__ __forceinline__ Key leaf_key(const DevStore& st, int i, int t) {
+  Key k{0.0, 0, -1};
+  if (i < st.n && st.mem[i] == t) {
+    k.drop = st.cdrop[i];
+    k.bytes = st.cbytes[i];
+    k.idx = i;
+  }
+  return k;
+}
+
+// Recompute the path from leaf c to the root of tier t's tree (whole warp).
+__device__ void tree_update(const DevStore& st, int t, int c) {
+  const int lane = threadIdx.x & 31;
+  int* tree = st.tree + static_cast<size_t>(t) * st.tree_stride;
+  int node = c >> 5;
+  Key k = warp_min(leaf_key(st, (node << 5) + lane, t));
+  if (lane == 0) tree[st.lvl_off[0] + node] = k.idx;
+  __syncwarp();
+  for (int l = 1; l < st.nlev; ++l) {
+    node >>= 5;
+    const int i = (node << 5) + lane;
+    Key kk{0.0, 0, -1};
+    if (i < st.lvl_size[l - 1]) {
+      const int w = tree[st.lvl_off[l - 1] + i];
+      if (w >= 0) {
+        kk.drop = st.cdrop[w];
+        kk.bytes = st.cbytes[w];
+        kk.idx = w;
+      }
+    }
+    kk = warp_min(kk);
+    if (lane == 0) tree[st.lvl_off[l] + node] = kk.idx;
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ int tree_root(const DevStore& st, int t) {
+  return st.tree[static_cast<size_t>(t) * st.tree_stride + st.lvl_off[st.nlev - 1]];
+}
+
+struct Ops {
+  const int* ctx;
+  const long long* freq;  // null: use the store's saved stats (rearrange)
+  const long long* stamp;
+};
+
+// K3: persistent single-warp greedy. Processes ops[resume_op..n_ops):
+// insert_joint (placement.cpp:225-250) then resolve_overflow (206-223).
+__global__ void __launch_bounds__(32, 1) k_greedy(StepCtx X, Ops ops) {
+  const int lane = threadIdx.x;
+  DevStore& st = X.st;
+  Ctl* ctl = st.ctl;
+  const int T = st.TT.T, MR = X.S.M * X.S.R, R = X.S.R;
+  long long occ = lane < T ? ctl->occ[lane] : 0;
+  const long long capv = lane < T ? st.TT.cap[lane] : 0;
+  const bool finite = lane < T && !st.TT.unlimited[lane];
+  long long op = ctl->resume_op;
+  bool in_resolve = ctl->in_resolve != 0;
+  long long nact = ctl->n_act, seq = ctl->seq;
+  const long long cap_act = ctl->cap_act, n_ops = ctl->n_ops;
+  int status = ST_OK, err_ctx = -1, err_tier = -1;
+
+  while (true) {
+    if (!in_resolve) {
+      if (op >= n_ops) break;
+      const int c = ops.ctx[op];
+      if (st.tier[c] >= 0) {
+        status = ST_ERR_RESIDENT;
+        err_ctx = c;
+        break;
+      }
+      const kvt_best b = X.tb.best[c];
+      if (b.status != 0) {
+        status = ST_ERR_NO_CONFIG;
+        err_ctx = c;
+        break;
+      }
+      if (nact >= cap_act) {
+        status = ST_NEED_SPACE;
+        break;
+      }
+      const long long eorig = X.P.orig[c];
+      const long long sz = csize(eorig, b.ratio);
+      if (lane == b.tier_index) occ += sz;
+      if (lane == 0) {
+        st.tier[c] = b.tier_index;
+        st.meth[c] = b.method;
+        st.ridx[c] = b.ratio_index;
+        st.ratio[c] = b.ratio;
+        st.orig[c] = eorig;
+        st.freq[c] = ops.freq ? ops.freq[op] : st.freq[c];
+        st.last[c] = ops.freq ? ops.stamp[op] : st.last[c];
+        st.seq[c] = seq;
+        kvt_action a;
+        a.kind = KVT_INSERT;
+        a.ctx = c;
+        a.tier_id = b.tier_id;
+        a.method = b.method;
+        a.ratio = b.ratio;
+        st.act[nact] = a;
+      }
+      ++seq;
+      ++nact;
+      __syncwarp();
+      const int member = compute_cache(X, c, b.tier_index, b.method, b.ratio_index, b.ratio, eorig);
+      if (!st.TT.unlimited[b.tier_index]) tree_update(st, b.tier_index, c);
+      (void)member;
+      in_resolve = true;
+    }
+    // resolve_overflow: topmost over-full finite tier first (placement.cpp:54-59,211)
+    const unsigned over = __ballot_sync(0xffffffffu, finite && occ > capv);
+    if (over == 0) {
+      in_resolve = false;
+      ++op;
+      continue;
+    }
+    const int t = __ffs(over) - 1;
+    if (nact >= cap_act) {
+      status = ST_NEED_SPACE;
+      break;
+    }
+    if (ctl->errcount[t] > 0) {
+      status = ST_ERR_QUALITY;
+      err_tier = t;
+      break;
+    }
+    const int w = tree_root(st, t);
+    if (w < 0) {
+      status = ST_ERR_NO_OPTION;
+      err_tier = t;
+      break;
+    }
+    // apply the winner's cached option (placement.cpp:213-221)
+    const int e = st.copt[w];
+    const int me = st.meth[w], re = st.ridx[w];
+    const double rate = st.ratio[w];
+    const long long eorig = st.orig[w];
+    const int per = MR + 1;
+    const int j = e / per, wi = e - j * per, ti = t + j;
+    int nm, nr;
+    double nratio;
+    if (wi < MR) {
+      nm = wi / R;
+      nr = wi - nm * R;
+      nratio = X.S.ratio[nr];
+    } else {
+      nm = me;
+      nr = re;
+      nratio = rate;
+    }
+    const long long oldb = csize(eorig, rate), newb = csize(eorig, nratio);
+    if (ti == t) {
+      if (lane == t) occ += newb - oldb;
+    } else {
+      if (lane == t) occ -= oldb;
+      if (lane == ti) occ += newb;
+    }
+    if (lane == 0) {
+      st.meth[w] = nm;
+      st.ridx[w] = nr;
+      st.ratio[w] = nratio;
+      if (ti != t) {
+        st.tier[w] = ti;
+        st.seq[w] = seq;
+      }
+      kvt_action a;
+      a.kind = ti == t ? KVT_RECOMPRESS : KVT_EVICT;
+      a.ctx = w;
+      a.tier_id = st.TT.id[ti];
+      a.method = nm;
+      a.ratio = nratio;
+      st.act[nact] = a;
+    }
+    if (ti != t) ++seq;
+    ++nact;
+    __syncwarp();
+    compute_cache(X, w, ti, nm, nr, nratio, eorig);
+    tree_update(st, t, w);
+    if (ti != t && !st.TT.unlimited[ti]) tree_update(st, ti, w);
+  }
+  if (lane < T) ctl->occ[lane] = occ;
+  if (lane == 0) {
+    ctl->resume_op = op;
+    ctl->in_resolve = in_resolve ? 1 : 0;
+    ctl->n_act = nact;
+    ctl->seq = seq;
+    ctl->status = status;
+    ctl->err_ctx = err_ctx;
+    ctl->err_tier = err_tier;
+  }
+}
+
+// Rebuild every resident's cache (warp per context) after profile/space
+// changes or direct StoreState edits.
+__global__ void __launch_bounds__(128) k_rebuild_cache(StepCtx X) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= X.st.n) return;
+  const int t = X.st.tier[c];
+  if (t < 0) {
+    if ((threadIdx.x & 31) == 0) {
+      X.st.mem[c] = -1;
+      X.st.copt[c] = -1;
+    }
+    return;
+  }
+  // re-resolve the on-grid ratio index against the current space (exact ==,
+  // CompressionConfig::operator==, proj/include/kvtier/core.hpp:55-57)
+  const double rate = X.st.ratio[c];
+  int re = -1;
+  for (int r = 0; r < X.S.R; ++r)
+    if (X.S.ratio[r] == rate) re = r;
+  if ((threadIdx.x & 31) == 0) X.st.ridx[c] = re;
+  compute_cache(X, c, t, X.st.meth[c], re, rate, X.st.orig[c]);
+}
+
+// Build one tree level for every tier (warp per node).
+__global__ void __launch_bounds__(128) k_tree_level(DevStore st, int lvl) {
+  const int node = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.y;
+  if (node >= st.lvl_size[lvl]) return;
+  int* tree = st.tree + static_cast<size_t>(t) * st.tree_stride;
+  const int i = (node << 5) + lane;
+  Key k{0.0, 0, -1};
+  if (lvl == 0) {
+    k = leaf_key(st, i, t);
+  } else if (i < st.lvl_size[lvl - 1]) {
+    const int w = tree[st.lvl_off[lvl - 1] + i];
+    if (w >= 0) {
+      k.drop = st.cdrop[w];
+      k.bytes = st.cbytes[w];
+      k.idx = w;
+    }
+  }
+  k = warp_min(k);
+  if (lane == 0) tree[st.lvl_off[lvl] + node] = k.idx;
+}
+
+// Direct StoreState edits (placement.cpp:91-142); one thread.
+enum { OP_ADD, OP_REMOVE, OP_RECONF, OP_TOUCH };
+__global__ void k_store_op(DevStore st, int op, int c, kvt_entry e, kvt_entry* removed) {
+  Ctl* ctl = st.ctl;
+  ctl->status = ST_OK;
+  ctl->err_ctx = c;
+  const int t = st.tier[c];
+  if (op == OP_ADD) {
+    if (t >= 0) {
+      ctl->status = ST_ERR_RESIDENT;
+      return;
+    }
+    st.tier[c] = e.tier_index;
+    st.meth[c] = e.method;
+    st.ridx[c] = e.seq;  // host passes the resolved ratio index in seq
+    st.ratio[c] = e.ratio;
+    st.orig[c] = e.original_size_bytes;
+    st.freq[c] = e.frequency;
+    st.last[c] = e.last_access;
+    st.seq[c] = ctl->seq++;
+    ctl->occ[e.tier_index] += csize(e.original_size_bytes, e.ratio);
+    return;
+  }
+  if (t < 0) {
+    ctl->status = ST_ERR_NOT_RESIDENT;
+    return;
+  }
+  if (op == OP_REMOVE) {
+    removed->tier_index = t;
+    removed->method = st.meth[c];
+    removed->ratio = st.ratio[c];
+    removed->original_size_bytes = st.orig[c];
+    removed->frequency = st.freq[c];
+    removed->last_access = st.last[c];
+    removed->seq = st.seq[c];
+    ctl->occ[t] -= csize(st.orig[c], st.ratio[c]);
+    st.tier[c] = -1;
+    st.mem[c] = -1;
+  } else if (op == OP_RECONF) {
+    ctl->occ[t] += csize(st.orig[c], e.ratio) - csize(st.orig[c], st.ratio[c]);
+    st.meth[c] = e.method;
+    st.ratio[c] = e.ratio;
+    st.ridx[c] = e.seq;
+  } else {
+    st.freq[c] += 1;
+    st.last[c] = e.last_access;
+  }
+}
+
+// least_drop_update query: the root of tier t with its option spelled out.
+__global__ void k_ld_query(StepCtx X, int t, kvt_update* out) {
+  const DevStore& st = X.st;
+  Ctl* ctl = st.ctl;
+  ctl->status = ST_OK;
+  if (ctl->errcount[t] > 0) {
+    ctl->status = ST_ERR_QUALITY;
+    ctl->err_tier = t;
+    return;
+  }
+  const int w = tree_root(st, t);
+  if (w < 0) {
+    ctl->status = ST_ERR_NO_OPTION;
+    ctl->err_tier = t;
+    return;
+  }
+  const int MR = X.S.M * X.S.R, R = X.S.R;
+  const int e = st.copt[w], per = MR + 1, j = e / per, wi = e - j * per, ti = t + j;
+  int nm;
+  double nratio;
+  if (wi < MR) {
+    nm = wi / R;
+    nratio = X.S.ratio[wi - nm * R];
+  } else {
+    nm = st.meth[w];
+    nratio = st.ratio[w];
+  }
+  kvt_update u = {};
+  u.ctx = w;
+  u.kind = ti == t ? KVT_RECOMPRESS : KVT_EVICT;
+  u.tier_index = ti;
+  u.tier_id = st.TT.id[ti];
+  u.method = nm;
+  u.ratio = nratio;
+  long long sz = 0;
+  score_fly(X, w, ti, nm, nratio, &u.utility, &sz, &u.quality, &u.ttft);
+  u.size_bytes = sz;
+  u.utility_drop = st.cdrop[w];
+  u.bytes_freed = st.cbytes[w];
+  *out = u;
+}
+
+// rearrange (placement.cpp:252-283) sort keys: utility descending, then
+// context ascending (stable radix sort over contexts in index order).
+__global__ void k_rearrange_keys(DevStore st, const kvt_best* best, unsigned long long* keys, int* vals) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= st.n) return;
+  vals[c] = c;
+  if (st.tier[c] < 0) {
+    keys[c] = ~0ull;
+    return;
+  }
+  if (best[c].status != 0) {
+    st.ctl->status = ST_ERR_NO_CONFIG;
+    st.ctl->err_ctx = c;
+  }
+  double u = best[c].utility;
+  if (u == 0.0) u = 0.0;  // -0.0 == +0.0 in the reference's comparator
+  unsigned long long b = __double_as_longlong(u);
+  b = (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);  // ascending order key
+  keys[c] = ~b;  // descending utility
+  atomicAdd(&st.ctl->n_saved, 1);
+}
+
+__global__ void k_clear(DevStore st) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < st.n) {
+    st.tier[c] = -1;
+    st.mem[c] = -1;
+    st.copt[c] = -1;
+  }
+  if (c < KVT_MAX_TIERS) {
+    st.ctl->occ[c] = 0;
+    st.ctl->errcount[c] = 0;
+  }
+}
+
+// placement_utility (placement.cpp:285-298): per-resident utility, then an
+// ordered (tier, arrival) sum by one thread so the FP sum order matches.
+__global__ void k_util_terms(StepCtx X, double* term, unsigned long long* keys, int* vals, int* bad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= X.st.n) return;
+  vals[c] = c;
+  const int t = X.st.tier[c];
+  if (t < 0) {
+    keys[c] = ~0ull;
+    term[c] = 0.0;
+    return;
+  }
+  // occupancy-side size uses the entry's size (CacheEntry::compressed_bytes)
+  double q;
+  if (!quality_of(X.P, c, X.st.meth[c], X.st.ratio[c], &q)) {
+    *bad = c + 1;
+    term[c] = 0.0;
+  } else {
+    const long long sz = csize(X.st.orig[c], X.st.ratio[c]);
+    const double tt = load_time(sz, X.st.TT.lat[t], X.st.TT.bw[t], X.S.ovh[X.st.meth[c]]);
+    term[c] = utility_score(q, tt, X.P.freq[c], X.alpha);
+  }
+  keys[c] = (static_cast<unsigned long long>(t) << 56) | static_cast<unsigned long long>(X.st.seq[c]);
+}
+
+__global__ void k_util_sum(const double* term, const int* order, int n_res, double* out) {
+  double total = 0.0;
+  for (int i = 0; i < n_res; ++i) total = __dadd_rn(total, term[order[i]]);
+  *out = total;
+}
+
+struct kvt_store {
+  kvt_handle* h = nullptr;
+  DevStore d{};
+  DevTiers TT{};
+  int n = 0;
+  void* buf = nullptr;
+  // tables for this store's tiers
+  void* tbuf = nullptr;
+  size_t tbytes = 0;
+  Tables tb{};
+  uint64_t tkey = 0;
+  bool cache_dirty = true;
+  uint64_t cache_key = 0;
+  long long cap_act = 0;
+  kvt_action* act = nullptr;
+  int* ops_buf = nullptr;
+  long long* ops_l = nullptr;
+  long long ops_cap = 0;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  std::vector<std::string> names;
+  bool has_space = false;
+  DevSpace S{};
+};
+
+static int store_fetch_ctl(kvt_store* s, Ctl* c) {
+  KVT_CUDA_TRY(cudaMemcpyAsync(c, s->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->h->stream));
+  KVT_CUDA_TRY(cudaStreamSynchronize(s->h->stream));
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_tiers, int32_t n_ctx,
+                                kvt_store** out) {
+  DevTiers T;
+  int rc;
+  if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
+  if (n_ctx < 0) return set_error(KVT_EINVAL, "negative context count");
+  auto* s = new kvt_store();
+  s->h = h;
+  s->TT = T;
+  s->n = n_ctx;
+  DevStore& d = s->d;
+  d.n = n_ctx;
+  d.TT = T;
+  // tree levels
+  int sz = std::max(1, (n_ctx + 31) / 32), nl = 0, off = 0;
+  while (true) {
+    d.lvl_off[nl] = off;
+    d.lvl_size[nl] = sz;
+    off += sz;
+    ++nl;
+    if (sz == 1) break;
+    sz = (sz + 31) / 32;
+  }
+  d.nlev = nl;
+  d.tree_stride = off;
+  const size_t n = std::max(1, n_ctx);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t o = 0;
+  auto carve = [&](size_t bytes) {
+    size_t at = o;
+    o += align(bytes);
+    return at;
+  };
+  const size_t o_tier = carve(4 * n), o_meth = carve(4 * n), o_ridx = carve(4 * n), o_ratio = carve(8 * n),
+               o_orig = carve(8 * n), o_freq = carve(8 * n), o_last = carve(8 * n), o_seq = carve(8 * n),
+               o_cdrop = carve(8 * n), o_cbytes = carve(8 * n), o_copt = carve(4 * n), o_mem = carve(4 * n),
+               o_tree = carve(4 * static_cast<size_t>(off) * T.T), o_ctl = carve(sizeof(Ctl)),
+               o_saved = carve(4 * n);
+  cudaError_t e = cudaMalloc(&s->buf, o);
+  if (e != cudaSuccess) {
+    delete s;
+    return set_error(KVT_ECUDA, std::string("cudaMalloc store: ") + cudaGetErrorString(e));
+  }
+  char* b = static_cast<char*>(s->buf);
+  d.tier = reinterpret_cast<int*>(b + o_tier);
+  d.meth = reinterpret_cast<int*>(b + o_meth);
+  d.ridx = reinterpret_cast<int*>(b + o_ridx);
+  d.ratio = reinterpret_cast<double*>(b + o_ratio);
+  d.orig = reinterpret_cast<long long*>(b + o_orig);
+  d.freq = reinterpret_cast<long long*>(b + o_freq);
+  d.last = reinterpret_cast<long long*>(b + o_last);
+  d.seq = reinterpret_cast<long long*>(b + o_seq);
+  d.cdrop = reinterpret_cast<double*>(b + o_cdrop);
+  d.cbytes = reinterpret_cast<long long*>(b + o_cbytes);
+  d.copt = reinterpret_cast<int*>(b + o_copt);
+  d.mem = reinterpret_cast<int*>(b + o_mem);
+  d.tree = reinterpret_cast<int*>(b + o_tree);
+  d.ctl = reinterpret_cast<Ctl*>(b + o_ctl);
+  d.saved = reinterpret_cast<int*>(b + o_saved);
+  cudaStream_t st = h->stream;
+  cudaMemsetAsync(s->buf, 0, o, st);
+  cudaMemsetAsync(d.tier, 0xff, 4 * n, st);
+  cudaMemsetAsync(d.mem, 0xff, 4 * n, st);
+  cudaMemsetAsync(d.copt, 0xff, 4 * n, st);
+  cudaMemsetAsync(d.tree, 0xff, 4 * static_cast<size_t>(off) * T.T, st);
+  s->cap_act = 4096;
+  e = cudaMalloc(&s->act, sizeof(kvt_action) * s->cap_act);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(s->buf);
+    delete s;
+    return set_error(KVT_ECUDA, std::string("store init: ") + cudaGetErrorString(e));
+  }
+  d.act = s->act;
+  *out = s;
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_destroy(kvt_store* s) {
+  if (!s) return KVT_OK;
+  cudaFree(s->buf);
+  cudaFree(s->tbuf);
+  cudaFree(s->act);
+  cudaFree(s->ops_buf);
+  cudaFree(s->ops_l);
+  cudaFree(s->sort_tmp);
+  delete s;
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_bind_space(kvt_store* s, const kvt_space* space) {
+  DevSpace S;
+  int rc;
+  if ((rc = resolve_space(space, &S))) return rc;
+  s->S = S;
+  s->has_space = true;
+  return KVT_OK;
+}
+
+static int ratio_index(const kvt_store* s, double ratio) {
+  if (!s->has_space) return -1;
+  for (int r = 0; r < s->S.R; ++r)
+    if (s->S.ratio[r] == ratio) return r;
+  return -1;
+}
+
+static int store_status_error(kvt_store* s, const Ctl& c) {
+  const std::string ctx = std::to_string(c.err_ctx);
+  switch (c.status) {
+    case ST_OK:
+      return KVT_OK;
+    case ST_ERR_RESIDENT:
+      return set_error(KVT_EVALIDATION, "context " + ctx + " is already resident");
+    case ST_ERR_NO_CONFIG:
+      return set_error(KVT_EVALIDATION, "no scorable configuration for context " + ctx);
+    case ST_ERR_NO_OPTION:
+      return set_error(KVT_EVALIDATION, "tier " + std::to_string(s->TT.id[c.err_tier]) +
+                                            " is over capacity and no resident has a space-saving option");
+    case ST_ERR_QUALITY:
+      return set_error(KVT_EVALIDATION, "a resident of tier " + std::to_string(s->TT.id[c.err_tier]) +
+                                            " has a configuration its profile cannot score");
+    case ST_ERR_NOT_RESIDENT:
+      return set_error(KVT_EVALIDATION, "context " + ctx + " is not resident");
+    default:
+      return set_error(KVT_EINVAL, "store kernel status " + std::to_string(c.status));
+  }
+}
+
+static int run_store_op(kvt_store* s, int op, int c, const kvt_entry& e, kvt_entry* removed) {
+  if (c < 0 || c >= s->n) return set_error(KVT_EINVAL, "context index out of range");
+  kvt_entry* d_removed = nullptr;
+  if (removed) KVT_CUDA_TRY(cudaMallocAsync(&d_removed, sizeof(kvt_entry), s->h->stream));
+  k_store_op<<<1, 1, 0, s->h->stream>>>(s->d, op, c, e, d_removed);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  if (removed) {
+    KVT_CUDA_TRY(cudaMemcpyAsync(removed, d_removed, sizeof(kvt_entry), cudaMemcpyDeviceToHost, s->h->stream));
+    KVT_CUDA_TRY(cudaFreeAsync(d_removed, s->h->stream));
+  }
+  Ctl c2;
+  int rc = store_fetch_ctl(s, &c2);
+  if (rc) return rc;
+  if (op != OP_TOUCH) s->cache_dirty = true;
+  return store_status_error(s, c2);
+}
+
+extern "C" int kvt_store_add(kvt_store* s, int32_t ctx, const kvt_entry* e) {
+  if (e->tier_index < 0 || e->tier_index >= s->TT.T)
+    return set_error(KVT_EVALIDATION, "unknown tier index " + std::to_string(e->tier_index));
+  if (e->original_size_bytes <= 0) return set_error(KVT_EVALIDATION, "original size must be > 0");
+  if (!(e->ratio > 0.0) || e->ratio > 1.0 || !std::isfinite(e->ratio))
+    return set_error(KVT_EVALIDATION, "compression ratio must be in (0, 1]");
+  if (s->has_space && (e->method < 0 || e->method >= s->S.M))
+    return set_error(KVT_EVALIDATION, "unknown compression method index");
+  kvt_entry x = *e;
+  x.seq = ratio_index(s, e->ratio);
+  return run_store_op(s, OP_ADD, ctx, x, nullptr);
+}
+
+extern "C" int kvt_store_remove(kvt_store* s, int32_t ctx, kvt_entry* removed) {
+  kvt_entry x{};
+  kvt_entry tmp{};
+  return run_store_op(s, OP_REMOVE, ctx, x, removed ? removed : &tmp);
+}
+
+extern "C" int kvt_store_reconfigure(kvt_store* s, int32_t ctx, int32_t m, double ratio) {
+  if (!(ratio > 0.0) || ratio > 1.0 || !std::isfinite(ratio))
+    return set_error(KVT_EVALIDATION, "compression ratio must be in (0, 1]");
+  kvt_entry x{};
+  x.method = m;
+  x.ratio = ratio;
+  x.seq = ratio_index(s, ratio);
+  return run_store_op(s, OP_RECONF, ctx, x, nullptr);
+}
+
+extern "C" int kvt_store_touch(kvt_store* s, int32_t ctx, int64_t stamp) {
+  kvt_entry x{};
+  x.last_access = stamp;
+  return run_store_op(s, OP_TOUCH, ctx, x, nullptr);
+}
+
+extern "C" int kvt_store_clear(kvt_store* s) {
+  k_clear<<<(s->n + 255) / 256 + 1, 256, 0, s->h->stream>>>(s->d);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  KVT_CUDA_TRY(cudaMemsetAsync(s->d.tree, 0xff, 4 * static_cast<size_t>(s->d.tree_stride) * s->TT.T, s->h->stream));
+  KVT_CUDA_TRY(cudaStreamSynchronize(s->h->stream));
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_occupancy(kvt_store* s, int64_t* occ) {
+  Ctl c;
+  int rc = store_fetch_ctl(s, &c);
+  if (rc) return rc;
+  for (int t = 0; t < s->TT.T; ++t) occ[t] = c.occ[t];
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_snapshot(kvt_store* s, kvt_entry* out) {
+  const size_t n = s->n;
+  std::vector<int> tier(n), meth(n);
+  std::vector<double> ratio(n);
+  std::vector<long long> orig(n), freq(n), last(n), seq(n);
+  cudaStream_t st = s->h->stream;
+  if (n) {
+    KVT_CUDA_TRY(cudaMemcpyAsync(tier.data(), s->d.tier, 4 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(meth.data(), s->d.meth, 4 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(ratio.data(), s->d.ratio, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(orig.data(), s->d.orig, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(freq.data(), s->d.freq, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(last.data(), s->d.last, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(seq.data(), s->d.seq, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  for (size_t c = 0; c < n; ++c) {
+    kvt_entry& e = out[c];
+    std::memset(&e, 0, sizeof e);
+    e.tier_index = tier[c];
+    if (tier[c] < 0) continue;
+    e.method = meth[c];
+    e.ratio = ratio[c];
+    e.original_size_bytes = orig[c];
+    e.frequency = freq[c];
+    e.last_access = last[c];
+    e.seq = seq[c];
+  }
+  return KVT_OK;
+}
+
+extern "C" int kvt_store_actions(kvt_store* s, kvt_action* out, int64_t n) {
+  Ctl c;
+  int rc = store_fetch_ctl(s, &c);
+  if (rc) return rc;
+  if (n > c.n_act) n = c.n_act;
+  if (n > 0) {
+    KVT_CUDA_TRY(cudaMemcpyAsync(out, s->act, sizeof(kvt_action) * n, cudaMemcpyDeviceToHost, s->h->stream));
+    KVT_CUDA_TRY(cudaStreamSynchronize(s->h->stream));
+  }
+  return KVT_OK;
+}
+
+// Make the store's candidate tables and resident caches current for
+// (profiles, space, params, rule).
+static int prepare(kvt_store* s, const kvt_pset* p, const kvt_space* space, const kvt_params* params, int rule,
+                   StepCtx* X) {
+  DevSpace S;
+  int rc;
+  if ((rc = resolve_space(space, &S))) return rc;
+  if (p->dev.M != S.M) return set_error(KVT_EINVAL, "profile set / space method count mismatch");
+  if (p->dev.n != s->n) return set_error(KVT_EINVAL, "profile set and store disagree on the context count");
+  s->S = S;
+  s->has_space = true;
+  uint64_t key = fnv(&S, sizeof S);
+  key = fnv(&p->id, sizeof p->id, key);
+  key = fnv(&params->alpha, sizeof(double), key);
+  uint64_t tkey = fnv(&rule, sizeof rule, key);
+  cudaStream_t st = s->h->stream;
+  const size_t n = std::max(1, s->n), R = S.R, MR = S.M * S.R, TMR = s->TT.T * MR;
+  if (tkey != s->tkey) {
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t b_size = align(n * R * 8), b_q = align(n * MR * 8), b_v = align(n * MR), b_u = align(n * TMR * 8),
+                 b_best = align(n * sizeof(kvt_best));
+    const size_t need = b_size + b_q + b_v + b_u + b_best;
+    if (need > s->tbytes) {
+      cudaFree(s->tbuf);
+      s->tbuf = nullptr;
+      s->tbytes = 0;
+      KVT_CUDA_TRY(cudaMalloc(&s->tbuf, need));
+      s->tbytes = need;
+    }
+    char* b = static_cast<char*>(s->tbuf);
+    s->tb = Tables{reinterpret_cast<long long*>(b), reinterpret_cast<double*>(b + b_size),
+                   reinterpret_cast<unsigned char*>(b + b_size + b_q), nullptr,
+                   reinterpret_cast<double*>(b + b_size + b_q + b_v),
+                   reinterpret_cast<kvt_best*>(b + b_size + b_q + b_v + b_u)};
+    if ((rc = launch_score(s->h, p->dev, S, s->TT, params->alpha, rule, s->tb))) return rc;
+    s->tkey = tkey;
+  }
+  X->st = s->d;
+  X->P = p->dev;
+  X->S = S;
+  X->alpha = params->alpha;
+  X->tb = s->tb;
+  if (s->cache_dirty || s->cache_key != key) {
+    // errcount reset + per-resident cache + trees bottom-up
+    KVT_CUDA_TRY(cudaMemsetAsync(s->d.ctl->errcount, 0, sizeof(int) * KVT_MAX_TIERS, st));
+    if (s->n) {
+      k_rebuild_cache<<<(s->n * 32 + 127) / 128, 128, 0, st>>>(*X);
+      s->h->launches++;
+      for (int l = 0; l < s->d.nlev; ++l) {
+        dim3 grid((s->d.lvl_size[l] * 32 + 127) / 128, s->TT.T);
+        k_tree_level<<<grid, 128, 0, st>>>(s->d, l);
+        s->h->launches++;
+      }
+    }
+    KVT_CUDA_TRY(cudaGetLastError());
+    s->cache_dirty = false;
+    s->cache_key = key;
+  }
+  return KVT_OK;
+}
+
+// Run the persistent greedy over `n_ops` ops already staged on the device,
+// growing the action buffer when the kernel asks for it.
+static int run_greedy(kvt_store* s, StepCtx& X, Ops ops, long long n_ops, int64_t* n_actions, int64_t* n_done) {
+  cudaStream_t st = s->h->stream;
+  Ctl init{};
+  {
+    Ctl cur;
+    int rc = store_fetch_ctl(s, &cur);
+    if (rc) return rc;
+    init = cur;
+  }
+  init.n_act = 0;
+  init.n_ops = n_ops;
+  init.resume_op = 0;
+  init.in_resolve = n_ops < 0 ? 1 : 0;  // resolve-only call
+  if (n_ops < 0) init.n_ops = 1;        // one pseudo op: the resolve
+  init.status = ST_OK;
+  long long need = std::max<long long>(4096, 8 * (init.n_ops + 16));
+  if (need > s->cap_act) {
+    cudaFree(s->act);
+    s->act = nullptr;
+    KVT_CUDA_TRY(cudaMalloc(&s->act, sizeof(kvt_action) * need));
+    s->cap_act = need;
+    s->d.act = s->act;
+  }
+  init.cap_act = s->cap_act;
+  KVT_CUDA_TRY(cudaMemcpyAsync(s->d.ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  Ctl c;
+  while (true) {
+    X.st = s->d;
+    k_greedy<<<1, 32, 0, st>>>(X, ops);
+    s->h->launches++;
+    KVT_CUDA_TRY(cudaGetLastError());
+    int rc = store_fetch_ctl(s, &c);
+    if (rc) return rc;
+    if (c.status != ST_NEED_SPACE) break;
+    const long long ncap = s->cap_act * 2;
+    kvt_action* na = nullptr;
+    KVT_CUDA_TRY(cudaMalloc(&na, sizeof(kvt_action) * ncap));
+    KVT_CUDA_TRY(cudaMemcpyAsync(na, s->act, sizeof(kvt_action) * c.n_act, cudaMemcpyDeviceToDevice, st));
+    KVT_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(s->act);
+    s->act = na;
+    s->cap_act = ncap;
+    s->d.act = na;
+    c.cap_act = ncap;
+    c.status = ST_OK;
+    KVT_CUDA_TRY(cudaMemcpyAsync(s->d.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  }
+  *n_actions = c.n_act;
+  if (n_done) *n_done = n_ops < 0 ? 0 : (c.in_resolve ? c.resume_op : c.resume_op);
+  return store_status_error(s, c);
+}
+
+static int stage_ops(kvt_store* s, const int32_t* ctx, const int64_t* freq, const int64_t* stamp, long long n) {
+  if (n > s->ops_cap) {
+    cudaFree(s->ops_buf);
+    cudaFree(s->ops_l);
+    s->ops_buf = nullptr;
+    s->ops_l = nullptr;
+    KVT_CUDA_TRY(cudaMalloc(&s->ops_buf, 4 * n));
+    KVT_CUDA_TRY(cudaMalloc(&s->ops_l, 16 * n));
+    s->ops_cap = n;
+  }
+  cudaStream_t st = s->h->stream;
+  for (long long i = 0; i < n; ++i)
+    if (ctx[i] < 0 || ctx[i] >= s->n) return set_error(KVT_EINVAL, "context index out of range");
+  KVT_CUDA_TRY(cudaMemcpyAsync(s->ops_buf, ctx, 4 * n, cudaMemcpyHostToDevice, st));
+  if (freq) KVT_CUDA_TRY(cudaMemcpyAsync(s->ops_l, freq, 8 * n, cudaMemcpyHostToDevice, st));
+  else KVT_CUDA_TRY(cudaMemsetAsync(s->ops_l, 0, 8 * n, st));
+  if (stamp) KVT_CUDA_TRY(cudaMemcpyAsync(s->ops_l + n, stamp, 8 * n, cudaMemcpyHostToDevice, st));
+  else KVT_CUDA_TRY(cudaMemsetAsync(s->ops_l + n, 0, 8 * n, st));
+  return KVT_OK;
+}
+
+extern "C" int kvt_insert_joint(kvt_store* s, const kvt_pset* p, const kvt_space* space, const kvt_params* params,
+                                int32_t rule, const int32_t* ctx, const int64_t* frequency, const int64_t* stamp,
+                                int64_t n_ops, int64_t* n_actions, int64_t* n_done) {
+  *n_actions = 0;
+  *n_done = 0;
+  StepCtx X;
+  int rc;
+  if ((rc = prepare(s, p, space, params, rule, &X))) return rc;
+  if (n_ops <= 0) return KVT_OK;
+  if ((rc = stage_ops(s, ctx, frequency, stamp, n_ops))) return rc;
+  Ops ops{s->ops_buf, s->ops_l, s->ops_l + n_ops};
+  return run_greedy(s, X, ops, n_ops, n_actions, n_done);
+}
+
+extern "C" int kvt_resolve_overflow(kvt_store* s, const kvt_pset* p, const kvt_space* space,
+                                    const kvt_params* params, int64_t* n_actions) {
+  StepCtx X;
+  int rc;
+  *n_actions = 0;
+  if ((rc = prepare(s, p, space, params, KVT_RULE_UTILITY, &X))) return rc;
+  Ops ops{s->d.saved, nullptr, nullptr};
+  return run_greedy(s, X, ops, -1, n_actions, nullptr);
+}
+
+extern "C" int kvt_least_drop_update(kvt_store* s, const kvt_pset* p, const kvt_space* space,
+                                     const kvt_params* params, int32_t tier_index, kvt_update* out) {
+  StepCtx X;
+  int rc;
+  if (tier_index < 0 || tier_index >= s->TT.T) return set_error(KVT_EINVAL, "tier index out of range");
+  if ((rc = prepare(s, p, space, params, KVT_RULE_UTILITY, &X))) return rc;
+  kvt_update* d_u = nullptr;
+  KVT_CUDA_TRY(cudaMallocAsync(&d_u, sizeof(kvt_update), s->h->stream));
+  k_ld_query<<<1, 1, 0, s->h->stream>>>(X, tier_index, d_u);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  KVT_CUDA_TRY(cudaMemcpyAsync(out, d_u, sizeof(kvt_update), cudaMemcpyDeviceToHost, s->h->stream));
+  KVT_CUDA_TRY(cudaFreeAsync(d_u, s->h->stream));
+  Ctl c;
+  if ((rc = store_fetch_ctl(s, &c))) return rc;
+  return store_status_error(s, c);
+}
+
+static int ensure_sort_tmp(kvt_store* s, size_t bytes) {
+  if (bytes <= s->sort_tmp_bytes) return KVT_OK;
+  cudaFree(s->sort_tmp);
+  s->sort_tmp = nullptr;
+  KVT_CUDA_TRY(cudaMalloc(&s->sort_tmp, bytes));
+  s->sort_tmp_bytes = bytes;
+  return KVT_OK;
+}
+
+// keys/vals double buffers for the radix sorts (n each)
+static int sort_pairs(kvt_store* s, unsigned long long* k_in, unsigned long long* k_out, int* v_in, int* v_out,
+                      int n) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in, k_out, v_in, v_out, n, 0, 64, s->h->stream);
+  int rc = ensure_sort_tmp(s, tmp);
+  if (rc) return rc;
+  KVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(s->sort_tmp, tmp, k_in, k_out, v_in, v_out, n, 0, 64, s->h->stream));
+  s->h->launches += 4;
+  return KVT_OK;
+}
+
+extern "C" int kvt_rearrange(kvt_store* s, const kvt_pset* p, const kvt_space* space, const kvt_params* params,
+                             int32_t rule, int64_t* n_actions) {
+  StepCtx X;
+  int rc;
+  *n_actions = 0;
+  if ((rc = prepare(s, p, space, params, rule, &X))) return rc;
+  if (s->n == 0) return KVT_OK;
+  cudaStream_t st = s->h->stream;
+  const size_t n = s->n;
+  char* tmp = nullptr;
+  KVT_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * 24 + 1024, st));
+  auto* k_in = reinterpret_cast<unsigned long long*>(tmp);
+  auto* k_out = k_in + n;
+  auto* v_in = reinterpret_cast<int*>(k_out + n);
+  Ctl c;
+  if ((rc = store_fetch_ctl(s, &c))) return rc;
+  c.n_saved = 0;
+  c.status = ST_OK;
+  KVT_CUDA_TRY(cudaMemcpyAsync(s->d.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+  k_rearrange_keys<<<(s->n + 255) / 256, 256, 0, st>>>(s->d, s->tb.best, k_in, v_in);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  if ((rc = sort_pairs(s, k_in, k_out, v_in, s->d.saved, s->n))) return rc;
+  if ((rc = store_fetch_ctl(s, &c))) return rc;
+  cudaFreeAsync(tmp, st);
+  if (c.status != ST_OK) return store_status_error(s, c);
+  const int n_saved = c.n_saved;
+  // store.clear() then re-insert in saved order, keeping access stats
+  k_clear<<<(s->n + 255) / 256 + 1, 256, 0, st>>>(s->d);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaMemsetAsync(s->d.tree, 0xff, 4 * static_cast<size_t>(s->d.tree_stride) * s->TT.T, st));
+  KVT_CUDA_TRY(cudaGetLastError());
+  Ops ops{s->d.saved, nullptr, nullptr};
+  if (n_saved == 0) return KVT_OK;
+  return run_greedy(s, X, ops, n_saved, n_actions, nullptr);
+}
+
+extern "C" int kvt_placement_utility(kvt_store* s, const kvt_pset* p, const kvt_space* space,
+                                     const kvt_params* params, double* out) {
+  StepCtx X;
+  int rc;
+  if ((rc = prepare(s, p, space, params, KVT_RULE_UTILITY, &X))) return rc;
+  *out = 0.0;
+  if (s->n == 0) return KVT_OK;
+  cudaStream_t st = s->h->stream;
+  const size_t n = s->n;
+  char* tmp = nullptr;
+  KVT_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * 36 + 2048, st));
+  auto* term = reinterpret_cast<double*>(tmp);
+  auto* k_in = reinterpret_cast<unsigned long long*>(term + n);
+  auto* k_out = k_in + n;
+  auto* v_in = reinterpret_cast<int*>(k_out + n);
+  auto* v_out = v_in + n;
+  auto* bad = v_out + n;
+  auto* d_out = reinterpret_cast<double*>(bad + 2);
+  KVT_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  k_util_terms<<<(s->n + 255) / 256, 256, 0, st>>>(X, term, k_in, v_in, bad);
+  s->h->launches++;
+  if ((rc = sort_pairs(s, k_in, k_out, v_in, v_out, s->n))) return rc;
+  Ctl c;
+  if ((rc = store_fetch_ctl(s, &c))) return rc;
+  int n_res = 0;
+  {
+    // number of residents = contexts with a tier; count on host from keys
+    std::vector<unsigned long long> keys(n);
+    KVT_CUDA_TRY(cudaMemcpyAsync(keys.data(), k_out, 8 * n, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaStreamSynchronize(st));
+    while (n_res < s->n && keys[n_res] != ~0ull) ++n_res;
+  }
+  k_util_sum<<<1, 1, 0, st>>>(term, v_out, n_res, d_out);
+  s->h->launches++;
+  int h_bad = 0;
+  KVT_CUDA_TRY(cudaMemcpyAsync(out, d_out, sizeof(double), cudaMemcpyDeviceToHost, st));
+  KVT_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KVT_CUDA_TRY(cudaFreeAsync(tmp, st));
+  KVT_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_bad) return set_error(KVT_EVALIDATION, "resident " + std::to_string(h_bad - 1) +
+                                                   " has a configuration its profile cannot score");
+  return KVT_OK;
+}

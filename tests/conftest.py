@@ -38,7 +38,7 @@ def oracle_abi():
     from paper_2512_14946_b200 import _abi
     if not os.path.exists(ORACLE_LIB):
         pytest.fail("oracle/liboracle.so missing: run make -C oracle")
-    return _abi.Abi(ORACLE_LIB, "orc_", codec=False)
+    return _abi.Abi(ORACLE_LIB, "orc_", codec=True)
 
 
 @pytest.fixture(scope="session")

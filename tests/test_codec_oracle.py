@@ -1,0 +1,186 @@
+"""Pins the codec oracle (oracle/orc_codec.c). The reference has no codec, so
+parity is UNPINNED against the reference; the oracle is instead checked
+against known answers derived from the spec and an independent numpy
+restatement (tests/codec_ref.py)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2512_14946_b200 import _abi as A
+
+import codec_ref as R
+
+
+def shape(L, H, T, D=128):
+    return A.KvShape(L, H, T, D)
+
+
+def plan(abi, method, ratio, s):
+    cfg = A.CodecCfg()
+    abi.check(abi.codec_plan(method.encode(), ratio, C.byref(s), C.byref(cfg)))
+    return cfg
+
+
+@pytest.fixture(scope="module")
+def lib(oracle_abi):
+    L = oracle_abi.lib
+    L.orc_f2h.restype = C.c_uint16
+    L.orc_f2h.argtypes = [C.c_float]
+    L.orc_h2f.restype = C.c_float
+    L.orc_h2f.argtypes = [C.c_uint16]
+    L.orc_f2bf.restype = C.c_uint16
+    L.orc_f2bf.argtypes = [C.c_float]
+    return oracle_abi
+
+
+def test_half_and_bf16_rounding_match_numpy_torch(lib):
+    import torch
+    rng = np.random.default_rng(0)
+    vals = np.concatenate([
+        rng.standard_normal(3000).astype(np.float32) * np.float32(2.0) ** rng.integers(-30, 18, 3000).astype(np.float32),
+        np.array([0.0, -0.0, 65504, 65519.99, 65520, 1e-8, 5.96e-8, 2.98e-8, 6.1e-5, -3.3e-6, 1 / 3], np.float32)])
+    for v in vals:
+        h = lib.lib.orc_f2h(float(v))
+        assert h == np.float32(v).astype(np.float16).view(np.uint16), v
+        assert lib.lib.orc_h2f(h) == np.float16(np.uint16(h).view(np.float16)).astype(np.float32) or np.isnan(v)
+    t = torch.tensor(vals).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    for v, want in zip(vals, t):
+        assert lib.lib.orc_f2bf(float(v)) == want
+
+
+def test_codec_plan_known_answers(lib):
+    s = shape(32, 8, 8192)
+    c = plan(lib, "knorm", 0.4, s)  # bf16 token drop, keep 0.4
+    assert (c.scorer, c.bits, c.keep) == (A.KVT_SCORER_KNORM, 16, 3277)
+    c = plan(lib, "keydiff-q4", 0.2, s)  # 4-bit: eff 0.265625 -> keep 0.7529
+    assert (c.scorer, c.bits, c.keep) == (A.KVT_SCORER_KEYDIFF, 4, int(np.floor(0.2 / 0.265625 * 8192 + 0.5)))
+    c = plan(lib, "keydiff-q4", 0.4, s)  # too big for 4 bits -> 8 bits
+    assert c.bits == 8 and c.keep == int(np.floor(0.4 / (0.5 + 1 / 64) * 8192 + 0.5))
+    c = plan(lib, "snapkv-q2", 0.9, s)  # -> bf16
+    assert c.bits == 16 and c.keep == int(np.floor(0.9 * 8192 + 0.5))
+    c = plan(lib, "snapkv", 0.0001, s)  # snapkv keeps at least its window
+    assert c.keep == 32 and c.window == 32
+    c = plan(lib, "knorm-q8", 1.0, s)
+    assert c.bits == 16 and c.keep == 8192
+    with pytest.raises(A.ValidationError):
+        plan(lib, "h2o", 0.5, s)
+    with pytest.raises(A.ValidationError):
+        plan(lib, "knorm-q3", 0.5, s)
+
+
+def test_blob_layout_sizes(lib):
+    s = shape(2, 2, 300)
+    for method, ratio in [("knorm-q4", 0.2), ("knorm-q8", 0.3), ("knorm-q2", 0.1), ("knorm", 0.5)]:
+        c = plan(lib, method, ratio, s)
+        m = A.BlobMap()
+        lib.check(lib.blob_layout(C.byref(s), C.byref(c), C.byref(m)))
+        S, k, b = 4, c.keep, c.bits
+        assert m.idx_bytes == 4 * S * k
+        if b == 16:
+            assert m.kcode_bytes == m.vcode_bytes == 2 * S * k * 128
+        else:
+            ng = -(-k // 128)
+            assert m.kcode_bytes == S * k * 128 * b // 8
+            assert m.kparam_bytes == 2 * S * ng * 128 and m.vparam_bytes == 2 * S * k
+        assert m.total_bytes % 256 == 0
+
+
+def test_kv_generate_matches_numpy(lib):
+    s = shape(2, 3, 17)
+    k = np.zeros((2, 3, 17, 128), np.uint16)
+    v = np.zeros_like(k)
+    lib.check(lib.kv_generate(None, C.byref(s), 11, 5, A.ptr(k), A.ptr(v)))
+    rk, rv = R.gen_kv(2, 3, 17, 128, 11, 5)
+    assert np.array_equal(k, rk) and np.array_equal(v, rv)
+    assert np.isfinite(R.bf2f(k)).all()
+
+
+def _kv(L, H, T, seed=3, ctx=1):
+    return R.gen_kv(L, H, T, 128, seed, ctx)
+
+
+def _scores(lib, s, cfg, k):
+    out = np.zeros((s.L, s.H, s.T), np.float32)
+    lib.check(lib.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+    return out
+
+
+def test_knorm_scores_exact(lib):
+    s = shape(2, 2, 200)
+    k, _ = _kv(2, 2, 200)
+    got = _scores(lib, s, plan(lib, "knorm", 0.5, s), k)
+    assert np.array_equal(got, R.knorm_scores(k))
+
+
+def test_keydiff_scores_track_cosine_similarity(lib):
+    s = shape(1, 2, 300)
+    k, _ = _kv(1, 2, 300)
+    got = _scores(lib, s, plan(lib, "keydiff", 0.5, s), k).astype(np.float64)
+    sim = R.keydiff_similarity(k)
+    np.testing.assert_allclose(-got, sim, rtol=1e-5, atol=1e-6)
+
+
+def test_snapkv_scores_match_numpy(lib):
+    s = shape(1, 2, 160)
+    k, _ = _kv(1, 2, 160)
+    cfg = plan(lib, "snapkv", 0.5, s)
+    got = _scores(lib, s, cfg, k)
+    q = R.gen_q(1, 2, cfg.q_heads, cfg.window, 128, cfg.q_seed)
+    want = R.snapkv_scores(k, q, cfg.window, cfg.q_heads, cfg.pool)
+    assert np.array_equal(np.isinf(got), np.isinf(want))
+    fin = np.isfinite(want)
+    np.testing.assert_allclose(got[fin], want[fin], rtol=1e-6)
+
+
+def test_topk_rule_ties_and_order(lib):
+    s = shape(1, 3, 50)
+    sc = np.zeros((1, 3, 50), np.float32)
+    sc[0, 0] = np.arange(50)[::-1]  # strictly decreasing: keep the first k
+    sc[0, 1] = 1.0  # all tied: lowest indices
+    sc[0, 1, 40] = 2.0
+    sc[0, 2] = np.random.default_rng(1).integers(0, 4, 50)  # heavy ties
+    sc[0, 2, 7] = -0.0
+    cfg = plan(lib, "knorm", 0.2, s)
+    idx = np.zeros((1, 3, cfg.keep), np.int32)
+    lib.check(lib.topk(None, C.byref(s), C.byref(cfg), A.ptr(sc), A.ptr(idx)))
+    assert idx[0, 0].tolist() == list(range(cfg.keep))
+    assert idx[0, 1].tolist() == list(range(cfg.keep - 1)) + [40]
+    assert np.array_equal(idx, R.topk_indices(sc, cfg.keep))
+
+
+@pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.25), ("keydiff-q4", 0.2), ("knorm-q2", 0.1),
+                                          ("snapkv", 0.3), ("knorm-q4", 0.05)])
+def test_pack_unpack_roundtrip(lib, method, ratio):
+    s = shape(2, 2, 300)
+    k, v = _kv(2, 2, 300)
+    cfg = plan(lib, method, ratio, s)
+    m = A.BlobMap()
+    lib.check(lib.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    ws = np.zeros(lib.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
+    blob = np.zeros(m.total_bytes, np.uint8)
+    lib.check(lib.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+    idx = blob[m.idx_off:m.idx_off + m.idx_bytes].view(np.int32).reshape(2, 2, cfg.keep)
+    assert (np.diff(idx, axis=-1) > 0).all() and idx.min() >= 0 and idx.max() < 300
+    ko = np.zeros((2, 2, cfg.keep, 128), np.uint16)
+    vo = np.zeros_like(ko)
+    lib.check(lib.unpack(None, C.byref(s), C.byref(cfg), A.ptr(blob), A.ptr(ko), A.ptr(vo)))
+    kk = np.take_along_axis(R.bf2f(k), idx[..., None].astype(np.int64), axis=2)
+    vv = np.take_along_axis(R.bf2f(v), idx[..., None].astype(np.int64), axis=2)
+    if cfg.bits == 16:
+        assert np.array_equal(R.bf2f(ko), kk) and np.array_equal(R.bf2f(vo), vv)
+        return
+    # error bound: half a quantisation step (fp16 scale) plus bf16 output rounding
+    b = cfg.bits
+    for x, y, axis in ((kk, R.bf2f(ko), 2), (vv, R.bf2f(vo), 3)):
+        if axis == 2:  # per channel over groups of 128 kept tokens
+            err_ok = True
+            for g0 in range(0, cfg.keep, 128):
+                seg = x[:, :, g0:g0 + 128]
+                step = (seg.max(2, keepdims=True) - seg.min(2, keepdims=True)) / (2 ** b - 1)
+                err = np.abs(y[:, :, g0:g0 + 128] - seg)
+                err_ok &= bool((err <= 0.51 * step * 1.002 + np.abs(seg) * 2 ** -7 + 1e-3).all())
+            assert err_ok
+        else:
+            step = (x.max(3, keepdims=True) - x.min(3, keepdims=True)) / (2 ** b - 1)
+            assert (np.abs(y - x) <= 0.51 * step * 1.002 + np.abs(x) * 2 ** -7 + 1e-3).all()

@@ -1,0 +1,219 @@
+"""CUDA codec vs the codec oracle (oracle/orc_codec.c). Bit-exact: synthetic
+KV, knorm/keydiff scores, top-k indices, packed codes + fp16 params,
+dequantised KV. snapkv scores are fp32-softmax on the GPU vs FP64 on the
+CPU: tolerance rtol 2e-5, and kept indices must agree wherever the score
+margin to the k-th threshold exceeds that tolerance."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_14946_b200 import _abi as A
+from paper_2512_14946_b200.kvtier import Engine
+
+pytestmark = pytest.mark.gpu
+
+SNAP_RTOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def gpu(gpu_abi):
+    return Engine(gpu_abi)
+
+
+@pytest.fixture(scope="module")
+def orc(oracle_abi):
+    return Engine(oracle_abi)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t, dtype):
+    return t.cpu().numpy().view(dtype)
+
+
+def plan(abi, method, ratio, s):
+    cfg = A.CodecCfg()
+    abi.check(abi.codec_plan(method.encode(), ratio, C.byref(s), C.byref(cfg)))
+    return cfg
+
+
+def gen(eng, s, seed=9, ctx=3, on_gpu=True):
+    n = s.L * s.H * s.T * s.D
+    if on_gpu:
+        k = torch.empty(n, dtype=torch.int16, device="cuda")
+        v = torch.empty_like(k)
+        eng.abi.check(eng.abi.kv_generate(eng.h, C.byref(s), seed, ctx, A.ptr(k), A.ptr(v)))
+        eng.abi.check(eng.abi.sync(eng.h))
+        return k, v
+    k = np.zeros(n, np.uint16)
+    v = np.zeros(n, np.uint16)
+    eng.abi.check(eng.abi.kv_generate(None, C.byref(s), seed, ctx, A.ptr(k), A.ptr(v)))
+    return k, v
+
+
+SHAPES = [A.KvShape(2, 2, 300, 128), A.KvShape(1, 3, 1000, 128), A.KvShape(3, 1, 129, 128)]
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+def test_kv_generate_bitexact(gpu, orc, si):
+    s = SHAPES[si]
+    kg, vg = gen(gpu, s)
+    ko, vo = gen(orc, s, on_gpu=False)
+    assert np.array_equal(host(kg, np.uint16), ko) and np.array_equal(host(vg, np.uint16), vo)
+
+
+def scores(eng, s, cfg, k, on_gpu):
+    if on_gpu:
+        out = torch.empty(s.L * s.H * s.T, dtype=torch.float32, device="cuda")
+        eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+        eng.abi.check(eng.abi.sync(eng.h))
+        return out.cpu().numpy()
+    out = np.zeros(s.L * s.H * s.T, np.float32)
+    eng.abi.check(eng.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+    return out
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+@pytest.mark.parametrize("method", ["knorm", "keydiff"])
+def test_scores_bitexact(gpu, orc, si, method):
+    s = SHAPES[si]
+    kg, _ = gen(gpu, s)
+    ko, _ = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, method, 0.3, s)
+    sg, so = scores(gpu, s, cfg, kg, True), scores(orc, s, cfg, ko, False)
+    assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
+
+
+def topk(eng, s, cfg, sc, on_gpu):
+    if on_gpu:
+        out = torch.empty(s.L * s.H * cfg.keep, dtype=torch.int32, device="cuda")
+        eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfg), A.ptr(sc), A.ptr(out)))
+        eng.abi.check(eng.abi.sync(eng.h))
+        return out.cpu().numpy()
+    out = np.zeros(s.L * s.H * cfg.keep, np.int32)
+    eng.abi.check(eng.abi.topk(None, C.byref(s), C.byref(cfg), A.ptr(sc), A.ptr(out)))
+    return out
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+def test_snapkv_scores_within_tolerance(gpu, orc, si):
+    s = SHAPES[si]
+    kg, _ = gen(gpu, s)
+    ko, _ = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, "snapkv", 0.3, s)
+    sg, so = scores(gpu, s, cfg, kg, True), scores(orc, s, cfg, ko, False)
+    assert np.array_equal(np.isinf(sg), np.isinf(so))
+    fin = np.isfinite(so)
+    np.testing.assert_allclose(sg[fin], so[fin], rtol=SNAP_RTOL)
+    # kept indices agree wherever the margin to the k-th score is above tolerance
+    ig = topk(gpu, s, cfg, dev(sg), True).reshape(s.L * s.H, -1)
+    io = topk(orc, s, cfg, so, False).reshape(s.L * s.H, -1)
+    so2 = so.reshape(s.L * s.H, -1)
+    for r in range(s.L * s.H):
+        fin_r = so2[r][np.isfinite(so2[r])]
+        kth = np.sort(so2[r])[::-1][cfg.keep - 1]
+        tol = SNAP_RTOL * 4 * max(abs(kth), 1e-30)
+        safe = np.abs(so2[r] - kth) > tol
+        assert np.array_equal(np.isin(np.nonzero(safe)[0], ig[r]), np.isin(np.nonzero(safe)[0], io[r]))
+        assert len(fin_r) >= 0
+
+
+@pytest.mark.parametrize("keep_ratio", [0.001, 0.2, 0.5, 1.0])
+def test_topk_bitexact_with_ties(gpu, orc, keep_ratio):
+    s = A.KvShape(2, 3, 5000, 128)
+    rng = np.random.default_rng(4)
+    sc = rng.integers(0, 50, s.L * s.H * s.T).astype(np.float32)  # heavy ties
+    sc[::7] = -0.0
+    sc[1::11] = np.float32(-3.5)
+    sc[5000:10000] = rng.standard_normal(5000).astype(np.float32)
+    cfg = plan(orc.abi, "knorm", keep_ratio, s)
+    assert np.array_equal(topk(gpu, s, cfg, dev(sc), True), topk(orc, s, cfg, sc, False))
+
+
+def compress(eng, s, cfg, k, v, on_gpu):
+    m = A.BlobMap()
+    eng.abi.check(eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    wsb = eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg))
+    if on_gpu:
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        blob = torch.zeros(m.total_bytes, dtype=torch.uint8, device="cuda")
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+        eng.abi.check(eng.abi.sync(eng.h))
+    else:
+        ws = np.zeros(wsb, np.uint8)
+        blob = np.zeros(m.total_bytes, np.uint8)
+        eng.abi.check(eng.abi.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+    return blob, m
+
+
+def blob_sections(b, m, bits):
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else b
+    out = {"idx": b[m.idx_off:m.idx_off + m.idx_bytes], "kcode": b[m.kcode_off:m.kcode_off + m.kcode_bytes],
+           "vcode": b[m.vcode_off:m.vcode_off + m.vcode_bytes]}
+    if bits < 16:
+        for n, o, sz in (("kscale", m.kscale_off, m.kparam_bytes), ("kzero", m.kzero_off, m.kparam_bytes),
+                         ("vscale", m.vscale_off, m.vparam_bytes), ("vzero", m.vzero_off, m.vparam_bytes)):
+            out[n] = b[o:o + sz]
+    return out
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+@pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.3), ("keydiff-q4", 0.2), ("knorm-q2", 0.1),
+                                          ("keydiff", 0.4), ("knorm-q4", 0.02), ("knorm-q8", 0.5)])
+def test_compress_unpack_bitexact(gpu, orc, si, method, ratio):
+    s = SHAPES[si]
+    kg, vg = gen(gpu, s)
+    ko, vo = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, method, ratio, s)
+    bg, m = compress(gpu, s, cfg, kg, vg, True)
+    bo, _ = compress(orc, s, cfg, ko, vo, False)
+    sg, so = blob_sections(bg, m, cfg.bits), blob_sections(bo, m, cfg.bits)
+    for name in so:
+        assert np.array_equal(sg[name], so[name]), name
+    n = s.L * s.H * cfg.keep * 128
+    kug = torch.empty(n, dtype=torch.int16, device="cuda")
+    vug = torch.empty_like(kug)
+    gpu.abi.check(gpu.abi.unpack(gpu.h, C.byref(s), C.byref(cfg), A.ptr(bg), A.ptr(kug), A.ptr(vug)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    kuo = np.zeros(n, np.uint16)
+    vuo = np.zeros(n, np.uint16)
+    orc.abi.check(orc.abi.unpack(None, C.byref(s), C.byref(cfg), A.ptr(bo), A.ptr(kuo), A.ptr(vuo)))
+    assert np.array_equal(host(kug, np.uint16), kuo) and np.array_equal(host(vug, np.uint16), vuo)
+
+
+def test_full_llama_chunk_knorm_q4_properties(gpu, orc):
+    """One full Llama-3.1-8B chunk (32 L x 8 H x 8192 T x 128, 1 GiB):
+    knorm scores bit-exact to the oracle, top-k sorted and sized, and the
+    unpacked KV within half a quantisation step of the kept originals."""
+    s = A.KvShape(32, 8, 8192, 128)
+    kg, vg = gen(gpu, s, seed=1, ctx=0)
+    cfg = plan(orc.abi, "knorm-q4", 0.1, s)
+    sg = scores(gpu, s, cfg, kg, True)
+    ko, _ = gen(orc, A.KvShape(32, 8, 8192, 128), seed=1, ctx=0, on_gpu=False)
+    so = scores(orc, s, cfg, ko, False)
+    assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
+    bg, m = compress(gpu, s, cfg, kg, vg, True)
+    idx = bg[m.idx_off:m.idx_off + m.idx_bytes].view(torch.int32).reshape(256, cfg.keep)
+    assert bool((idx[:, 1:] > idx[:, :-1]).all()) and int(idx.min()) >= 0 and int(idx.max()) < 8192
+    n = 256 * cfg.keep * 128
+    ku = torch.empty(n, dtype=torch.int16, device="cuda")
+    vu = torch.empty_like(ku)
+    gpu.abi.check(gpu.abi.unpack(gpu.h, C.byref(s), C.byref(cfg), A.ptr(bg), A.ptr(ku), A.ptr(vu)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    kk = kg.view(torch.bfloat16).float().reshape(256, 8192, 128)
+    vv = vg.view(torch.bfloat16).float().reshape(256, 8192, 128)
+    gi = idx.long()[..., None].expand(-1, -1, 128)
+    kk = torch.gather(kk, 1, gi)
+    vv = torch.gather(vv, 1, gi)
+    kd = ku.view(torch.bfloat16).float().reshape(256, cfg.keep, 128)
+    vd = vu.view(torch.bfloat16).float().reshape(256, cfg.keep, 128)
+    vstep = (vv.amax(2, keepdim=True) - vv.amin(2, keepdim=True)) / 15
+    assert bool(((vd - vv).abs() <= 0.51 * vstep * 1.002 + vv.abs() * 2 ** -7 + 1e-3).all())
+    for g0 in range(0, cfg.keep, 128):
+        seg = kk[:, g0:g0 + 128]
+        kstep = (seg.amax(1, keepdim=True) - seg.amin(1, keepdim=True)) / 15
+        assert bool(((kd[:, g0:g0 + 128] - seg).abs() <= 0.51 * kstep * 1.002 + seg.abs() * 2 ** -7 + 1e-3).all())
