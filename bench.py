@@ -1,0 +1,445 @@
+"""Bench: KV GB/s compressed + scored + placed (BASELINE.json metric).
+
+One step = one pass of the hot path over a batch of contexts with inputs
+resident in HBM: K1 candidate scoring + K3 greedy placement of every context
+(insert_joint in arrival order into an empty 3-tier store), then the codec
+(token scores -> per-head top-k -> gather + quantise + pack) of every
+context's KV chunk at the configuration it was placed at. value = original
+KV bytes of the batch / device time of the step, summed over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference   # CPU reference arm (oracle/_ref + codec port)
+
+N > 1 (torchrun): each rank owns n_ctx contexts (weak scaling). The
+placement is global: profiles are all-gathered over NCCL and every rank runs
+the identical deterministic greedy over all contexts, then compresses only
+its own contexts.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+
+def algorithmic_bytes(L, H, T, cfg, m):
+    """Per-launch algorithmic HBM bytes of each codec phase."""
+    S, D, k = L * H, 128, cfg.keep
+    kv_rows = S * T * D * 2
+    return {
+        "scores": kv_rows + S * T * 4,                          # read K once, write f32 scores
+        "topk": S * T * 4 + S * k * 4,                          # read scores, write indices
+        "pack": 2 * S * k * D * 2 + (m.total_bytes),            # read kept K,V rows, write blob
+    }
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_14946_b200 as pkg
+    from paper_2512_14946_b200 import _abi as A
+    from paper_2512_14946_b200 import workload
+    from paper_2512_14946_b200.kvtier import Engine, ProfileArrays
+    from paper_2512_14946_b200.pipeline import Codec, KVPool, compress_placed, place
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    W = workload.build(args.config, n_ctx=args.n_ctx, seed=7 + rank)
+    cfg, shape, space, mine, params = W["cfg"], W["shape"], W["space"], W["arrays"], W["params"]
+    L, H, D = shape["L"], shape["H"], shape["D"]
+    bpt = W["bytes_per_token"]
+    n_local = mine.n
+
+    # global profile set: all-gather every rank's profile rows (NCCL)
+    if world > 1:
+        def gather(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device="cuda")
+            dist.all_gather_into_tensor(out, t)
+            return out.cpu().numpy().reshape((-1,) + tuple(a.shape[1:]))
+        G = len(mine.grid) // mine.n
+        orig = gather(mine.orig)
+        freq = gather(mine.freq)
+        qual = gather(mine.qual.reshape(mine.n, -1)).reshape(-1)
+        has = gather(mine.has)
+        ids = [f"r{r:03d}-{i:07d}" for r in range(world) for i in range(n_local)]
+        arrays = ProfileArrays.uniform_grid(ids, orig, freq, mine.grid[:G],
+                                            qual.reshape(world * n_local, len(space.methods), G), has)
+    else:
+        arrays = mine
+    tiers = workload.three_tiers(int(arrays.orig.sum()), cfg["gpu_frac"], 0.30)
+    my_lo, my_hi = rank * n_local, (rank + 1) * n_local
+
+    stream = torch.cuda.Stream()
+    eng = Engine(pkg.product(), device=local, stream=stream.cuda_stream)
+    max_T = int(arrays.orig.max() // bpt)
+    pool = KVPool(eng, L, H, max_T, D, n_chunks=args.pool)
+    codec = Codec(eng, L, H, D)
+    codec.reserve(max_T, n_out=2)
+    ps = eng.pset(arrays)
+    store = eng.store(tiers, arrays.n, space)
+    order = np.arange(arrays.n, dtype=np.int32)
+
+    class Mine:  # the contexts this rank compresses
+        n = n_local
+        orig = arrays.orig[my_lo:my_hi]
+
+    def step():
+        acts = place(store, ps, space, params, order)
+        snap_full = store.snapshot()
+        names = space.method_names
+        in_b = out_b = 0
+        for c in range(my_lo, my_hi):
+            if snap_full["tier_index"][c] < 0:
+                continue
+            T = int(arrays.orig[c] // bpt)
+            k, v = pool.chunk(c)
+            out_b += codec.compress(names[snap_full["method"][c]], float(snap_full["ratio"][c]), k, v, T, c)
+            in_b += int(arrays.orig[c])
+        return len(acts), in_b, out_b
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    l0 = eng.abi.launch_count(eng.h)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        t0.record(stream)
+        n_act = in_b = out_b = 0
+        for _ in range(args.steps):
+            n_act, in_b, out_b = step()
+        t1.record(stream)
+        barrier()
+    launches = eng.abi.launch_count(eng.h) - l0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_bytes = int(arrays.orig.sum())  # all ranks' contexts
+    value = total_bytes / (ms_step / 1e3) / 1e9
+
+    # ---- e2e: through the C ABI with host buffers, copies inside the timed region
+    h2d = d2h = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ps_e = eng.pset(arrays)  # H2D of every profile row
+        h2d = (arrays.orig.nbytes + arrays.freq.nbytes + arrays.goff.nbytes + arrays.grid.nbytes +
+               arrays.qual.nbytes + arrays.has.nbytes + order.nbytes * 3)
+        acts = place(store, ps_e, space, params, order)  # actions D2H
+        snap_full = store.snapshot()  # placement D2H
+        names = space.method_names
+        for c in range(my_lo, my_hi):
+            T = int(arrays.orig[c] // bpt)
+            k, v = pool.chunk(c)
+            codec.compress(names[snap_full["method"][c]], float(snap_full["ratio"][c]), k, v, T, c)
+        d2h = acts.nbytes + snap_full.nbytes
+        del ps_e
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = total_bytes / (e2e_ms / args.steps / 1e3) / 1e9
+
+    # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
+    roof = None
+    phases = {}
+    if rank == 0:
+        snap_full = store.snapshot()
+        names = space.method_names
+        ev = {}
+        acc = {"scores": 0.0, "topk": 0.0, "pack": 0.0}
+        alg = {"scores": 0, "topk": 0, "pack": 0}
+        nl = {"scores": 0, "topk": 0, "pack": 0}
+        by_scorer = {}
+        for c in range(my_lo, my_hi):
+            T = int(arrays.orig[c] // bpt)
+            cfgc, m, _ = codec.plan(names[snap_full["method"][c]], float(snap_full["ratio"][c]), T)
+            s = A.KvShape(L, H, T, D)
+            k, v = pool.chunk(c)
+            ws = codec.ws
+            sc = ws  # scores at offset 0
+            idx_off = eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfgc)) - ((4 * L * H * cfgc.keep + 255) // 256) * 256
+            idx = ws.data_ptr() + idx_off
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            evs[0].record(stream)
+            eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(sc)))
+            evs[1].record(stream)
+            eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfgc), A.ptr(sc), idx))
+            evs[2].record(stream)
+            eng.abi.check(eng.abi.pack(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), idx,
+                                       A.ptr(codec.out[c % 2])))
+            evs[3].record(stream)
+            ab = algorithmic_bytes(L, H, T, cfgc, m)
+            ev[c] = (evs, ab, cfgc.scorer)
+        torch.cuda.synchronize()
+        for c, (evs, ab, scorer) in ev.items():
+            for i, ph in enumerate(("scores", "topk", "pack")):
+                dt = evs[i].elapsed_time(evs[i + 1])
+                acc[ph] += dt
+                alg[ph] += ab[ph]
+                nl[ph] += 1
+                if ph == "scores":
+                    b = by_scorer.setdefault(scorer, [0.0, 0, 0])
+                    b[0] += dt
+                    b[1] += ab[ph]
+                    b[2] += 1
+        tot = sum(acc.values())
+        phases = {ph: round(acc[ph] / tot, 4) for ph in acc}
+        dom = max(acc, key=acc.get)
+        pk, how = peaks()
+        achieved = alg[dom] / (acc[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
+                "peak_source": how, "avg_launch_ms": round(acc[dom] / max(1, nl[dom]), 4),
+                "phase_share": phases,
+                "scores_by_scorer_gbs": {["knorm", "keydiff", "snapkv"][s_]: round(b[1] / (b[0] / 1e3) / 1e9, 1)
+                                         for s_, b in by_scorer.items()}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "KV GB/s compressed+scored+placed",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f64 scoring",
+            "data": "synthetic (counter-hash KV, generated profiles)",
+            "config": {"workload": f"{args.config}: {cfg['model']} KV, {n_local} contexts/GPU x {cfg['tokens']} tokens, "
+                                   f"{len(space.methods)} methods x {len(space.ratios)} ratios x 3 tiers",
+                       "contexts_total": arrays.n, "methods": space.method_names,
+                       "kv_bytes_per_step": total_bytes, "kv_pool_chunks": args.pool,
+                       "l2": "inputs larger than L2 (1 GiB chunks, pool of distinct chunks)",
+                       "actions_per_step": n_act, "compressed_bytes_per_step_rank0": out_b,
+                       "parallelism": f"dp{world} (contexts sharded, global greedy replicated)"},
+            "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ CPU reference
+
+def cpu_reference_sample(W, seconds=20.0, steps=1):
+    """The reference's own CPU path on a bounded sample of the workload:
+    placement = the reference kvtier library (oracle/_ref) running
+    insert_joint over every context of the batch; codec = the CPU codec port
+    (oracle/liboracle.so; the reference has no codec) on a sample of
+    (layer, head) slices of the placed configurations, extrapolated to full
+    chunks. Returns the cpu_baseline object (value in the bench's unit)."""
+    from paper_2512_14946_b200 import _abi as A
+    from paper_2512_14946_b200.kvtier import Engine
+
+    ref_path = os.path.join(ROOT, "oracle", "_ref", "libkvtier_ref.so")
+    orc_path = os.path.join(ROOT, "oracle", "liboracle.so")
+    kind = "reference" if os.path.exists(ref_path) else "port"
+    place_abi = A.Abi(ref_path, "ref_", codec=False) if kind == "reference" else A.Abi(orc_path, "orc_", codec=False)
+    orc = A.Abi(orc_path, "orc_", codec=True)
+    arrays, space, params, tiers = W["arrays"], W["space"], W["params"], W["tiers"]
+    L, H = W["shape"]["L"], W["shape"]["H"]
+    bpt = W["bytes_per_token"]
+    eng = Engine(place_abi)
+    ps = eng.pset(arrays)
+    st = eng.store(tiers, arrays.n, space)
+    t0 = time.perf_counter()
+    st.insert_joint(ps, space, params, np.arange(arrays.n))
+    t_place = time.perf_counter() - t0
+    snap = st.snapshot()
+    # codec: time each distinct (method, ratio, T) on a 1-layer slice sample
+    groups = {}
+    for c in range(arrays.n):
+        key = (space.method_names[snap["method"][c]], float(snap["ratio"][c]), int(arrays.orig[c] // bpt))
+        groups[key] = groups.get(key, 0) + 1
+    threads = int(orc.lib.orc_parallel_threads()) if hasattr(orc.lib, "orc_parallel_threads") else os.cpu_count()
+    budget = max(1.0, seconds - t_place)
+    t_codec_timed = 0.0  # extrapolated full-chunk codec seconds of the timed groups
+    timed_ctx = 0
+    spent = 0.0
+    for (meth, ratio, T), count in sorted(groups.items(), key=lambda kv: -kv[1]):
+        if spent > budget:
+            break
+        Ls = 1
+        s = A.KvShape(Ls, H, T, 128)
+        cfg = A.CodecCfg()
+        orc.check(orc.codec_plan(meth.encode(), ratio, C.byref(s), C.byref(cfg)))
+        m = A.BlobMap()
+        orc.check(orc.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+        n = Ls * H * T * 128
+        k = np.zeros(n, np.uint16)
+        v = np.zeros(n, np.uint16)
+        orc.check(orc.kv_generate(None, C.byref(s), 1, 0, A.ptr(k), A.ptr(v)))
+        ws = np.zeros(orc.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
+        blob = np.zeros(m.total_bytes, np.uint8)
+        t0 = time.perf_counter()
+        orc.check(orc.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+        dt = time.perf_counter() - t0
+        spent += dt
+        t_codec_timed += dt * (L / Ls) * count  # full chunk, every context of this group
+        timed_ctx += count
+    # configurations not timed within the budget cost the timed mean per context
+    t_codec_all = t_codec_timed / max(1, timed_ctx) * arrays.n
+    t_total = t_place + t_codec_all
+    value = float(arrays.orig.sum()) / t_total / 1e9
+    return {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": (f"placement: {'reference kvtier' if kind == 'reference' else 'oracle'} insert_joint over all "
+                       f"{arrays.n} contexts ({t_place:.2f} s, 1 thread); codec: CPU port (no reference codec) on "
+                       f"1 of {L} layers x {H} heads per distinct placed config ({timed_ctx}/{arrays.n} contexts' "
+                       f"configs timed in {spent:.1f} s on {threads} threads), extrapolated x{L} per chunk"),
+            "t_place_s": round(t_place, 3), "t_codec_extrapolated_s": round(t_codec_all, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_2512_14946_b200 import workload
+    W = workload.build(args.config, n_ctx=args.n_ctx)
+    vals = []
+    cpu = None
+    for i in range(args.warmup + args.steps):
+        cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
+        if i >= args.warmup:
+            vals.append(cpu["value"])
+    value = statistics.median(vals)
+    cfg = W["cfg"]
+    line = {"impl": "reference", "metric": "KV GB/s compressed+scored+placed", "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 scoring, bf16 KV",
+            "data": "synthetic (counter-hash KV, generated profiles)",
+            "config": {"workload": f"{args.config}: {cfg['model']} KV, {W['arrays'].n} contexts x {cfg['tokens']} tokens",
+                       "methods": W["space"].method_names},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cpu["cores"], "kind": cpu["kind"],
+                             "sample": cpu["sample"]},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--n-ctx", type=int, default=None)
+    ap.add_argument("--pool", type=int, default=8, help="distinct resident KV chunks")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
   const int l16 = threadIdx.x & 15;
   const long long hw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
   const long long nhw = (gridDim.x * (long long)blockDim.x) >> 4;
-  for (long long t0 = hw; t0 < ntok; t0 += nhw * kUnroll) {
+  // loop bounds are warp-uniform (both half-warps run the same trip count)
+  for (long long b0 = hw & ~1LL; b0 < ntok; b0 += nhw * kUnroll) {
+    const long long t0 = b0 + (hw & 1);
     uint4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -194,8 +196,10 @@ __global__ void __launch_bounds__(256) k_keydiff_sum(const uint4* __restrict__ K
   const int t_begin = blockIdx.x * kKdTokens;
   const uint4* Ks = K + static_cast<size_t>(slice) * T * 16;
   long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int t = t_begin + hw; t < min(T, t_begin + kKdTokens); t += 16) {
-    const uint4 v = Ks[static_cast<size_t>(t) * 16 + l16];
+  const int t_end = min(T, t_begin + kKdTokens);
+  for (int b = t_begin + (hw & ~1); b < t_end; b += 16) {  // warp-uniform trip count
+    const int t = b + (hw & 1);
+    const uint4 v = t < t_end ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
     const double n2 = half_butterfly(chunk_sumsq(v));
     const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -230,8 +234,10 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     sd[i] = __dmul_rn(__ll2double_rn(S[static_cast<size_t>(slice) * kD + l16 * 8 + i]), 1.0 / kFx);
-  for (int t = t_begin + hw; t < min(T, t_begin + kKdTokens); t += 16) {
-    const uint4 v = __ldcs(Ks + static_cast<size_t>(t) * 16 + l16);
+  const int t_end = min(T, t_begin + kKdTokens);
+  for (int b = t_begin + (hw & ~1); b < t_end; b += 16) {  // warp-uniform trip count
+    const int t = b + (hw & 1);
+    const uint4 v = t < t_end ? __ldcs(Ks + static_cast<size_t>(t) * 16 + l16) : make_uint4(0, 0, 0, 0);
     const double n2 = half_butterfly(chunk_sumsq(v));
     const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -244,7 +250,7 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
       acc = __dadd_rn(acc, __dmul_rn(b, sd[2 * j + 1]));
     }
     const double p = half_butterfly(acc);
-    if (l16 == 0) out[static_cast<size_t>(slice) * T + t] = __double2float_rn(-p);
+    if (l16 == 0 && t < t_end) out[static_cast<size_t>(slice) * T + t] = __double2float_rn(-p);
   }
 }
 
