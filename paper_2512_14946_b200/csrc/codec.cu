@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <string>
 
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "codec_common.cuh"
@@ -511,28 +512,32 @@ __global__ void __launch_bounds__(256) k_gather16(const uint4* __restrict__ K, c
   if (l16 == 0) oidx[static_cast<size_t>(slice) * k + j] = t;
 }
 
-// K quantisation: per channel over a group of <=128 kept tokens. Block =
-// (group, slice), 256 threads: rows staged in smem, channel min/max split
-// over two thread halves, codes packed row-wise with coalesced stores.
-__global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
-                                                uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
-                                                uint16_t* __restrict__ kz, int T, int k, int bits) {
-  extern __shared__ uint4 pack_smem[];
-  uint4 (*rows)[16] = reinterpret_cast<uint4 (*)[16]>(pack_smem);  // 32 KB bf16 tile
-  uint8_t (*codes)[kD + 4] = reinterpret_cast<uint8_t (*)[kD + 4]>(pack_smem + KVT_QGROUP * 16);
-  __shared__ float pmn[2][kD], pmx[2][kD];
-  __shared__ QParam prm[kD];
-  const int slice = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+// K quantisation: per channel over a group of <=128 kept tokens. The whole
+// block (256 threads) packs group g of one slice: rows staged in smem,
+// channel min/max split over two thread halves, codes packed row-wise with
+// coalesced stores. Block-uniform: call from every thread.
+struct PackKSmem {
+  uint4 rows[KVT_QGROUP][16];        // 32 KB bf16 tile
+  uint8_t codes[KVT_QGROUP][kD + 4];
+  float pmn[2][kD], pmx[2][kD];
+  QParam prm[kD];
+};
+
+__device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
+                                             uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
+                                             uint16_t* __restrict__ kz, int T, int k, int bits, int slice, int g,
+                                             PackKSmem& sm) {
+  const int tid = threadIdx.x;
   const int j0 = g * KVT_QGROUP, nr = min(KVT_QGROUP, k - j0);
   const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
   const int32_t* ix = idx + static_cast<size_t>(slice) * k + j0;
   for (int i = tid; i < nr * 16; i += 256) {
     const int r = i >> 4, l16 = i & 15;
-    rows[r][l16] = __ldcs(K + (static_cast<size_t>(slice) * T + ix[r]) * 16 + l16);
+    sm.rows[r][l16] = __ldcs(K + (static_cast<size_t>(slice) * T + ix[r]) * 16 + l16);
   }
   __syncthreads();
   const int d = tid & (kD - 1), half = tid >> 7;
-  const uint16_t* tile = reinterpret_cast<const uint16_t*>(rows);
+  const uint16_t* tile = reinterpret_cast<const uint16_t*>(sm.rows);
   {
     const int r0 = half * 64, r1 = min(nr, r0 + 64);
     float mn = INFINITY, mx = -INFINITY;
@@ -541,24 +546,24 @@ __global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, con
       mn = x < mn ? x : mn;
       mx = x > mx ? x : mx;
     }
-    pmn[half][d] = mn;
-    pmx[half][d] = mx;
+    sm.pmn[half][d] = mn;
+    sm.pmx[half][d] = mx;
   }
   __syncthreads();
   if (half == 0) {
-    const float mn = pmn[1][d] < pmn[0][d] ? pmn[1][d] : pmn[0][d];
-    const float mx = pmx[1][d] > pmx[0][d] ? pmx[1][d] : pmx[0][d];
+    const float mn = sm.pmn[1][d] < sm.pmn[0][d] ? sm.pmn[1][d] : sm.pmn[0][d];
+    const float mx = sm.pmx[1][d] > sm.pmx[0][d] ? sm.pmx[1][d] : sm.pmx[0][d];
     const QParam p = make_param(mn, mx, bits);
-    prm[d] = p;
+    sm.prm[d] = p;
     const size_t po = (static_cast<size_t>(slice) * ng + g) * kD + d;
     ks[po] = p.s16;
     kz[po] = p.z16;
   }
   __syncthreads();
   {
-    const QParam p = prm[d];
+    const QParam p = sm.prm[d];
     const int r0 = half * 64, r1 = min(nr, r0 + 64);
-    for (int r = r0; r < r1; ++r) codes[r][d] = static_cast<uint8_t>(quant(bf2f(tile[r * kD + d]), p, bits));
+    for (int r = r0; r < r1; ++r) sm.codes[r][d] = static_cast<uint8_t>(quant(bf2f(tile[r * kD + d]), p, bits));
   }
   __syncthreads();
   const int wpr = kD * bits / 32, per = 32 / bits;
@@ -566,18 +571,26 @@ __global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, con
   for (int i = tid; i < nr * wpr; i += 256) {
     const int r = i / wpr, w = i - r * wpr;
     uint32_t word = 0;
-    for (int q = 0; q < per; ++q) word |= uint32_t(codes[r][w * per + q]) << (bits * q);
+    for (int q = 0; q < per; ++q) word |= uint32_t(sm.codes[r][w * per + q]) << (bits * q);
     out[i] = word;
   }
+  __syncthreads();  // smem reused by the next group
+}
+
+__global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
+                                                uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
+                                                uint16_t* __restrict__ kz, int T, int k, int bits) {
+  extern __shared__ uint4 pack_smem[];
+  pack_k_group(K, idx, kc, ks, kz, T, k, bits, blockIdx.y, blockIdx.x, *reinterpret_cast<PackKSmem*>(pack_smem));
 }
 
 // V quantisation: per kept token over its 128 channels; half-warp per row.
-__global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
-                                                int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
-                                                uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
-                                                int bits) {
-  const int slice = blockIdx.y, l16 = threadIdx.x & 15;
-  const int j = blockIdx.x * 16 + (threadIdx.x >> 4);
+// Warp-uniform: both half-warps must call (shuffles use the full mask).
+__device__ __forceinline__ void pack_v_row(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
+                                           int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
+                                           uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
+                                           int bits, int slice, int j) {
+  const int l16 = threadIdx.x & 15;
   const bool live = j < k;
   const int t = live ? idx[static_cast<size_t>(slice) * k + j] : 0;
   const uint4 v = live ? __ldcs(V + (static_cast<size_t>(slice) * T + t) * 16 + l16) : make_uint4(0, 0, 0, 0);
@@ -609,24 +622,31 @@ __global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, con
   if (bits == 8) {
     const uint32_t w0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
     const uint32_t w1 = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-    if (live) reinterpret_cast<uint2*>(out)[l16] = make_uint2(w0, w1);
+    if (live) __stcs(reinterpret_cast<uint2*>(out) + l16, make_uint2(w0, w1));
   } else if (bits == 4) {
     uint32_t w0 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) w0 |= c[i] << (4 * i);
-    if (live) out[l16] = w0;
+    if (live) __stcs(out + l16, w0);
   } else {  // 2 bits: 16 codes per word = two lanes
     uint32_t h0 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) h0 |= c[i] << (2 * i);
     const uint32_t other = __shfl_xor_sync(0xffffffffu, h0, 1);
-    if (live && (l16 & 1) == 0) out[l16 >> 1] = h0 | (other << 16);
+    if (live && (l16 & 1) == 0) __stcs(out + (l16 >> 1), h0 | (other << 16));
   }
   if (live && l16 == 0) {
     vs[static_cast<size_t>(slice) * k + j] = p.s16;
     vz[static_cast<size_t>(slice) * k + j] = p.z16;
-    oidx[static_cast<size_t>(slice) * k + j] = t;
+    if (oidx) oidx[static_cast<size_t>(slice) * k + j] = t;
   }
+}
+
+__global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
+                                                int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
+                                                uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
+                                                int bits) {
+  pack_v_row(V, idx, oidx, vc, vs, vz, T, k, bits, blockIdx.y, blockIdx.x * 16 + (threadIdx.x >> 4));
 }
 
 static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
@@ -646,7 +666,7 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
     return KVT_OK;
   }
   dim3 kgrid((kk + KVT_QGROUP - 1) / KVT_QGROUP, S);
-  const size_t pk_smem = sizeof(uint4) * KVT_QGROUP * 16 + KVT_QGROUP * (kD + 4);
+  const size_t pk_smem = sizeof(PackKSmem);
   static bool pk_attr = false;
   if (!pk_attr) {
     KVT_CUDA_TRY(cudaFuncSetAttribute(k_pack_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pk_smem)));
@@ -727,12 +747,275 @@ extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_
   return KVT_OK;
 }
 
+
+// ------------------------------------------------------- fused compress
+//
+// One thread-block cluster of kFuseC CTAs per (layer, kv-head) slice does
+// scores -> top-k -> gather + quantise + pack in a single launch. Each CTA
+// owns a contiguous token range of the slice. Cross-CTA steps go through
+// distributed shared memory: keydiff's mean direction (exact int64 fixed
+// point, so the sum order does not matter), the four radix-select
+// histograms and the (above, equal) counts that place each CTA's kept
+// indices. Only kFuseC x (#clusters in flight) slices are live at a time
+// (~40 x 2 MiB of K at T = 8192), so the re-reads of K (keydiff's second
+// pass, the kept rows in the pack) are L2 hits: HBM sees K once, the kept V
+// rows once and the blob once. Bit-identical to the unfused kernels.
+namespace cg = cooperative_groups;
+constexpr int kFuseC = 8;
+constexpr int kFuseThreads = 256;
+constexpr int kFuseUnroll = 4;
+constexpr size_t kFuseUnion = sizeof(PackKSmem) > 16 * kD * sizeof(long long) ? sizeof(PackKSmem)
+                                                                                : 16 * kD * sizeof(long long);
+constexpr size_t kFuseMaxSmem = 200 * 1024;
+using FuseScan = cub::BlockScan<int, kFuseThreads>;
+
+static size_t fuse_smem_bytes(int T) {
+  const size_t per = (T + kFuseC - 1) / kFuseC;
+  return kFuseUnion + al256(4 * per);
+}
+
+__global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2)
+    k_compress_fused(const uint4* __restrict__ K, const uint4* __restrict__ V, int T, int k, int bits, int scorer,
+                     kvt_blob_map m, char* __restrict__ blob) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int slice = blockIdx.y, tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
+  const int per = (T + kFuseC - 1) / kFuseC;
+  const int t_lo = min(T, rank * per), t_hi = min(T, t_lo + per), n_loc = t_hi - t_lo;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  PackKSmem& pk = *reinterpret_cast<PackKSmem*>(fsm);
+  long long(*part)[kD] = reinterpret_cast<long long(*)[kD]>(fsm);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFuseUnion);
+  __shared__ int hist[2][256];
+  __shared__ int tot[256];
+  __shared__ long long sfix[kD];
+  __shared__ double sdir[kD];
+  __shared__ int cnt[2];
+  __shared__ uint32_t s_prefix, s_mask;
+  __shared__ int s_rem;
+  __shared__ typename FuseScan::TempStorage scan_tmp;
+  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+
+  // ---- phase 1: token scores of [t_lo, t_hi) as orderable keys
+  if (scorer == KVT_SCORER_KNORM) {
+    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {  // warp-uniform trip count
+      uint4 v[kFuseUnroll];
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const int t = b0 + (hw & 1) + 16 * u;
+        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const int t = b0 + (hw & 1) + 16 * u;
+        const double n2 = half_butterfly(chunk_sumsq(v[u]));
+        if (t < n_loc && l16 == 0) keys[t] = score_key(__double2float_rn(n2));
+      }
+    }
+  } else {  // keydiff: exact fixed-point mean direction over the whole slice, then cosine
+    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {
+      uint4 v[kFuseUnroll];
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const int t = b0 + (hw & 1) + 16 * u;
+        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const double n2 = half_butterfly(chunk_sumsq(v[u]));
+        const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
+          const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
+          acc[2 * j] += __double2ll_rn(__dmul_rn(a, kFx));
+          acc[2 * j + 1] += __double2ll_rn(__dmul_rn(b, kFx));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = acc[i];
+    __syncthreads();
+    if (tid < kD) {
+      long long sum = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sum += part[i][tid];
+      sfix[tid] = sum;
+    }
+    cl.sync();
+    if (tid < kD) {
+      long long sum = 0;
+      for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(sfix, c)[tid];
+      sdir[tid] = __dmul_rn(__ll2double_rn(sum), 1.0 / kFx);
+    }
+    __syncthreads();
+    double sd[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sd[i] = sdir[l16 * 8 + i];
+    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {
+      uint4 v[kFuseUnroll];
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const int t = b0 + (hw & 1) + 16 * u;
+        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kFuseUnroll; ++u) {
+        const int t = b0 + (hw & 1) + 16 * u;
+        const double n2 = half_butterfly(chunk_sumsq(v[u]));
+        const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double x0 = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
+          const double x1 = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
+          a = __dadd_rn(a, __dmul_rn(x0, sd[2 * j]));
+          a = __dadd_rn(a, __dmul_rn(x1, sd[2 * j + 1]));
+        }
+        const double p = half_butterfly(a);
+        if (t < n_loc && l16 == 0) keys[t] = score_key(__double2float_rn(-p));
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: cluster-wide MSB-first radix select of the k-th key
+  uint32_t prefix = 0, mask = 0;
+  int rem = k;
+  for (int shift = 24, rd = 0; shift >= 0; shift -= 8, ++rd) {
+    int* h = hist[rd & 1];
+    h[tid] = 0;  // kFuseThreads == 256 bins
+    __syncthreads();
+    for (int t = tid; t < n_loc; t += kFuseThreads) {
+      const uint32_t key = keys[t];
+      if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255], 1);
+    }
+    cl.sync();
+    {
+      int sum = 0;
+      for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(h, c)[tid];
+      tot[tid] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int b = 255;
+      for (; b > 0; --b) {
+        if (tot[b] >= rem) break;
+        rem -= tot[b];
+      }
+      s_rem = rem;
+      s_prefix = prefix | (uint32_t(b) << shift);
+      s_mask = mask | (255u << shift);
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    mask = s_mask;
+    rem = s_rem;
+  }
+  const uint32_t kth = prefix;
+  const int ties = rem;
+
+  // ---- order-preserving compaction of the kept indices (ascending)
+  const int seg = (n_loc + kFuseThreads - 1) / kFuseThreads;
+  const int s0 = min(n_loc, tid * seg), s1 = min(n_loc, s0 + seg);
+  int above = 0, eq = 0;
+  for (int t = s0; t < s1; ++t) {
+    const uint32_t key = keys[t];
+    above += key > kth;
+    eq += key == kth;
+  }
+  int above_before, eq_before, above_all, eq_all;
+  FuseScan(scan_tmp).ExclusiveSum(above, above_before, above_all);
+  __syncthreads();
+  FuseScan(scan_tmp).ExclusiveSum(eq, eq_before, eq_all);
+  if (tid == 0) {
+    cnt[0] = above_all;
+    cnt[1] = eq_all;
+  }
+  cl.sync();
+  int a_base = 0, e_base = 0;
+  for (int c = 0; c < rank; ++c) {
+    const int* rc = cl.map_shared_rank(cnt, c);
+    a_base += rc[0];
+    e_base += rc[1];
+  }
+  int32_t* bidx = reinterpret_cast<int32_t*>(blob + m.idx_off);
+  {
+    int eq_seen = e_base + eq_before;
+    int pos = a_base + above_before + min(eq_seen, ties);
+    int32_t* out = bidx + static_cast<size_t>(slice) * k;
+    for (int t = s0; t < s1; ++t) {
+      const uint32_t key = keys[t];
+      if (key > kth) {
+        out[pos++] = t_lo + t;
+      } else if (key == kth) {
+        if (eq_seen < ties) out[pos++] = t_lo + t;
+        ++eq_seen;
+      }
+    }
+  }
+  cl.sync();  // every CTA's indices are visible; no DSMEM access after this point
+
+  // ---- phase 3: gather + quantise + pack (rows re-read from L2)
+  if (bits == 16) {
+    uint4* ko = reinterpret_cast<uint4*>(blob + m.kcode_off);
+    uint4* vo = reinterpret_cast<uint4*>(blob + m.vcode_off);
+    for (int jb = rank * 16; jb < k; jb += kFuseC * 16) {
+      const int j = jb + hw;
+      if (j < k) {
+        const int t = bidx[static_cast<size_t>(slice) * k + j];
+        const size_t src = (static_cast<size_t>(slice) * T + t) * 16 + l16;
+        const size_t dst = (static_cast<size_t>(slice) * k + j) * 16 + l16;
+        const uint4 a = __ldcs(K + src), b = __ldcs(V + src);
+        __stcs(ko + dst, a);
+        __stcs(vo + dst, b);
+      }
+    }
+  } else {
+    const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
+    for (int g = rank; g < ng; g += kFuseC)
+      pack_k_group(K, bidx, reinterpret_cast<uint32_t*>(blob + m.kcode_off),
+                   reinterpret_cast<uint16_t*>(blob + m.kscale_off), reinterpret_cast<uint16_t*>(blob + m.kzero_off),
+                   T, k, bits, slice, g, pk);
+    for (int jb = rank * 16; jb < k; jb += kFuseC * 16)
+      pack_v_row(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
+                 reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off), T,
+                 k, bits, slice, jb + hw);
+  }
+}
+
+static bool fused_ok(const kvt_kv_shape* s, const kvt_codec_cfg* c) {
+  return c->scorer != KVT_SCORER_SNAPKV && fuse_smem_bytes(s->T) <= kFuseMaxSmem;
+}
+
+static int launch_fused(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
+                        const uint16_t* v, void* blob) {
+  kvt_blob_map m;
+  blob_map(*s, *c, &m);
+  const size_t smem = fuse_smem_bytes(s->T);
+  static bool attr = false;
+  if (!attr) {
+    KVT_CUDA_TRY(cudaFuncSetAttribute(k_compress_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFuseMaxSmem)));
+    attr = true;
+  }
+  dim3 grid(kFuseC, s->L * s->H);
+  k_compress_fused<<<grid, kFuseThreads, smem, h->stream>>>(reinterpret_cast<const uint4*>(k),
+                                                             reinterpret_cast<const uint4*>(v), s->T, c->keep, c->bits,
+                                                             c->scorer, m, static_cast<char*>(blob));
+  LAUNCHED(h);
+  return KVT_OK;
+}
+
 // ---------------------------------------------------------------- compress
 
 extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
                             const uint16_t* v, void* workspace, void* blob) {
   int rc;
   if ((rc = check_shape(s, c))) return rc;
+  if (fused_ok(s, c) && !getenv("KVT_UNFUSED")) return launch_fused(h, s, c, k, v, blob);
   char* w = static_cast<char*>(workspace);
   float* scores = reinterpret_cast<float*>(w);
   float* votes = reinterpret_cast<float*>(w + ws_scores(s));

@@ -2,9 +2,12 @@
 these are the *inputs* both arms (CUDA and reference) consume.
 
 Profiles follow the reference's generator conventions: sensitivity-anchored
-curves (synth_quality, proj/src/quality.cpp:115-127), one shared grid, and
+curves (synth_quality, proj/src/quality.cpp:115-127) applied to the kept
+token fraction plus a per-bit-width quantisation cost, one shared grid, and
 Zipf-shaped frequencies (assign_zipf_frequencies, proj/src/workload.cpp:
-236-245, arrival rate 4, exponent 1). KV chunks come from the counter hash
+236-245, arrival rate 4, exponent 1). With these tables the greedy places a
+mix of q4 / q8 / token-drop / uncompressed configurations (c2, 1000 ctx:
+~19 % at ratio 1.0), so the codec does real work. KV chunks come from the counter hash
 of the codec spec (kvt_kv_generate), so no dataset is needed.
 """
 from __future__ import annotations
@@ -33,7 +36,29 @@ def three_tiers(total_bytes, gpu_frac=0.10, cpu_frac=0.30):
             TierSpec(2, "ssd", None, 6e9, 1e-4)]
 
 
-def profiles(n_ctx, space: CandidateSpace, seed=7, tokens=8192, bpt=131072, varied=False) -> ProfileArrays:
+QUANT_LOSS = {8: 0.002, 4: 0.01, 2: 0.04}  # quality cost of b-bit codes per unit sensitivity
+
+
+def eff_bytes(bits):
+    """Retained bytes per bf16 byte of a b-bit blob (codes + fp16 params);
+    DESIGN.md §4.1, same arithmetic as kvt_codec_plan."""
+    return 1.0 if bits >= 16 else bits / 16.0 + 1.0 / 64.0
+
+
+def codec_bits_keep(method, ratio):
+    """(bits, kept token fraction) the codec uses for `ratio` (kvt_codec_plan)."""
+    b = int(method.split("-q")[1]) if "-q" in method else 16
+    bb = next(w for w in (2, 4, 8, 16) if w >= b and (w == 16 or ratio <= eff_bytes(w)))
+    return bb, min(1.0, ratio / eff_bytes(bb))
+
+
+def profiles(n_ctx, space: CandidateSpace, seed=7, tokens=8192, bpt=131072, varied=False,
+             sensitivity=(0.0, 0.05), shape_k=1.5) -> ProfileArrays:
+    """Synthetic quality tables for "<scorer>[-q<b>]" methods. Token dropping
+    follows the reference's curve synth_quality (proj/src/quality.cpp:115-127),
+    1 - s*((1 - keep)/0.1)^k, applied to the fraction of tokens the codec
+    keeps at that ratio; b-bit codes cost QUANT_LOSS[b] x U(0.5, 1.5) more.
+    One sensitivity per (context, scorer), uniform in `sensitivity`."""
     rng = np.random.default_rng(seed)
     M = len(space.methods)
     grid = sorted(space.ratios)
@@ -41,14 +66,17 @@ def profiles(n_ctx, space: CandidateSpace, seed=7, tokens=8192, bpt=131072, vari
         orig = (rng.integers(1024, 2 * tokens, size=n_ctx) * bpt).astype(np.int64)
     else:
         orig = np.full(n_ctx, tokens * bpt, np.int64)
-    s = rng.uniform(0.02, 0.8, size=(n_ctx, M))
+    scorers = ["keydiff", "knorm", "snapkv"]
+    s = rng.uniform(*sensitivity, size=(n_ctx, len(scorers)))
+    u = rng.uniform(0.5, 1.5, size=(n_ctx, len(scorers)))
+    q = np.zeros((n_ctx, M, len(grid)))
     for m, meth in enumerate(space.methods):
-        if "-q" in meth.name:  # lower bit widths cost a little more quality
-            b = int(meth.name.split("-q")[1])
-            s[:, m] = np.minimum(1.0, s[:, m] * (1.0 + 0.5 * (8 - b) / 8))
-    g = np.asarray(grid)
-    q = np.clip(1.0 - s[:, :, None] * ((1.0 - g[None, None, :]) / 0.1), 0.0, 1.0)
-    q[:, :, -1] = 1.0
+        sc = scorers.index(meth.name.split("-")[0])
+        for gi, r in enumerate(grid):
+            bits, keep = codec_bits_keep(meth.name, r)
+            drop = s[:, sc] * ((1.0 - keep) / 0.1) ** shape_k
+            qloss = 0.0 if bits == 16 else QUANT_LOSS[bits] * u[:, sc]
+            q[:, m, gi] = np.clip(1.0 - drop - qloss, 0.0, 1.0)
     ranks = rng.permutation(n_ctx)
     w = 1.0 / (ranks + 1.0)
     freq = 4.0 * w / w.sum()

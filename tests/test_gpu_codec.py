@@ -56,6 +56,9 @@ def gen(eng, s, seed=9, ctx=3, on_gpu=True):
 
 
 SHAPES = [A.KvShape(2, 2, 300, 128), A.KvShape(1, 3, 1000, 128), A.KvShape(3, 1, 129, 128)]
+# compress also at Llama chunk length (T = 8192: 1024 tokens per cluster CTA),
+# a ragged length and a length below the cluster size
+PACK_SHAPES = SHAPES + [A.KvShape(1, 2, 8192, 128), A.KvShape(2, 1, 4097, 128), A.KvShape(1, 1, 5, 128)]
 
 
 @pytest.mark.parametrize("si", range(len(SHAPES)))
@@ -161,11 +164,19 @@ def blob_sections(b, m, bits):
     return out
 
 
-@pytest.mark.parametrize("si", range(len(SHAPES)))
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "unfused"])
+@pytest.mark.parametrize("si", range(len(PACK_SHAPES)))
 @pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.3), ("keydiff-q4", 0.2), ("knorm-q2", 0.1),
-                                          ("keydiff", 0.4), ("knorm-q4", 0.02), ("knorm-q8", 0.5)])
-def test_compress_unpack_bitexact(gpu, orc, si, method, ratio):
-    s = SHAPES[si]
+                                          ("keydiff", 0.4), ("knorm-q4", 0.02), ("knorm-q8", 0.5),
+                                          ("keydiff-q8", 1.0), ("knorm", 1.0)])
+def test_compress_unpack_bitexact(gpu, orc, si, method, ratio, fused, monkeypatch):
+    """compress = scores + top-k + pack; `fused` is the one-launch cluster
+    kernel (knorm/keydiff), `unfused` the three-phase kernels."""
+    if fused:
+        monkeypatch.delenv("KVT_UNFUSED", raising=False)
+    else:
+        monkeypatch.setenv("KVT_UNFUSED", "1")
+    s = PACK_SHAPES[si]
     kg, vg = gen(gpu, s)
     ko, vo = gen(orc, s, on_gpu=False)
     cfg = plan(orc.abi, method, ratio, s)
