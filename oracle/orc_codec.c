@@ -328,47 +328,110 @@ static void keydiff_slice(void* a, int64_t sl) {
   free(inv);
 }
 
+/* snapkv, exact-integer formulation: the
+ * window queries and the prefix keys are quantised to int8 per row (absmax /
+ * 127), so every logit is an exact integer dot product times two fp32
+ * scales; exp2 is a fixed mul/add polynomial, and every sum is an integer.
+ * Only IEEE single ops with a fixed association appear, so the CUDA path
+ * (integer tensor cores) reproduces it bit for bit. */
+#define SNAP_C0 0.12751743082459868f /* log2(e) / sqrt(128) */
+#define SNAP_P0 1.535336188319500E-4f /* 2^f on [-1/2, 1/2] (Cephes exp2f) */
+#define SNAP_P1 1.339887440266574E-3f
+#define SNAP_P2 9.618437357674640E-3f
+#define SNAP_P3 5.550332471162809E-2f
+#define SNAP_P4 2.402264791363012E-1f
+#define SNAP_P5 6.931472028550421E-1f
+
+/* int8 row quantisation: returns the scale absmax/127, writes the codes */
+static float quant_row_i8(const float* x, int8_t* q) {
+  float a = 0.0f;
+  for (int d = 0; d < D_HEAD; ++d) {
+    const float v = fabsf(x[d]);
+    a = v > a ? v : a;
+  }
+  if (a == 0.0f) {
+    memset(q, 0, D_HEAD);
+    return 0.0f;
+  }
+  const float inv = 127.0f / a;
+  for (int d = 0; d < D_HEAD; ++d) {
+    float r = nearbyintf(x[d] * inv);
+    r = r > 127.0f ? 127.0f : (r < -127.0f ? -127.0f : r);
+    q[d] = (int8_t)r;
+  }
+  return a / 127.0f;
+}
+
+/* round(2^22 * 2^d) for d <= 0, 0 below d = -30 */
+static uint32_t snap_exp_fx(float d) {
+  if (d < -30.0f) return 0u;
+  const float n = nearbyintf(d);
+  const float f = d - n;
+  float p = SNAP_P0;
+  p = p * f + SNAP_P1;
+  p = p * f + SNAP_P2;
+  p = p * f + SNAP_P3;
+  p = p * f + SNAP_P4;
+  p = p * f + SNAP_P5;
+  p = p * f + 1.0f;
+  const float x = ldexpf(p, 22 + (int)n);
+  return (uint32_t)nearbyintf(x);
+}
+
 static void snapkv_slice(void* a, int64_t sl) {
   score_job_t* J = (score_job_t*)a;
   const kvt_kv_shape* s = J->s;
   const kvt_codec_cfg* c = J->c;
-  const int T = s->T, W = c->window, G = c->q_heads, P = T - W, rows = W * G;
+  const int T = s->T, W = c->window, G = c->q_heads, P = T - W, R = W * G;
   const int l = (int)(sl / s->H), h = (int)(sl % s->H);
   const uint16_t* K = J->k + (size_t)sl * T * D_HEAD;
   float* out = J->scores + (size_t)sl * T;
-  for (int t = P; t < T; ++t) out[t] = INFINITY; /* window always kept */
+  for (int t = P > 0 ? P : 0; t < T; ++t) out[t] = INFINITY; /* window always kept */
   if (P <= 0) return;
-  double* q = (double*)malloc(sizeof(double) * (size_t)rows * D_HEAD);
+  int8_t* q8 = (int8_t*)malloc((size_t)R * D_HEAD);
+  float* cr = (float*)malloc(sizeof(float) * (size_t)R);
+  float row[D_HEAD];
   for (int g = 0; g < G; ++g)
-    for (int w = 0; w < W; ++w)
-      for (int d = 0; d < D_HEAD; ++d)
-        q[((size_t)g * W + w) * D_HEAD + d] = (double)bf2f(synth_q(s, c, l, h * G + g, w, d));
-  double* logit = (double*)malloc(sizeof(double) * (size_t)rows * P);
-  const double inv_sqrt_d = 1.0 / sqrt((double)D_HEAD);
-  for (int r = 0; r < rows; ++r)
-    for (int t = 0; t < P; ++t) {
-      double acc = 0.0;
-      for (int d = 0; d < D_HEAD; ++d) acc += q[(size_t)r * D_HEAD + d] * (double)bf2f(K[(size_t)t * D_HEAD + d]);
-      logit[(size_t)r * P + t] = acc * inv_sqrt_d;
+    for (int w = 0; w < W; ++w) {
+      const int r = g * W + w;
+      for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(synth_q(s, c, l, h * G + g, w, d));
+      cr[r] = quant_row_i8(row, q8 + (size_t)r * D_HEAD) * SNAP_C0;
     }
-  double* vote = (double*)calloc((size_t)P, sizeof(double));
-  for (int r = 0; r < rows; ++r) {
-    const double* lr = logit + (size_t)r * P;
-    double m = lr[0];
-    for (int t = 1; t < P; ++t) m = lr[t] > m ? lr[t] : m;
-    double sum = 0.0;
-    for (int t = 0; t < P; ++t) sum += exp(lr[t] - m);
-    for (int t = 0; t < P; ++t) vote[t] += exp(lr[t] - m) / sum;
+  int8_t* k8 = (int8_t*)malloc((size_t)P * D_HEAD);
+  float* tau = (float*)malloc(sizeof(float) * (size_t)P);
+  for (int t = 0; t < P; ++t) {
+    for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(K[(size_t)t * D_HEAD + d]);
+    tau[t] = quant_row_i8(row, k8 + (size_t)t * D_HEAD);
+  }
+  float* y = (float*)malloc(sizeof(float) * (size_t)R * P);
+  for (int r = 0; r < R; ++r)
+    for (int t = 0; t < P; ++t) {
+      int32_t acc = 0;
+      for (int d = 0; d < D_HEAD; ++d) acc += (int32_t)q8[(size_t)r * D_HEAD + d] * (int32_t)k8[(size_t)t * D_HEAD + d];
+      y[(size_t)r * P + t] = ((float)acc * tau[t]) * cr[r];
+    }
+  uint64_t* vote = (uint64_t*)calloc((size_t)P, sizeof(uint64_t));
+  for (int r = 0; r < R; ++r) {
+    const float* yr = y + (size_t)r * P;
+    float m = yr[0];
+    for (int t = 1; t < P; ++t) m = yr[t] > m ? yr[t] : m;
+    uint64_t L = 0;
+    for (int t = 0; t < P; ++t) L += snap_exp_fx(yr[t] - m);
+    const uint64_t w = (1ull << 46) / L;
+    for (int t = 0; t < P; ++t) vote[t] += (uint64_t)snap_exp_fx(yr[t] - m) * w;
   }
   const int half = c->pool / 2;
   for (int t = 0; t < P; ++t) {
-    double m = vote[t];
+    uint64_t m = vote[t];
     for (int j = t - half; j <= t + half; ++j)
       if (j >= 0 && j < P && vote[j] > m) m = vote[j];
-    out[t] = (float)m;
+    out[t] = (float)m * 1.4210854715202004e-14f; /* 2^-46 */
   }
-  free(q);
-  free(logit);
+  free(q8);
+  free(cr);
+  free(k8);
+  free(tau);
+  free(y);
   free(vote);
 }
 
@@ -451,6 +514,8 @@ typedef struct {
 static qparam_t make_param(float mn, float mx, int bits) {
   qparam_t p;
   const float levels = (float)((1 << bits) - 1);
+  mn = mn + 0.0f; /* -0 -> +0: independent of which zero the min/max scan kept */
+  mx = mx + 0.0f;
   const float scale = (mx - mn) / levels;
   p.s16 = f2h(scale);
   p.z16 = f2h(mn);

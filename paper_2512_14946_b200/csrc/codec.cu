@@ -22,9 +22,11 @@
 #include <cub/block/block_scan.cuh>
 
 #include "codec_common.cuh"
+#include "sm100.cuh"
 #include "kvt_common.cuh"
 
 using namespace kvt;
+namespace cg = cooperative_groups;
 
 
 
@@ -138,6 +140,49 @@ extern "C" int kvt_kv_generate(kvt_handle* h, const kvt_kv_shape* s, uint64_t se
   return KVT_OK;
 }
 
+// ------------------------------------------- K rows through a smem ring
+constexpr int kRingStages = 4;  // K streamed through smem in 64-token (16 KB) bulk-copy stages
+constexpr int kRingRows = 64;
+constexpr size_t kRingBytes = size_t(kRingStages) * kRingRows * 256;
+
+// Streams rows [0, n) of `src` (256 B each) through the smem ring; calls
+// f(t, row) once per row from the half-warp that owns it (16 lanes, one
+// uint4 each). `seq` counts ring chunks across calls (mbarrier parity).
+// Block-uniform; warp-uniform trip counts (f may use half-warp shuffles).
+template <class F>
+__device__ __forceinline__ void stream_rows(const uint4* __restrict__ src, int n, uint4* ring, uint64_t* full,
+                                            uint32_t& seq, F&& f) {
+  const int tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
+  const int nch = (n + kRingRows - 1) / kRingRows;
+  auto issue = [&](int c) {
+    const int st = (seq + c) % kRingStages;
+    const int rows = min(kRingRows, n - c * kRingRows);
+    mbar_expect_tx(&full[st], rows * 256);
+    bulk_g2s(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
+             rows * 256, &full[st]);
+  };
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem use before async writes
+    for (int c = 0; c < min(nch, kRingStages); ++c) issue(c);
+  }
+  for (int c = 0; c < nch; ++c) {
+    const uint32_t g = seq + c;
+    const int st = g % kRingStages;
+    mbar_wait(&full[st], (g / kRingStages) & 1);
+    const int rows = min(kRingRows, n - c * kRingRows);
+    const uint4* base = ring + static_cast<size_t>(st) * kRingRows * 16;
+#pragma unroll
+    for (int u = 0; u < kRingRows / 16; ++u) {
+      const int r = (hw & ~1) * (kRingRows / 16) + 2 * u + (hw & 1);  // both half-warps of a warp iterate together
+      const uint4 v = r < rows ? base[r * 16 + l16] : make_uint4(0, 0, 0, 0);
+      f(c * kRingRows + r, r < rows, v);
+    }
+    __syncthreads();  // stage consumed by every thread
+    if (tid == 0 && c + kRingStages < nch) issue(c + kRingStages);
+  }
+  seq += nch;
+}
+
 // --------------------------------------------------------------- scores
 
 // Sum of squares of one lane's 8 channels (chunk of the canonical order).
@@ -186,6 +231,13 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
 }
 
 constexpr double kFx = 1099511627776.0;  // 2^40 fixed-point scale
+
+// llrint for |x| < 2^51 without the (slow) F2I.S64 conversion pipe: adding
+// 1.5 * 2^52 rounds to an integer (ties-to-even) in the mantissa.
+__device__ __forceinline__ long long fx_round(double x) {
+  constexpr double kMagic = 6755399441055744.0;
+  return __double_as_longlong(__dadd_rn(x, kMagic)) - 0x4338000000000000LL;
+}
 constexpr int kKdTokens = 256;           // tokens per block (16 half-warps x 16)
 
 // keydiff pass 1: S[slice][d] = sum_t rint(x_td / |x_t| * 2^40) (exact int64)
@@ -208,8 +260,8 @@ __global__ void __launch_bounds__(256) k_keydiff_sum(const uint4* __restrict__ K
     for (int j = 0; j < 4; ++j) {
       const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
       const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-      acc[2 * j] += __double2ll_rn(__dmul_rn(a, kFx));
-      acc[2 * j + 1] += __double2ll_rn(__dmul_rn(b, kFx));
+      acc[2 * j] += fx_round(__dmul_rn(a, kFx));
+      acc[2 * j + 1] += fx_round(__dmul_rn(b, kFx));
     }
   }
 #pragma unroll
@@ -255,92 +307,332 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
   }
 }
 
-// snapkv: observation window of W synthetic queries per
-// q-head (GQA group G), softmax over the prefix, summed over the window and
-// the group, then max-pooled; window tokens always kept (+inf).
-// CUDA-core reference kernel: one block per (layer, kv head), one thread
-// per query row, two passes (row stats, then probabilities).
-constexpr int kSnapTile = 32;
-__global__ void __launch_bounds__(128) k_snapkv_votes(const uint16_t* __restrict__ K, float* __restrict__ vote,
-                                                      int L, int H, int T, int W, int G, uint64_t q_seed) {
-  extern __shared__ float sm[];
-  const int rows = W * G;
-  float* q = sm;                                 // [rows][kD+1]
-  float* kt = q + 128 * (kD + 1);                // [kSnapTile][kD]
-  float* red = kt + kSnapTile * kD;              // [4][kSnapTile]
-  const int slice = blockIdx.x, l = slice / H, h = slice % H;
-  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
-  const int P = T - W;
-  const uint64_t Hq = uint64_t(H) * G;
-  for (int i = threadIdx.x; i < rows * kD; i += blockDim.x) {
-    const int rr = i / kD, d = i % kD, g = rr / W, w = rr % W;
-    const uint64_t idx = ((uint64_t(l) * Hq + uint64_t(h * G + g)) * uint64_t(W) + uint64_t(w)) * kD + d;
-    q[rr * (kD + 1) + d] = bf2f(synth_bf16(q_seed, 0x51ull, idx, d % 16 == 3));
-  }
-  const uint16_t* Ks = K + static_cast<size_t>(slice) * T * kD;
-  const float scale = 1.0f / sqrtf(float(kD));
-  float m = -INFINITY, lsum = 0.0f;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int t0 = 0; t0 < P; t0 += kSnapTile) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < kSnapTile * kD; i += blockDim.x) {
-        const int tt = t0 + i / kD;
-        kt[i] = tt < P ? bf2f(Ks[static_cast<size_t>(tt) * kD + (i % kD)]) : 0.0f;
-      }
-      __syncthreads();
-      const int nt = min(kSnapTile, P - t0);
-      for (int j = 0; j < nt; ++j) {
-        float s = 0.0f;
-        if (r < rows) {
-#pragma unroll 8
-          for (int d = 0; d < kD; ++d) s = fmaf(q[r * (kD + 1) + d], kt[j * kD + d], s);
-          s *= scale;
-        }
-        if (pass == 0) {
-          if (r < rows) {
-            if (s > m) {
-              lsum = lsum * expf(m - s) + 1.0f;
-              m = s;
-            } else {
-              lsum += expf(s - m);
-            }
-          }
-        } else {
-          float p = r < rows ? expf(s - m) / lsum : 0.0f;
+// snapkv on the integer tensor cores, exact-integer spec of
+// DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): the R = W x G window
+// queries and the prefix keys are quantised to int8 per row, so every logit
+// is an exact s8 x s8 -> s32 dot product (tcgen05.mma kind::i8, M = N = 128,
+// K = 128) times two fp32 scales; exp2 is a fixed mul/add polynomial and all
+// sums are integers, so the result is bit-identical to the CPU oracle.
+//
+// One thread-block cluster per (layer, kv-head) slice; CTA `rank` owns
+// `tpc` 128-token tiles of the prefix and keeps them as int8 in smem (SW128
+// K-major UMMA layout, 16 KB per tile) for three passes over the logits:
+//   1. row max m_r            (D[r][t] = Q8 . K8^T, TMEM lane = query row)
+//   2. row sum L_r of E_rt    (same orientation), w_r = floor(2^46 / L_r)
+//   3. vote V_t = sum_r E_rt w_r  (D[t][r] = K8 . Q8^T, TMEM lane = token)
+// The MMA of tile j+1 runs while the 8 epilogue warps drain tile j (two
+// 128-column TMEM accumulators). m_r and L_r are combined across the
+// cluster through DSMEM; pooling reads the neighbours' votes the same way.
+constexpr int kSnapTiles = 8;  // tiles per CTA: 8 x 16 KB int8 K
+constexpr int kSnapThreads = 256;
+constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
+
+struct SnapSmem {
+  uint8_t k8[kSnapTiles][128 * 128];  // 1024-aligned (offset 0 of the aligned base)
+  uint8_t q8[128 * 128];
+  uint4 ring[kRingStages * kRingRows * 16];  // bf16 K staging; reused for the votes
+  float tau[kSnapTiles * 128];
+  float cr[128], mr[128], mcl[128];
+  uint32_t wr[128];
+  float red_f[2][128];
+  unsigned long long red_u[2][128], lcl[128];
+  uint64_t full[kRingStages], mma_bar[2];
+  uint32_t tmem_base;
+};
+
+// round(2^22 * 2^d) for d <= 0, 0 below -30: fixed mul/add polynomial for
+// 2^f on [-1/2, 1/2] (Cephes exp2f), n = rint(d) via the 1.5*2^23 trick,
+// exact 2^(22+n) scaling on the exponent bits, rint via 2^23.
+__device__ __forceinline__ uint32_t snap_exp_fx(float d) {
+  const float t = __fadd_rn(d, 12582912.0f);
+  const float n = __fsub_rn(t, 12582912.0f);
+  const float f = __fsub_rn(d, n);
+  float p = 1.535336188319500E-4f;
+  p = __fadd_rn(__fmul_rn(p, f), 1.339887440266574E-3f);
+  p = __fadd_rn(__fmul_rn(p, f), 9.618437357674640E-3f);
+  p = __fadd_rn(__fmul_rn(p, f), 5.550332471162809E-2f);
+  p = __fadd_rn(__fmul_rn(p, f), 2.402264791363012E-1f);
+  p = __fadd_rn(__fmul_rn(p, f), 6.931472028550421E-1f);
+  p = __fadd_rn(__fmul_rn(p, f), 1.0f);
+  const int ni = __float_as_int(t) - 0x4B400000;
+  const float x = __int_as_float(__float_as_int(p) + ((22 + ni) << 23));
+  const uint32_t e = __float_as_uint(__fadd_rn(x, 8388608.0f)) - 0x4B000000u;
+  return d < -30.0f ? 0u : e;
+}
+
+// |I| < 2^22: exact int -> float without the conversion pipe
+__device__ __forceinline__ float i2f_exact(uint32_t i) {
+  return __fsub_rn(__int_as_float(static_cast<int>(i) + 0x4B400000), 12582912.0f);
+}
+
+// Half-warp int8 quantisation of one 128-channel row (lane: channels
+// 8*l16..8*l16+7): absmax/127 scale, rint(x * (127/absmax)) codes written to
+// row r of a SW128 K-major tile. Returns the scale. Warp-uniform.
+__device__ __forceinline__ float quant_row_i8(const float (&x)[8], uint8_t* tile, int r, int l16) {
+  float a = 0.0f;
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-          if (lane == 0) red[warp * kSnapTile + j] = p;
+  for (int e = 0; e < 8; ++e) a = fmaxf(a, fabsf(x[e]));
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+  const float inv = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float y = fminf(fmaxf(__fmul_rn(x[e], inv), -127.0f), 127.0f);
+    const uint32_t c = (__float_as_uint(__fadd_rn(y, 12582912.0f)) - 0x4B400000u) & 0xffu;
+    if (e < 4) lo |= c << (8 * e);
+    else hi |= c << (8 * (e - 4));
+  }
+  const int chunk = l16 >> 1;
+  *reinterpret_cast<uint2*>(tile + r * 128 + ((chunk ^ (r & 7)) << 4) + (l16 & 1) * 8) = make_uint2(lo, hi);
+  return a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
+}
+
+__global__ void __launch_bounds__(kSnapThreads, 1)
+    k_snapkv_tc(const uint4* __restrict__ K, float* __restrict__ scores, int H, int T, int W, int G, int pool,
+                uint64_t q_seed, int tpc) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  const int slice = blockIdx.y, l = slice / H, h = slice % H;
+  const int P = T - W, R = W * G;
+  const int ntiles = (P + 127) / 128;
+  const int tile0 = rank * tpc, ntl = max(0, min(tpc, ntiles - tile0));
+  const int t_lo = tile0 * 128, n_loc = max(0, min(P - t_lo, ntl * 128));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, l16 = tid & 15, hw = tid >> 4;
+  extern __shared__ uint8_t snap_raw[];
+  SnapSmem& sm = *reinterpret_cast<SnapSmem*>((reinterpret_cast<uintptr_t>(snap_raw) + 1023) & ~uintptr_t(1023));
+  float* out = scores + static_cast<size_t>(slice) * T;
+
+  if (tid == 0) {
+    for (int i = 0; i < kRingStages; ++i) mbar_init(&sm.full[i], 1);
+    mbar_init(&sm.mma_bar[0], 1);
+    mbar_init(&sm.mma_bar[1], 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  // ---- Q8: synthetic window queries, half-warp per row (rows >= R are zero)
+  const uint64_t Hq = uint64_t(H) * G;
+  for (int r = hw; r < 128; r += 16) {
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int d = l16 * 8 + e;
+      float v = 0.0f;
+      if (r < R) {
+        const int g = r / W, w = r - g * W;
+        const uint64_t idx = ((uint64_t(l) * Hq + uint64_t(h * G + g)) * uint64_t(W) + uint64_t(w)) * kD + d;
+        v = bf2f(synth_bf16(q_seed, 0x51ull, idx, d % 16 == 3));
+      }
+      x[e] = v;
+    }
+    const float sc = quant_row_i8(x, sm.q8, r, l16);
+    if (l16 == 0) sm.cr[r] = __fmul_rn(sc, kSnapC0);
+  }
+  // ---- K8: stream this CTA's prefix tokens, quantise per token into the tiles
+  uint32_t seq = 0;
+  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+  stream_rows(Ks, n_loc, sm.ring, sm.full, seq, [&](int t, bool live, const uint4& v) {
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+    float x[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[2 * q] = bf_lo(w4[q]);
+      x[2 * q + 1] = bf_hi(w4[q]);
+    }
+    if (t < ntl * 128) {  // rows past the prefix: zeros (live == false)
+      const float sc = quant_row_i8(x, sm.k8[t >> 7], t & 127, l16);
+      if (l16 == 0) sm.tau[t] = live ? sc : 0.0f;
+    }
+  });
+  for (int t0 = ((n_loc + kRingRows - 1) / kRingRows) * kRingRows + (hw & ~1); t0 < ntl * 128; t0 += 16) {
+    const int t = t0 + (hw & 1);  // tail of the last tile: zero rows
+    float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    quant_row_i8(x, sm.k8[t >> 7], t & 127, l16);
+    if (l16 == 0) sm.tau[t] = 0.0f;
+  }
+  fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+  __syncthreads();
+
+  // ---- three passes over the logits
+  constexpr uint32_t kIdesc = idesc_i8(128, 128);
+  uint32_t uses[2] = {0, 0};
+  const int quad = warp & 3, colh = warp >> 2;  // TMEM lanes 32*quad.., columns 64*colh..
+  auto run_pass = [&](bool tok_major, auto&& epi) {
+    auto issue = [&](int j) {
+      tc_fence_after();  // order after the barrier that freed accumulator j & 1
+      const uint64_t dk = umma_desc_sw128(sm.k8[j]), dq = umma_desc_sw128(sm.q8);
+      const uint64_t da = tok_major ? dk : dq, db = tok_major ? dq : dk;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + (j & 1) * 128, da + 2 * ks, db + 2 * ks, kIdesc, ks > 0);
+      umma_commit(&sm.mma_bar[j & 1]);
+    };
+    if (ntl > 0 && tid == 0) issue(0);
+    for (int j = 0; j < ntl; ++j) {
+      if (tid == 0 && j + 1 < ntl) issue(j + 1);
+      const int b = j & 1;
+      mbar_wait(&sm.mma_bar[b], uses[b] & 1);
+      ++uses[b];
+      tc_fence_after();
+      epi(j, tmem + b * 128 + (uint32_t(quad * 32) << 16) + colh * 64);
+      tc_fence_before();
+      __syncthreads();  // accumulator b drained: tile j + 2 may overwrite it
+    }
+  };
+  const int r_row = quad * 32 + lane;  // passes 1-2: this thread's query row
+
+  // pass 1: row max
+  {
+    const float c_r = sm.cr[r_row];
+    float mx = -INFINITY;
+    run_pass(false, [&](int j, uint32_t taddr) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t I[32];
+        tmem_ld32(taddr + cc * 32, I);
+        const int tb = j * 128 + colh * 64 + cc * 32;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), sm.tau[tb + i]), c_r);
+          if (tb + i < n_loc) mx = fmaxf(mx, y);
         }
       }
-      if (pass == 1) {
-        __syncthreads();
-        if (threadIdx.x < nt) {
-          const float v = red[threadIdx.x] + red[kSnapTile + threadIdx.x] + red[2 * kSnapTile + threadIdx.x] +
-                          red[3 * kSnapTile + threadIdx.x];
-          vote[static_cast<size_t>(slice) * T + t0 + threadIdx.x] = v;
+    });
+    sm.red_f[colh][r_row] = mx;
+    __syncthreads();
+    if (tid < 128) sm.mcl[tid] = fmaxf(sm.red_f[0][tid], sm.red_f[1][tid]);
+    cl.sync();
+    if (tid < 128) {
+      float m = -INFINITY;
+      for (int c = 0; c < C; ++c) m = fmaxf(m, cl.map_shared_rank(sm.mcl, c)[tid]);
+      sm.mr[tid] = m;
+    }
+    __syncthreads();
+  }
+  // pass 2: row sums of E, then w_r
+  {
+    const float c_r = sm.cr[r_row], m_r = sm.mr[r_row];
+    unsigned long long Ls = 0;
+    run_pass(false, [&](int j, uint32_t taddr) {
+      uint32_t part = 0;  // <= 64 x 2^22: no overflow
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t I[32];
+        tmem_ld32(taddr + cc * 32, I);
+        const int tb = j * 128 + colh * 64 + cc * 32;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), sm.tau[tb + i]), c_r);
+          const uint32_t e = snap_exp_fx(__fsub_rn(y, m_r));
+          if (tb + i < n_loc) part += e;
         }
+      }
+      Ls += part;
+    });
+    sm.red_u[colh][r_row] = Ls;
+    __syncthreads();
+    if (tid < 128) sm.lcl[tid] = sm.red_u[0][tid] + sm.red_u[1][tid];
+    cl.sync();
+    if (tid < 128) {
+      unsigned long long L = 0;
+      for (int c = 0; c < C; ++c) L += cl.map_shared_rank(sm.lcl, c)[tid];
+      sm.wr[tid] = tid < R ? static_cast<uint32_t>((1ull << 46) / L) : 0u;
+    }
+    __syncthreads();
+  }
+  // pass 3: votes (token-major accumulators)
+  unsigned long long* vote = reinterpret_cast<unsigned long long*>(sm.ring);
+  run_pass(true, [&](int j, uint32_t taddr) {
+    const int tl = j * 128 + quad * 32 + lane;
+    const float tau_t = sm.tau[tl];
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      uint32_t I[32];
+      tmem_ld32(taddr + cc * 32, I);
+      const int rb = colh * 64 + cc * 32;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), tau_t), sm.cr[rb + i]);
+        const uint32_t e = snap_exp_fx(__fsub_rn(y, sm.mr[rb + i]));
+        acc += static_cast<unsigned long long>(e) * sm.wr[rb + i];
       }
     }
+    sm.red_u[colh][quad * 32 + lane] = acc;
+    __syncthreads();
+    if (tid < 128) vote[j * 128 + tid] = sm.red_u[0][tid] + sm.red_u[1][tid];
+  });
+  cl.sync();  // every CTA's votes visible
+  // ---- pooling (max over +-pool/2 within the prefix) and scores
+  const int half = pool / 2;
+  for (int tl = tid; tl < n_loc; tl += kSnapThreads) {
+    unsigned long long m = 0;
+    for (int dj = -half; dj <= half; ++dj) {
+      const int tg = t_lo + tl + dj;  // global token
+      if (tg < 0 || tg >= P) continue;
+      const int owner = (tg / 128) / tpc;
+      const int tr = tg - owner * tpc * 128;
+      const unsigned long long* vv =
+          owner == rank ? vote : cl.map_shared_rank(reinterpret_cast<unsigned long long*>(sm.ring), owner);
+      const unsigned long long v = vv[tr];
+      m = v > m ? v : m;
+    }
+    out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 1.4210854715202004e-14f);  // 2^-46 (exact)
   }
+  if (rank == C - 1)
+    for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
+  cl.sync();  // no CTA leaves while its votes may still be read
+  if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
-__global__ void __launch_bounds__(256) k_snapkv_pool(const float* __restrict__ vote, float* __restrict__ out, int T,
-                                                     int W, int pool) {
-  const int slice = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const int P = T - W, half = pool / 2;
-  const float* v = vote + static_cast<size_t>(slice) * T;
-  float r;
-  if (t >= P) {
-    r = INFINITY;
-  } else {
-    r = v[t];
-    for (int j = max(0, t - half); j <= min(P - 1, t + half); ++j) r = fmaxf(r, v[j]);
-  }
-  out[static_cast<size_t>(slice) * T + t] = r;
+__global__ void k_fill_inf(float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) out[i] = INFINITY;
 }
 
+static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
+                         float* scores) {
+  const int S = s->L * s->H, T = s->T, W = c->window, G = c->q_heads;
+  if (W * G > 128 || W > T || W < 0 || G < 1) return set_error(KVT_EINVAL, "snapkv window x q_heads must be <= 128");
+  if (c->pool < 1 || (c->pool & 1) == 0) return set_error(KVT_EINVAL, "snapkv pool must be odd");
+  const int P = T - W;
+  if (P <= 0) {
+    const long long n = static_cast<long long>(S) * T;
+    k_fill_inf<<<static_cast<int>(std::min<long long>((n + 255) / 256, num_sms() * 8LL)), 256, 0, h->stream>>>(scores, n);
+    LAUNCHED(h);
+    return KVT_OK;
+  }
+  const int ntiles = (P + 127) / 128;
+  const int C = (ntiles + kSnapTiles - 1) / kSnapTiles;
+  if (C > 16) return set_error(KVT_EINVAL, "snapkv: prefix longer than 16 x 8 x 128 tokens is not supported");
+  const int tpc = (ntiles + C - 1) / C;
+  const size_t smem = sizeof(SnapSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, S);
+  cfg.blockDim = dim3(kSnapThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_snapkv_tc, reinterpret_cast<const uint4*>(k), scores, s->H, T, W, G,
+                                  c->pool, static_cast<uint64_t>(c->q_seed), tpc));
+  LAUNCHED(h);
+  return KVT_OK;
+}
 static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
                          float* scores, float* votes, unsigned long long* fixed) {
   const int S = s->L * s->H, T = s->T;
@@ -360,18 +652,7 @@ static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
                                           reinterpret_cast<const long long*>(fixed), scores, T);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_SNAPKV) {
-    if (c->window * c->q_heads > 128 || c->window > T) return set_error(KVT_EINVAL, "snapkv window too large");
-    const size_t smem = sizeof(float) * (128 * (kD + 1) + kSnapTile * kD + 4 * kSnapTile);
-    static bool attr = false;
-    if (!attr) {
-      KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_votes, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr = true;
-    }
-    k_snapkv_votes<<<S, 128, smem, st>>>(k, votes, s->L, s->H, T, c->window, c->q_heads, c->q_seed);
-    LAUNCHED(h);
-    dim3 grid((T + 255) / 256, S);
-    k_snapkv_pool<<<grid, 256, 0, st>>>(votes, scores, T, c->window, c->pool);
-    LAUNCHED(h);
+    return launch_snapkv(h, s, c, k, scores);
   } else {
     return set_error(KVT_EINVAL, "unknown scorer");
   }
@@ -400,6 +681,42 @@ extern "C" int kvt_token_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_
 
 // ------------------------------------------------------------------ top-k
 
+// Radix-select bucket choice, one warp: scanning bins 255 -> 1, the first
+// bin b whose count reaches `rem` (else bin 0), and what remains of `rem`
+// inside it. Same result as the sequential scan
+//   for (b = 255; b > 0 && hist[b] < rem; --b) rem -= hist[b];
+// but as 8 bins per lane + a warp prefix sum instead of 256 dependent loads.
+__device__ __forceinline__ void select_bucket(const int* hist, int rem, int* b_out, int* rem_out) {
+  const int lane = threadIdx.x & 31;
+  int c[8], s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    c[i] = hist[255 - 8 * lane - i];
+    s += c[i];
+  }
+  int incl = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, incl >= rem);
+  const int L = hit ? __ffs(hit) - 1 : 31;
+  if (lane == L) {
+    int r = rem - (incl - s), b = 255 - 8 * lane;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (b - i == 0 || c[i] >= r) {
+        b -= i;
+        break;
+      }
+      r -= c[i];
+    }
+    *b_out = b;
+    *rem_out = r;
+  }
+}
+
 constexpr int kTopkThreads = 512;
 using TopkScan = cub::BlockScan<int, kTopkThreads>;
 
@@ -411,7 +728,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   extern __shared__ uint32_t skeys[];
   __shared__ int hist[256];
   __shared__ uint32_t s_prefix, s_mask;
-  __shared__ int s_remaining;
+  __shared__ int s_remaining, s_bucket, s_remaining_next;
   __shared__ typename TopkScan::TempStorage scan_tmp;
   const int slice = blockIdx.x, tid = threadIdx.x;
   const float* sc = scores + static_cast<size_t>(slice) * T;
@@ -432,14 +749,11 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
     }
     __syncthreads();
+    if (tid < 32) select_bucket(hist, s_remaining, &s_bucket, &s_remaining_next);
+    __syncthreads();
     if (tid == 0) {
-      int rem = s_remaining, b = 255;
-      for (; b > 0; --b) {
-        if (hist[b] >= rem) break;
-        rem -= hist[b];
-      }
-      s_remaining = rem;
-      s_prefix = prefix | (uint32_t(b) << shift);
+      s_remaining = s_remaining_next;
+      s_prefix = prefix | (uint32_t(s_bucket) << shift);
       s_mask = mask | (255u << shift);
     }
     __syncthreads();
@@ -512,67 +826,114 @@ __global__ void __launch_bounds__(256) k_gather16(const uint4* __restrict__ K, c
   if (l16 == 0) oidx[static_cast<size_t>(slice) * k + j] = t;
 }
 
-// K quantisation: per channel over a group of <=128 kept tokens. The whole
-// block (256 threads) packs group g of one slice: rows staged in smem,
-// channel min/max split over two thread halves, codes packed row-wise with
-// coalesced stores. Block-uniform: call from every thread.
+// K quantisation: per channel over a group of <=128 kept tokens, one
+// 256-thread block per group. Thread (rs, cg) = rows 8rs..8rs+7 x channels
+// 8cg..8cg+7 held in registers (8 independent 16-byte loads in flight per
+// thread, no smem staging). Channel min/max: packed bf16x2 mins (max as the
+// min of negated values, exact) -> lane^16 shuffle -> smem over the 8 warps.
+// 128 threads make the per-channel fp16 params, then every thread quantises
+// its 64 values with packed fp32x2 math and writes whole code words.
+// Block-uniform: call from every thread of a 256-thread block.
 struct PackKSmem {
-  uint4 rows[KVT_QGROUP][16];        // 32 KB bf16 tile
-  uint8_t codes[KVT_QGROUP][kD + 4];
-  float pmn[2][kD], pmx[2][kD];
-  QParam prm[kD];
+  uint32_t red[8][16][8];  // [warp][cg][pair: 4 min | 4 -max] bf16x2
+  float zf[kD], inv[kD];
 };
 
 __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
                                              uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
                                              uint16_t* __restrict__ kz, int T, int k, int bits, int slice, int g,
                                              PackKSmem& sm) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rs = tid >> 4, cg = tid & 15;
   const int j0 = g * KVT_QGROUP, nr = min(KVT_QGROUP, k - j0);
   const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
   const int32_t* ix = idx + static_cast<size_t>(slice) * k + j0;
-  for (int i = tid; i < nr * 16; i += 256) {
-    const int r = i >> 4, l16 = i & 15;
-    sm.rows[r][l16] = __ldcs(K + (static_cast<size_t>(slice) * T + ix[r]) * 16 + l16);
+  const uint4* Ks = K + static_cast<size_t>(slice) * T * 16 + cg;
+  uint4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rs * 8 + i;
+    v[i] = r < nr ? __ldcs(Ks + static_cast<size_t>(ix[r]) * 16) : make_uint4(0, 0, 0, 0);
   }
-  __syncthreads();
-  const int d = tid & (kD - 1), half = tid >> 7;
-  const uint16_t* tile = reinterpret_cast<const uint16_t*>(sm.rows);
-  {
-    const int r0 = half * 64, r1 = min(nr, r0 + 64);
-    float mn = INFINITY, mx = -INFINITY;
-    for (int r = r0; r < r1; ++r) {
-      const float x = bf2f(tile[r * kD + d]);
-      mn = x < mn ? x : mn;
-      mx = x > mx ? x : mx;
+  const uint32_t kInf2 = 0x7f807f80u, kNeg = 0x80008000u;
+  uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, nmx[4] = {kInf2, kInf2, kInf2, kInf2};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (rs * 8 + i < nr) {
+      const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mn[q] = bmin2(mn[q], w[q]);
+        nmx[q] = bmin2(nmx[q], w[q] ^ kNeg);
+      }
     }
-    sm.pmn[half][d] = mn;
-    sm.pmx[half][d] = mx;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    mn[q] = bmin2(mn[q], __shfl_xor_sync(0xffffffffu, mn[q], 16));
+    nmx[q] = bmin2(nmx[q], __shfl_xor_sync(0xffffffffu, nmx[q], 16));
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sm.red[warp][cg][q] = mn[q];
+      sm.red[warp][cg][4 + q] = nmx[q];
+    }
   }
   __syncthreads();
-  if (half == 0) {
-    const float mn = sm.pmn[1][d] < sm.pmn[0][d] ? sm.pmn[1][d] : sm.pmn[0][d];
-    const float mx = sm.pmx[1][d] > sm.pmx[0][d] ? sm.pmx[1][d] : sm.pmx[0][d];
-    const QParam p = make_param(mn, mx, bits);
-    sm.prm[d] = p;
-    const size_t po = (static_cast<size_t>(slice) * ng + g) * kD + d;
+  if (tid < kD) {
+    const int c = tid >> 3, q = (tid & 7) >> 1, hi = tid & 1;
+    uint32_t a = sm.red[0][c][q], b = sm.red[0][c][4 + q];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      a = bmin2(a, sm.red[w][c][q]);
+      b = bmin2(b, sm.red[w][c][4 + q]);
+    }
+    const float fmn = hi ? bf_hi(a) : bf_lo(a);
+    const float fmx = -(hi ? bf_hi(b) : bf_lo(b));
+    const QParam p = make_param(fmn, fmx, bits);
+    sm.zf[tid] = p.zf;
+    sm.inv[tid] = p.inv;
+    const size_t po = (static_cast<size_t>(slice) * ng + g) * kD + tid;
     ks[po] = p.s16;
     kz[po] = p.z16;
   }
   __syncthreads();
-  {
-    const QParam p = sm.prm[d];
-    const int r0 = half * 64, r1 = min(nr, r0 + 64);
-    for (int r = r0; r < r1; ++r) sm.codes[r][d] = static_cast<uint8_t>(quant(bf2f(tile[r * kD + d]), p, bits));
+  float z[8], iv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    z[e] = sm.zf[cg * 8 + e];
+    iv[e] = sm.inv[cg * 8 + e];
   }
-  __syncthreads();
-  const int wpr = kD * bits / 32, per = 32 / bits;
-  uint32_t* out = kc + (static_cast<size_t>(slice) * k + j0) * wpr;
-  for (int i = tid; i < nr * wpr; i += 256) {
-    const int r = i / wpr, w = i - r * wpr;
-    uint32_t word = 0;
-    for (int q = 0; q < per; ++q) word |= uint32_t(sm.codes[r][w * per + q]) << (bits * q);
-    out[i] = word;
+  const float hiv = float((1 << bits) - 1);
+  const int wpr = kD * bits / 32;
+  uint32_t* out = kc + static_cast<size_t>(slice) * k * wpr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rs * 8 + i;
+    const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    uint32_t c[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      quant2(bf_lo(w[q]), bf_hi(w[q]), z[2 * q], z[2 * q + 1], iv[2 * q], iv[2 * q + 1], hiv, c[2 * q], c[2 * q + 1]);
+    uint32_t* orow = out + static_cast<size_t>(j0 + r) * wpr;
+    if (bits == 8) {
+      if (r < nr)
+        __stcs(reinterpret_cast<uint2*>(orow) + cg,
+               make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
+                          c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
+    } else if (bits == 4) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) word |= c[e] << (4 * e);
+      if (r < nr) __stcs(orow + cg, word);
+    } else {  // 2 bits: channels 16w..16w+15 = lanes cg (even) and cg + 1
+      uint32_t h = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) h |= c[e] << (2 * e);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+      if (r < nr && (cg & 1) == 0) __stcs(orow + (cg >> 1), h | (other << 16));
+    }
   }
   __syncthreads();  // smem reused by the next group
 }
@@ -580,73 +941,92 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
 __global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
                                                 uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
                                                 uint16_t* __restrict__ kz, int T, int k, int bits) {
-  extern __shared__ uint4 pack_smem[];
-  pack_k_group(K, idx, kc, ks, kz, T, k, bits, blockIdx.y, blockIdx.x, *reinterpret_cast<PackKSmem*>(pack_smem));
+  __shared__ PackKSmem sm;
+  pack_k_group(K, idx, kc, ks, kz, T, k, bits, blockIdx.y, blockIdx.x, sm);
 }
 
-// V quantisation: per kept token over its 128 channels; half-warp per row.
+// V quantisation: per kept token over its 128 channels. A half-warp packs
+// kVRows rows: loads all of them first (kVRows 16-byte loads in flight per
+// lane), reduces each row's (min, -max) as one bf16x2 butterfly, lane i
+// makes row i's fp16 params (one division per row, not per lane), then the
+// params are shuffled back for the packed fp32x2 quantisation.
 // Warp-uniform: both half-warps must call (shuffles use the full mask).
-__device__ __forceinline__ void pack_v_row(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
-                                           int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
-                                           uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
-                                           int bits, int slice, int j) {
-  const int l16 = threadIdx.x & 15;
-  const bool live = j < k;
-  const int t = live ? idx[static_cast<size_t>(slice) * k + j] : 0;
-  const uint4 v = live ? __ldcs(V + (static_cast<size_t>(slice) * T + t) * 16 + l16) : make_uint4(0, 0, 0, 0);
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  float x[8];
+constexpr int kVRows = 8;
+
+__device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
+                                            int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
+                                            uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
+                                            int bits, int slice, int j_first) {
+  const int l16 = threadIdx.x & 15, base = threadIdx.x & 16;
+  const int32_t* ix = idx + static_cast<size_t>(slice) * k;
+  const uint4* Vs = V + static_cast<size_t>(slice) * T * 16 + l16;
+  int tok[kVRows];
+  uint4 v[kVRows];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    x[2 * i] = bf2f(w[i] & 0xffffu);
-    x[2 * i + 1] = bf2f(w[i] >> 16);
+  for (int i = 0; i < kVRows; ++i) tok[i] = j_first + i < k ? ix[j_first + i] : 0;
+#pragma unroll
+  for (int i = 0; i < kVRows; ++i)
+    v[i] = j_first + i < k ? __ldcs(Vs + static_cast<size_t>(tok[i]) * 16) : make_uint4(0, 0, 0, 0);
+  const uint32_t kNeg = 0x80008000u;
+  uint32_t mm_mine = 0;  // lane i < kVRows: (min, -max) of row i as bf16 pair
+#pragma unroll
+  for (int i = 0; i < kVRows; ++i) {
+    const uint32_t a = bmin2(v[i].x, v[i].y), b = bmin2(v[i].z, v[i].w);
+    const uint32_t m2 = bmin2(a, b);  // per-lane mins of even / odd channels
+    const uint32_t n2 = bmin2(bmin2(v[i].x ^ kNeg, v[i].y ^ kNeg), bmin2(v[i].z ^ kNeg, v[i].w ^ kNeg));
+    // (min, -max) of the lane's 8 channels as one bf16 pair
+    uint32_t mm = bmin2(__byte_perm(m2, n2, 0x5410), __byte_perm(m2, n2, 0x7632));
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) mm = bmin2(mm, __shfl_xor_sync(0xffffffffu, mm, off));
+    if (l16 == i) mm_mine = mm;
   }
-  float mn = x[0], mx = x[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) {
-    mn = x[i] < mn ? x[i] : mn;
-    mx = x[i] > mx ? x[i] : mx;
+  QParam p{};
+  if (l16 < kVRows) p = make_param(bf_lo(mm_mine), -bf_hi(mm_mine), bits);
+  const int j_mine = j_first + l16;
+  if (l16 < kVRows && j_mine < k) {
+    vs[static_cast<size_t>(slice) * k + j_mine] = p.s16;
+    vz[static_cast<size_t>(slice) * k + j_mine] = p.z16;
+    if (oidx) oidx[static_cast<size_t>(slice) * k + j_mine] = ix[j_mine];
   }
-#pragma unroll
-  for (int off = 8; off > 0; off >>= 1) {
-    const float a = __shfl_xor_sync(0xffffffffu, mn, off), b = __shfl_xor_sync(0xffffffffu, mx, off);
-    mn = a < mn ? a : mn;
-    mx = b > mx ? b : mx;
-  }
-  const QParam p = make_param(mn, mx, bits);
-  uint32_t c[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) c[i] = quant(x[i], p, bits);
+  const float hiv = float((1 << bits) - 1);
   const int wpr = kD * bits / 32;
-  uint32_t* out = vc + (static_cast<size_t>(slice) * k + j) * wpr;
-  if (bits == 8) {
-    const uint32_t w0 = c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24);
-    const uint32_t w1 = c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24);
-    if (live) __stcs(reinterpret_cast<uint2*>(out) + l16, make_uint2(w0, w1));
-  } else if (bits == 4) {
-    uint32_t w0 = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) w0 |= c[i] << (4 * i);
-    if (live) __stcs(out + l16, w0);
-  } else {  // 2 bits: 16 codes per word = two lanes
-    uint32_t h0 = 0;
+  for (int i = 0; i < kVRows; ++i) {
+    const int j = j_first + i;
+    const float zf = __shfl_sync(0xffffffffu, p.zf, base + i), inv = __shfl_sync(0xffffffffu, p.inv, base + i);
+    const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    uint32_t c[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) h0 |= c[i] << (2 * i);
-    const uint32_t other = __shfl_xor_sync(0xffffffffu, h0, 1);
-    if (live && (l16 & 1) == 0) __stcs(out + (l16 >> 1), h0 | (other << 16));
-  }
-  if (live && l16 == 0) {
-    vs[static_cast<size_t>(slice) * k + j] = p.s16;
-    vz[static_cast<size_t>(slice) * k + j] = p.z16;
-    if (oidx) oidx[static_cast<size_t>(slice) * k + j] = t;
+    for (int q = 0; q < 4; ++q) quant2(bf_lo(w[q]), bf_hi(w[q]), zf, zf, inv, inv, hiv, c[2 * q], c[2 * q + 1]);
+    uint32_t* out = vc + (static_cast<size_t>(slice) * k + j) * wpr;
+    const bool live = j < k;
+    if (bits == 8) {
+      if (live)
+        __stcs(reinterpret_cast<uint2*>(out) + l16,
+               make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
+                          c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
+    } else if (bits == 4) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) word |= c[e] << (4 * e);
+      if (live) __stcs(out + l16, word);
+    } else {
+      uint32_t h = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) h |= c[e] << (2 * e);
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
+      if (live && (l16 & 1) == 0) __stcs(out + (l16 >> 1), h | (other << 16));
+    }
   }
 }
 
+// grid (ceil(k / (16 * kVRows)), S): 16 half-warps x kVRows rows per block
 __global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
                                                 int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
                                                 uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
                                                 int bits) {
-  pack_v_row(V, idx, oidx, vc, vs, vz, T, k, bits, blockIdx.y, blockIdx.x * 16 + (threadIdx.x >> 4));
+  pack_v_rows(V, idx, oidx, vc, vs, vz, T, k, bits, blockIdx.y,
+              (blockIdx.x * 16 + (threadIdx.x >> 4)) * kVRows);
 }
 
 static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
@@ -666,17 +1046,12 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
     return KVT_OK;
   }
   dim3 kgrid((kk + KVT_QGROUP - 1) / KVT_QGROUP, S);
-  const size_t pk_smem = sizeof(PackKSmem);
-  static bool pk_attr = false;
-  if (!pk_attr) {
-    KVT_CUDA_TRY(cudaFuncSetAttribute(k_pack_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pk_smem)));
-    pk_attr = true;
-  }
-  k_pack_k<<<kgrid, 256, pk_smem, st>>>(reinterpret_cast<const uint4*>(k), idx, reinterpret_cast<uint32_t*>(b + m.kcode_off),
+  k_pack_k<<<kgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), idx, reinterpret_cast<uint32_t*>(b + m.kcode_off),
                                   reinterpret_cast<uint16_t*>(b + m.kscale_off),
                                   reinterpret_cast<uint16_t*>(b + m.kzero_off), s->T, kk, c->bits);
   LAUNCHED(h);
-  k_pack_v<<<rows_grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(v), idx, reinterpret_cast<int32_t*>(b + m.idx_off),
+  dim3 vgrid((kk + 16 * kVRows - 1) / (16 * kVRows), S);
+  k_pack_v<<<vgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(v), idx, reinterpret_cast<int32_t*>(b + m.idx_off),
                                       reinterpret_cast<uint32_t*>(b + m.vcode_off),
                                       reinterpret_cast<uint16_t*>(b + m.vscale_off),
                                       reinterpret_cast<uint16_t*>(b + m.vzero_off), s->T, kk, c->bits);
@@ -760,12 +1135,11 @@ extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_
 // (~40 x 2 MiB of K at T = 8192), so the re-reads of K (keydiff's second
 // pass, the kept rows in the pack) are L2 hits: HBM sees K once, the kept V
 // rows once and the blob once. Bit-identical to the unfused kernels.
-namespace cg = cooperative_groups;
 constexpr int kFuseC = 8;
 constexpr int kFuseThreads = 256;
-constexpr int kFuseUnroll = 4;
-constexpr size_t kFuseUnion = sizeof(PackKSmem) > 16 * kD * sizeof(long long) ? sizeof(PackKSmem)
-                                                                                : 16 * kD * sizeof(long long);
+
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kFuseUnion = cmax(kRingBytes, cmax(sizeof(PackKSmem), 16 * kD * sizeof(long long)));
 constexpr size_t kFuseMaxSmem = 200 * 1024;
 using FuseScan = cub::BlockScan<int, kFuseThreads>;
 
@@ -791,50 +1165,43 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
   __shared__ long long sfix[kD];
   __shared__ double sdir[kD];
   __shared__ int cnt[2];
-  __shared__ uint32_t s_prefix, s_mask;
-  __shared__ int s_rem;
+  __shared__ int s_rem, s_bucket;
   __shared__ typename FuseScan::TempStorage scan_tmp;
   const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+  uint4* ring = reinterpret_cast<uint4*>(fsm);  // aliases part / pk: used in different phases
+  __shared__ __align__(8) uint64_t full[kRingStages];
+  uint32_t seq = 0;
+  if (tid == 0) {
+    for (int i = 0; i < kRingStages; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
 
+  int32_t* bidx = reinterpret_cast<int32_t*>(blob + m.idx_off);
+  if (k == T) {  // every token kept: the indices are 0..T-1 whatever the scores
+    for (int t = tid; t < n_loc; t += kFuseThreads) bidx[static_cast<size_t>(slice) * k + t_lo + t] = t_lo + t;
+    cl.sync();
+  } else {
   // ---- phase 1: token scores of [t_lo, t_hi) as orderable keys
   if (scorer == KVT_SCORER_KNORM) {
-    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {  // warp-uniform trip count
-      uint4 v[kFuseUnroll];
-#pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const int t = b0 + (hw & 1) + 16 * u;
-        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const int t = b0 + (hw & 1) + 16 * u;
-        const double n2 = half_butterfly(chunk_sumsq(v[u]));
-        if (t < n_loc && l16 == 0) keys[t] = score_key(__double2float_rn(n2));
-      }
-    }
+    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
+      const double n2 = half_butterfly(chunk_sumsq(v));
+      if (live && l16 == 0) keys[t] = score_key(__double2float_rn(n2));
+    });
   } else {  // keydiff: exact fixed-point mean direction over the whole slice, then cosine
     long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {
-      uint4 v[kFuseUnroll];
+    stream_rows(Ks, n_loc, ring, full, seq, [&](int, bool, const uint4& v) {
+      const double n2 = half_butterfly(chunk_sumsq(v));  // zero rows add nothing
+      const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const int t = b0 + (hw & 1) + 16 * u;
-        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
+      for (int j = 0; j < 4; ++j) {
+        const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
+        const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
+        acc[2 * j] += fx_round(__dmul_rn(a, kFx));
+        acc[2 * j + 1] += fx_round(__dmul_rn(b, kFx));
       }
-#pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const double n2 = half_butterfly(chunk_sumsq(v[u]));
-        const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-          const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-          acc[2 * j] += __double2ll_rn(__dmul_rn(a, kFx));
-          acc[2 * j + 1] += __double2ll_rn(__dmul_rn(b, kFx));
-        }
-      }
-    }
+    });
 #pragma unroll
     for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = acc[i];
     __syncthreads();
@@ -854,31 +1221,21 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
     double sd[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) sd[i] = sdir[l16 * 8 + i];
-    for (int b0 = hw & ~1; b0 < n_loc; b0 += 16 * kFuseUnroll) {
-      uint4 v[kFuseUnroll];
+    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {  // second pass: L2 hits
+      const double n2 = half_butterfly(chunk_sumsq(v));
+      const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      double a = 0.0;
 #pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const int t = b0 + (hw & 1) + 16 * u;
-        v[u] = t < n_loc ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
+      for (int j = 0; j < 4; ++j) {
+        const double x0 = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
+        const double x1 = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
+        a = __dadd_rn(a, __dmul_rn(x0, sd[2 * j]));
+        a = __dadd_rn(a, __dmul_rn(x1, sd[2 * j + 1]));
       }
-#pragma unroll
-      for (int u = 0; u < kFuseUnroll; ++u) {
-        const int t = b0 + (hw & 1) + 16 * u;
-        const double n2 = half_butterfly(chunk_sumsq(v[u]));
-        const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-        double a = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double x0 = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-          const double x1 = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-          a = __dadd_rn(a, __dmul_rn(x0, sd[2 * j]));
-          a = __dadd_rn(a, __dmul_rn(x1, sd[2 * j + 1]));
-        }
-        const double p = half_butterfly(a);
-        if (t < n_loc && l16 == 0) keys[t] = score_key(__double2float_rn(-p));
-      }
-    }
+      const double p = half_butterfly(a);
+      if (live && l16 == 0) keys[t] = score_key(__double2float_rn(-p));
+    });
   }
   __syncthreads();
 
@@ -900,19 +1257,10 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
       tot[tid] = sum;
     }
     __syncthreads();
-    if (tid == 0) {
-      int b = 255;
-      for (; b > 0; --b) {
-        if (tot[b] >= rem) break;
-        rem -= tot[b];
-      }
-      s_rem = rem;
-      s_prefix = prefix | (uint32_t(b) << shift);
-      s_mask = mask | (255u << shift);
-    }
+    if (tid < 32) select_bucket(tot, rem, &s_bucket, &s_rem);
     __syncthreads();
-    prefix = s_prefix;
-    mask = s_mask;
+    prefix |= uint32_t(s_bucket) << shift;
+    mask |= 255u << shift;
     rem = s_rem;
   }
   const uint32_t kth = prefix;
@@ -942,7 +1290,6 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
     a_base += rc[0];
     e_base += rc[1];
   }
-  int32_t* bidx = reinterpret_cast<int32_t*>(blob + m.idx_off);
   {
     int eq_seen = e_base + eq_before;
     int pos = a_base + above_before + min(eq_seen, ties);
@@ -958,6 +1305,7 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
     }
   }
   cl.sync();  // every CTA's indices are visible; no DSMEM access after this point
+  }
 
   // ---- phase 3: gather + quantise + pack (rows re-read from L2)
   if (bits == 16) {
@@ -980,15 +1328,16 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
       pack_k_group(K, bidx, reinterpret_cast<uint32_t*>(blob + m.kcode_off),
                    reinterpret_cast<uint16_t*>(blob + m.kscale_off), reinterpret_cast<uint16_t*>(blob + m.kzero_off),
                    T, k, bits, slice, g, pk);
-    for (int jb = rank * 16; jb < k; jb += kFuseC * 16)
-      pack_v_row(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
-                 reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off), T,
-                 k, bits, slice, jb + hw);
+    // warp-uniform trip count: both half-warps of a warp run every iteration
+    for (int wb = (rank * 16 + (hw & ~1)) * kVRows; wb < k; wb += kFuseC * 16 * kVRows)
+      pack_v_rows(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
+                  reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off),
+                  T, k, bits, slice, wb + (hw & 1) * kVRows);
   }
 }
 
 static bool fused_ok(const kvt_kv_shape* s, const kvt_codec_cfg* c) {
-  return c->scorer != KVT_SCORER_SNAPKV && fuse_smem_bytes(s->T) <= kFuseMaxSmem;
+  return (c->scorer != KVT_SCORER_SNAPKV || c->keep == s->T) && fuse_smem_bytes(s->T) <= kFuseMaxSmem;
 }
 
 static int launch_fused(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
@@ -1011,16 +1360,29 @@ static int launch_fused(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cf
 
 // ---------------------------------------------------------------- compress
 
+__global__ void __launch_bounds__(256) k_iota(int32_t* __restrict__ idx, int T, long long n) {
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) idx[i] = static_cast<int32_t>(i % T);
+}
+
 extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
                             const uint16_t* v, void* workspace, void* blob) {
   int rc;
   if ((rc = check_shape(s, c))) return rc;
-  if (fused_ok(s, c) && !getenv("KVT_UNFUSED")) return launch_fused(h, s, c, k, v, blob);
   char* w = static_cast<char*>(workspace);
   float* scores = reinterpret_cast<float*>(w);
   float* votes = reinterpret_cast<float*>(w + ws_scores(s));
   auto* fixed = reinterpret_cast<unsigned long long*>(w + 2 * ws_scores(s));
   int32_t* idx = reinterpret_cast<int32_t*>(w + 2 * ws_scores(s) + ws_fixed(s));
+  if (c->keep == s->T) {  // every token kept: indices 0..T-1 whatever the scores; no scoring pass
+    const long long n = static_cast<long long>(s->L) * s->H * s->T;
+    k_iota<<<static_cast<int>(std::min<long long>((n + 255) / 256, num_sms() * 8LL)), 256, 0, h->stream>>>(idx, s->T,
+                                                                                                          n);
+    LAUNCHED(h);
+    return launch_pack(h, s, c, k, v, idx, blob);
+  }
+  // one-launch cluster path (experimental: slower than the three kernels
+  // below at 2 CTAs/SM; profiles/README.md r1e)
+  if (fused_ok(s, c) && getenv("KVT_FUSED")) return launch_fused(h, s, c, k, v, blob);
   if ((rc = launch_scores(h, s, c, k, scores, votes, fixed))) return rc;
   if ((rc = launch_topk(h, s, c, scores, idx))) return rc;
   return launch_pack(h, s, c, k, v, idx, blob);

@@ -89,6 +89,8 @@ struct QParam {
 // asymmetric min/max group parameters stored as fp16 scale + zero
 __device__ __forceinline__ QParam make_param(float mn, float mx, int bits) {
   QParam p;
+  mn = __fadd_rn(mn, 0.0f);  // -0 -> +0: the result does not depend on which zero min/max kept
+  mx = __fadd_rn(mx, 0.0f);
   const float levels = float((1 << bits) - 1);
   const float scale = __fdiv_rn(__fsub_rn(mx, mn), levels);
   const __half hs = __float2half_rn(scale), hz = __float2half_rn(mn);
@@ -106,6 +108,29 @@ __device__ __forceinline__ uint32_t quant(float x, const QParam& p, int bits) {
   if (!(r >= 0.0f)) r = 0.0f;
   if (r > hi) r = hi;
   return uint32_t(r);
+}
+
+// Two codes at once with packed fp32x2 arithmetic (FADD2/FMUL2; each lane
+// rounds exactly like the scalar ops): clamp(rint((x - z) * inv), 0, hi).
+// Clamping before rounding is equivalent because 0 and hi are integers;
+// fmaxf maps NaN to 0 like quant(). rint = add 1.5*2^23 (round-half-even).
+__device__ __forceinline__ void quant2(float x0, float x1, float z0, float z1, float i0, float i1, float hi,
+                                       uint32_t& c0, uint32_t& c1) {
+  float2 y = __fmul2_rn(__fadd2_rn(make_float2(x0, x1), make_float2(-z0, -z1)), make_float2(i0, i1));
+  y.x = fminf(fmaxf(y.x, 0.0f), hi);
+  y.y = fminf(fmaxf(y.y, 0.0f), hi);
+  const float2 r = __fadd2_rn(y, make_float2(12582912.0f, 12582912.0f));
+  c0 = __float_as_uint(r.x) - 0x4B400000u;
+  c1 = __float_as_uint(r.y) - 0x4B400000u;
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// packed bf16x2 min (exact); max is taken as min of negated values
+__device__ __forceinline__ uint32_t bmin2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmin2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
 }
 
 __device__ __forceinline__ uint16_t dequant_bf16(uint32_t code, float sf, float zf) {

@@ -64,22 +64,60 @@ def keydiff_similarity(k):
     return (xn * s).sum(-1)
 
 
+SNAP_C0 = np.float32(0.12751743082459868)  # log2(e) / sqrt(128)
+SNAP_P = [np.float32(x) for x in (1.535336188319500E-4, 1.339887440266574E-3, 9.618437357674640E-3,
+                                  5.550332471162809E-2, 2.402264791363012E-1, 6.931472028550421E-1)]
+
+
+def quant_rows_i8(x):
+    """int8 codes + fp32 scale per row: absmax/127, rint(x * (127/absmax))."""
+    x = x.astype(np.float32)
+    a = np.abs(x).max(-1)
+    safe = np.where(a > 0, a, np.float32(1))
+    inv = (np.float32(127) / safe).astype(np.float32)
+    q = np.clip(np.rint((x * inv[..., None]).astype(np.float32)), -127, 127)
+    q = np.where(a[..., None] > 0, q, 0).astype(np.int64)
+    scale = np.where(a > 0, (a / np.float32(127)).astype(np.float32), np.float32(0))
+    return q, scale.astype(np.float32)
+
+
+def snap_exp_fx(d):
+    """round(2^22 * 2^d) for d <= 0 (fp32 mul/add polynomial), 0 below -30."""
+    d = d.astype(np.float32)
+    n = np.rint(d).astype(np.float32)
+    f = (d - n).astype(np.float32)
+    p = np.full_like(f, SNAP_P[0])
+    for c in SNAP_P[1:] + [np.float32(1.0)]:
+        p = (p * f).astype(np.float32)
+        p = (p + c).astype(np.float32)
+    e = np.clip(n, -30, 0).astype(np.int32)
+    x = np.ldexp(p, 22 + e).astype(np.float32)
+    return np.where(d < np.float32(-30), 0, np.rint(x)).astype(np.uint64)
+
+
 def snapkv_scores(k, q, W, G, pool):
+    """Exact-integer snapkv, vectorised numpy, float32 ops."""
     L, H, T, D = k.shape
     P = T - W
-    out = np.full((L, H, T), np.inf)
-    kf = bf2f(k).astype(np.float64)
-    qf = bf2f(q).astype(np.float64)
+    out = np.full((L, H, T), np.inf, np.float32)
+    if P <= 0:
+        return out
     for l in range(L):
         for h in range(H):
-            rows = qf[l, h * G:(h + 1) * G].reshape(G * W, D)
-            lg = rows @ kf[l, h, :P].T / np.sqrt(D)
-            p = np.exp(lg - lg.max(1, keepdims=True))
-            p /= p.sum(1, keepdims=True)
-            vote = p.sum(0)
-            pooled = np.array([vote[max(0, t - pool // 2):t + pool // 2 + 1].max() for t in range(P)])
-            out[l, h, :P] = pooled
-    return out.astype(np.float32)
+            rows = bf2f(q[l, h * G:(h + 1) * G].reshape(G * W, D))
+            q8, sig = quant_rows_i8(rows)
+            cr = (sig * SNAP_C0).astype(np.float32)
+            k8, tau = quant_rows_i8(bf2f(k[l, h, :P]))
+            I = q8 @ k8.T  # exact integers
+            y = ((I.astype(np.float32) * tau[None, :]).astype(np.float32) * cr[:, None]).astype(np.float32)
+            m = y.max(1, keepdims=True)
+            E = snap_exp_fx((y - m).astype(np.float32))
+            Ls = E.sum(1)
+            w = (np.uint64(1) << np.uint64(46)) // Ls
+            vote = (E * w[:, None]).sum(0)
+            pooled = np.array([vote[max(0, t - pool // 2):t + pool // 2 + 1].max() for t in range(P)], np.uint64)
+            out[l, h, :P] = (pooled.astype(np.float64).astype(np.float32) * np.float32(2.0 ** -46)).astype(np.float32)
+    return out
 
 
 def topk_indices(scores, k):

@@ -128,9 +128,7 @@ def test_snapkv_scores_match_numpy(lib):
     got = _scores(lib, s, cfg, k)
     q = R.gen_q(1, 2, cfg.q_heads, cfg.window, 128, cfg.q_seed)
     want = R.snapkv_scores(k, q, cfg.window, cfg.q_heads, cfg.pool)
-    assert np.array_equal(np.isinf(got), np.isinf(want))
-    fin = np.isfinite(want)
-    np.testing.assert_allclose(got[fin], want[fin], rtol=1e-6)
+    assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
 
 
 def test_topk_rule_ties_and_order(lib):
