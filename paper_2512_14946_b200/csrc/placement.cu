@@ -803,10 +803,10 @@ __global__ void __launch_bounds__(128) k_rebuild_cache(StepCtx X) {
 }
 
 // Build one tree level for every tier (warp per node).
-__global__ void __launch_bounds__(128) k_tree_level(DevStore st, int lvl) {
+__global__ void __launch_bounds__(128) k_tree_level(DevStore st, int lvl, int t0) {
   const int node = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.y;
+  const int t = t0 + blockIdx.y;
   if (node >= st.lvl_size[lvl]) return;
   int* tree = st.tree + static_cast<size_t>(t) * st.tree_stride;
   const int i = (node << 5) + lane;
@@ -1304,7 +1304,7 @@ static int prepare(kvt_store* s, const kvt_pset* p, const kvt_space* space, cons
       s->h->launches++;
       for (int l = 0; l < s->d.nlev; ++l) {
         dim3 grid((s->d.lvl_size[l] * 32 + 127) / 128, s->TT.T);
-        k_tree_level<<<grid, 128, 0, st>>>(s->d, l);
+        k_tree_level<<<grid, 128, 0, st>>>(s->d, l, 0);
         s->h->launches++;
       }
     }
@@ -1422,6 +1422,15 @@ extern "C" int kvt_least_drop_update(kvt_store* s, const kvt_pset* p, const kvt_
   if ((rc = prepare(s, p, space, params, KVT_RULE_UTILITY, &X))) return rc;
   kvt_update* d_u = nullptr;
   KVT_CUDA_TRY(cudaMallocAsync(&d_u, sizeof(kvt_update), s->h->stream));
+  if (s->TT.unlimited[tier_index] && s->n) {
+    // the greedy never pops the unlimited bottom tier, so it does not keep
+    // that tier's tree current: rebuild it from the per-resident caches
+    for (int l = 0; l < s->d.nlev; ++l) {
+      dim3 grid((s->d.lvl_size[l] * 32 + 127) / 128, 1);
+      k_tree_level<<<grid, 128, 0, s->h->stream>>>(s->d, l, tier_index);
+      s->h->launches++;
+    }
+  }
   k_ld_query<<<1, 1, 0, s->h->stream>>>(X, tier_index, d_u);
   s->h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
