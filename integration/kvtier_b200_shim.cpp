@@ -32,6 +32,7 @@
 // -> std::runtime_error (proj/include/kvtier/core.hpp:18-24).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -46,6 +47,15 @@
 namespace kvtier {
 namespace {
 
+// KVT_SHIM_TRACE=1: report at exit how many reference calls the shim served
+// (the drop-in test uses it to prove the interposition took effect).
+struct CallCount {
+  long n = 0;
+  ~CallCount() {
+    if (std::getenv("KVT_SHIM_TRACE")) std::fprintf(stderr, "kvt_b200 shim: %ld kvtier calls served\n", n);
+  }
+} g_calls;
+
 void check(int rc) {
   if (rc == KVT_OK) return;
   const std::string msg = kvt_last_error();
@@ -57,6 +67,7 @@ void check(int rc) {
 // One handle per thread (the reference runs independent stores on worker
 // threads under `compare --jobs`, proj/tools/kvtier_main.cpp:206-235).
 kvt_handle* handle() {
+  ++g_calls.n;
   struct Owner {
     kvt_handle* h = nullptr;
     ~Owner() {
