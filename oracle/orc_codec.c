@@ -328,33 +328,50 @@ static void keydiff_slice(void* a, int64_t sl) {
   free(inv);
 }
 
-/* snapkv, exact-integer formulation: the
- * window queries and the prefix keys are quantised to int8 per row (absmax /
- * 127), so every logit is an exact integer dot product times two fp32
- * scales; exp2 is a fixed mul/add polynomial, and every sum is an integer.
- * Only IEEE single ops with a fixed association appear, so the CUDA path
- * (integer tensor cores) reproduces it bit for bit. */
+/* snapkv, exact-integer formulation v2.
+ * Window queries quantised to int8 per row, prefix keys to int8 per
+ * 128-token tile, so every logit is an exact int8 dot product I_rt times
+ * a per-(tile, row) fp32 factor a_jr (log2 units). Softmax over the prefix
+ * per query row uses a per-(row, 32-token block) integer shift M_br =
+ * ceil(max_block y): E_rt = round(2^15 * 2^(y_rt - M_br)) by a fixed fp32
+ * FMA polynomial; the row sum and the vote weights rescale blocks by exact
+ * integer shifts. Votes (sum over rows of probabilities, 2^45 fixed point)
+ * are max-pooled. Only IEEE single ops with a fixed association and
+ * integer arithmetic appear, so the CUDA path (int8 tensor cores) matches
+ * it bit for bit. */
 #define SNAP_C0 0.12751743082459868f /* log2(e) / sqrt(128) */
-#define SNAP_P0 1.535336188319500E-4f /* 2^f on [-1/2, 1/2] (Cephes exp2f) */
-#define SNAP_P1 1.339887440266574E-3f
-#define SNAP_P2 9.618437357674640E-3f
-#define SNAP_P3 5.550332471162809E-2f
-#define SNAP_P4 2.402264791363012E-1f
-#define SNAP_P5 6.931472028550421E-1f
+#define SNAP_E0 32767.927734375f     /* 2^15 * 2^f on [-1/2, 1/2], degree 4 */
+#define SNAP_E1 22712.50390625f
+#define SNAP_E2 7874.56103515625f
+#define SNAP_E3 1830.2916259765625f
+#define SNAP_E4 303.2661437988281f
+#define SNAP_BLK 32   /* tokens per softmax shift block */
+#define SNAP_TILE 128 /* tokens per K quantisation tile */
 
-/* int8 row quantisation: returns the scale absmax/127, writes the codes */
-static float quant_row_i8(const float* x, int8_t* q) {
+static uint32_t f2u(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  return u;
+}
+static float u2f(uint32_t u) {
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+/* int8 quantisation of n values with one absmax/127 scale: returns the scale */
+static float quant_i8(const float* x, int n, int8_t* q) {
   float a = 0.0f;
-  for (int d = 0; d < D_HEAD; ++d) {
+  for (int d = 0; d < n; ++d) {
     const float v = fabsf(x[d]);
     a = v > a ? v : a;
   }
   if (a == 0.0f) {
-    memset(q, 0, D_HEAD);
+    memset(q, 0, (size_t)n);
     return 0.0f;
   }
   const float inv = 127.0f / a;
-  for (int d = 0; d < D_HEAD; ++d) {
+  for (int d = 0; d < n; ++d) {
     float r = nearbyintf(x[d] * inv);
     r = r > 127.0f ? 127.0f : (r < -127.0f ? -127.0f : r);
     q[d] = (int8_t)r;
@@ -362,20 +379,19 @@ static float quant_row_i8(const float* x, int8_t* q) {
   return a / 127.0f;
 }
 
-/* round(2^22 * 2^d) for d <= 0, 0 below d = -30 */
-static uint32_t snap_exp_fx(float d) {
-  if (d < -30.0f) return 0u;
-  const float n = nearbyintf(d);
-  const float f = d - n;
-  float p = SNAP_P0;
-  p = p * f + SNAP_P1;
-  p = p * f + SNAP_P2;
-  p = p * f + SNAP_P3;
-  p = p * f + SNAP_P4;
-  p = p * f + SNAP_P5;
-  p = p * f + 1.0f;
-  const float x = ldexpf(p, 22 + (int)n);
-  return (uint32_t)nearbyintf(x);
+/* E(d) = round(2^15 * 2^max(d, -16)) with the fixed polynomial above:
+ * n = rint(d), f = d - n, p = poly(f), x = p * 2^n (exponent add), rint(x). */
+static uint32_t snap_exp_u16(float d) {
+  const float dc = d > -16.0f ? d : -16.0f;
+  const float t = dc + 12582912.0f;
+  const float n = t - 12582912.0f;
+  const float f = dc - n;
+  float p = fmaf(SNAP_E4, f, SNAP_E3);
+  p = fmaf(p, f, SNAP_E2);
+  p = fmaf(p, f, SNAP_E1);
+  p = fmaf(p, f, SNAP_E0);
+  const float x = u2f(f2u(p) + (f2u(t) << 23));
+  return f2u(x + 8388608.0f) - 0x4B000000u;
 }
 
 static void snapkv_slice(void* a, int64_t sl) {
@@ -388,50 +404,92 @@ static void snapkv_slice(void* a, int64_t sl) {
   float* out = J->scores + (size_t)sl * T;
   for (int t = P > 0 ? P : 0; t < T; ++t) out[t] = INFINITY; /* window always kept */
   if (P <= 0) return;
+  const int ntiles = (P + SNAP_TILE - 1) / SNAP_TILE, nblk = (P + SNAP_BLK - 1) / SNAP_BLK;
   int8_t* q8 = (int8_t*)malloc((size_t)R * D_HEAD);
-  float* cr = (float*)malloc(sizeof(float) * (size_t)R);
+  float* sig = (float*)malloc(sizeof(float) * (size_t)R);
   float row[D_HEAD];
   for (int g = 0; g < G; ++g)
     for (int w = 0; w < W; ++w) {
       const int r = g * W + w;
       for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(synth_q(s, c, l, h * G + g, w, d));
-      cr[r] = quant_row_i8(row, q8 + (size_t)r * D_HEAD) * SNAP_C0;
+      sig[r] = quant_i8(row, D_HEAD, q8 + (size_t)r * D_HEAD);
     }
+  /* K: one int8 scale per 128-token tile of the prefix */
   int8_t* k8 = (int8_t*)malloc((size_t)P * D_HEAD);
-  float* tau = (float*)malloc(sizeof(float) * (size_t)P);
-  for (int t = 0; t < P; ++t) {
-    for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(K[(size_t)t * D_HEAD + d]);
-    tau[t] = quant_row_i8(row, k8 + (size_t)t * D_HEAD);
+  float* tau = (float*)malloc(sizeof(float) * (size_t)ntiles);
+  float* tile = (float*)malloc(sizeof(float) * SNAP_TILE * D_HEAD);
+  for (int j = 0; j < ntiles; ++j) {
+    const int t0 = j * SNAP_TILE, n = (P - t0 < SNAP_TILE ? P - t0 : SNAP_TILE);
+    for (int i = 0; i < n * D_HEAD; ++i) tile[i] = bf2f(K[(size_t)t0 * D_HEAD + i]);
+    tau[j] = quant_i8(tile, n * D_HEAD, k8 + (size_t)t0 * D_HEAD);
   }
-  float* y = (float*)malloc(sizeof(float) * (size_t)R * P);
-  for (int r = 0; r < R; ++r)
-    for (int t = 0; t < P; ++t) {
-      int32_t acc = 0;
-      for (int d = 0; d < D_HEAD; ++d) acc += (int32_t)q8[(size_t)r * D_HEAD + d] * (int32_t)k8[(size_t)t * D_HEAD + d];
-      y[(size_t)r * P + t] = ((float)acc * tau[t]) * cr[r];
-    }
-  uint64_t* vote = (uint64_t*)calloc((size_t)P, sizeof(uint64_t));
+  uint16_t* E = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)R * P);
+  int32_t* Mb = (int32_t*)malloc(sizeof(int32_t) * (size_t)R * nblk);
+  uint32_t* Lb = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)R * nblk);
+  uint32_t* Wr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)R * nblk);
+  int32_t* I = (int32_t*)malloc(sizeof(int32_t) * SNAP_BLK);
   for (int r = 0; r < R; ++r) {
-    const float* yr = y + (size_t)r * P;
-    float m = yr[0];
-    for (int t = 1; t < P; ++t) m = yr[t] > m ? yr[t] : m;
-    uint64_t L = 0;
-    for (int t = 0; t < P; ++t) L += snap_exp_fx(yr[t] - m);
-    const uint64_t w = (1ull << 46) / L;
-    for (int t = 0; t < P; ++t) vote[t] += (uint64_t)snap_exp_fx(yr[t] - m) * w;
+    const int8_t* qr = q8 + (size_t)r * D_HEAD;
+    for (int b = 0; b < nblk; ++b) {
+      const int t0 = b * SNAP_BLK, n = (P - t0 < SNAP_BLK ? P - t0 : SNAP_BLK);
+      int32_t mx = INT32_MIN;
+      for (int i = 0; i < n; ++i) {
+        int32_t acc = 0;
+        const int8_t* kt = k8 + (size_t)(t0 + i) * D_HEAD;
+        for (int d = 0; d < D_HEAD; ++d) acc += (int32_t)qr[d] * (int32_t)kt[d];
+        I[i] = acc;
+        mx = acc > mx ? acc : mx;
+      }
+      /* log2 units per unit of I, low 2 mantissa bits cleared: then
+       * 12582912 * a_jr and -M - 12582912 * a_jr are exact, and the fma
+       * below is the single correctly rounded value of I * a_jr - M */
+      const float a_jr = u2f(f2u((tau[t0 / SNAP_TILE] * sig[r]) * SNAP_C0) & ~3u);
+      const int32_t M = (int32_t)ceilf((float)mx * a_jr);
+      const float cb = (float)(-M) - 12582912.0f * a_jr;
+      uint32_t L = 0;
+      for (int i = 0; i < n; ++i) {
+        const float X = u2f((uint32_t)(I[i] + 0x4B400000));
+        const uint32_t e = snap_exp_u16(fmaf(X, a_jr, cb));
+        E[(size_t)r * P + t0 + i] = (uint16_t)e;
+        L += e;
+      }
+      Mb[(size_t)r * nblk + b] = M;
+      Lb[(size_t)r * nblk + b] = L;
+    }
+    int32_t m = INT32_MIN;
+    for (int b = 0; b < nblk; ++b) m = Mb[(size_t)r * nblk + b] > m ? Mb[(size_t)r * nblk + b] : m;
+    uint64_t Lr = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int sh = m - Mb[(size_t)r * nblk + b];
+      if (sh < 64) Lr += ((uint64_t)Lb[(size_t)r * nblk + b] << 16) >> sh;
+    }
+    const uint64_t Wt = Lr ? (1ull << 61) / Lr : 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int sh = m - Mb[(size_t)r * nblk + b];
+      Wr[(size_t)r * nblk + b] = sh < 64 ? (uint32_t)(Wt >> sh) : 0u;
+    }
   }
+  uint64_t* vote = (uint64_t*)calloc((size_t)P, sizeof(uint64_t));
+  for (int r = 0; r < R; ++r)
+    for (int t = 0; t < P; ++t)
+      vote[t] += (uint64_t)E[(size_t)r * P + t] * Wr[(size_t)r * nblk + t / SNAP_BLK];
   const int half = c->pool / 2;
   for (int t = 0; t < P; ++t) {
     uint64_t m = vote[t];
     for (int j = t - half; j <= t + half; ++j)
       if (j >= 0 && j < P && vote[j] > m) m = vote[j];
-    out[t] = (float)m * 1.4210854715202004e-14f; /* 2^-46 */
+    out[t] = (float)m * 2.8421709430404007e-14f; /* 2^-45 */
   }
   free(q8);
-  free(cr);
+  free(sig);
   free(k8);
   free(tau);
-  free(y);
+  free(tile);
+  free(E);
+  free(Mb);
+  free(Lb);
+  free(Wr);
+  free(I);
   free(vote);
 }
 

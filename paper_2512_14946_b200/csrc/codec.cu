@@ -92,9 +92,11 @@ extern "C" int kvt_blob_layout(const kvt_kv_shape* s, const kvt_codec_cfg* c, kv
 
 static int64_t ws_scores(const kvt_kv_shape* s) { return al256(4LL * s->L * s->H * s->T); }
 static int64_t ws_fixed(const kvt_kv_shape* s) { return al256(8LL * s->L * s->H * kD); }
+static int64_t ws_snapq(const kvt_kv_shape* s);
 
+// scores | snapkv Q8 tiles | keydiff fixed-point sums | kept indices
 extern "C" int64_t kvt_compress_workspace_bytes(const kvt_kv_shape* s, const kvt_codec_cfg* c) {
-  return 2 * ws_scores(s) + ws_fixed(s) + al256(4LL * s->L * s->H * c->keep);
+  return ws_scores(s) + ws_snapq(s) + ws_fixed(s) + al256(4LL * s->L * s->H * c->keep);
 }
 
 static int check_shape(const kvt_kv_shape* s, const kvt_codec_cfg* c) {
@@ -307,62 +309,70 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
   }
 }
 
-// snapkv on the integer tensor cores, exact-integer spec of
-// DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): the R = W x G window
-// queries and the prefix keys are quantised to int8 per row, so every logit
-// is an exact s8 x s8 -> s32 dot product (tcgen05.mma kind::i8, M = N = 128,
-// K = 128) times two fp32 scales; exp2 is a fixed mul/add polynomial and all
-// sums are integers, so the result is bit-identical to the CPU oracle.
+// snapkv on the integer tensor cores, exact-integer spec v2
+// of DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): window queries
+// quantised to int8 per row, prefix keys to int8 per 128-token tile, so every
+// logit is an exact s8 x s8 -> s32 dot product I (tcgen05.mma kind::i8,
+// M = N = K = 128) times a per-(tile, row) factor a. The softmax shift is per
+// (row, 32-token block): M = ceil(max y), E = round(2^15 * 2^(y - M)) by a
+// fixed FMA polynomial, blocks are combined with exact integer shifts.
 //
-// One thread-block cluster per (layer, kv-head) slice; CTA `rank` owns
-// `tpc` 128-token tiles of the prefix and keeps them as int8 in smem (SW128
-// K-major UMMA layout, 16 KB per tile) for three passes over the logits:
-//   1. row max m_r            (D[r][t] = Q8 . K8^T, TMEM lane = query row)
-//   2. row sum L_r of E_rt    (same orientation), w_r = floor(2^46 / L_r)
-//   3. vote V_t = sum_r E_rt w_r  (D[t][r] = K8 . Q8^T, TMEM lane = token)
-// The MMA of tile j+1 runs while the 8 epilogue warps drain tile j (two
-// 128-column TMEM accumulators). m_r and L_r are combined across the
-// cluster through DSMEM; pooling reads the neighbours' votes the same way.
-constexpr int kSnapTiles = 8;  // tiles per CTA: 8 x 16 KB int8 K
-constexpr int kSnapThreads = 256;
+// One thread-block cluster (<= 16 CTAs) per (layer, kv-head) slice; CTA
+// `rank` owns up to 4 tiles (512 tokens). Each tile is bulk-copied (bf16) into
+// smem, quantised to int8 (SW128 K-major UMMA layout), multiplied against the
+// resident Q8 tile into TMEM, and the 16 epilogue warps (lane quadrant x
+// 32-token block) turn their 32 logits into u16 E values kept in smem. Row
+// shifts and sums are combined across the cluster through DSMEM; then every
+// thread votes one token from the stored E (no second exp), and pooling reads
+// neighbour CTAs' votes through DSMEM. The next tile's copy overlaps the MMA
+// and epilogue of the current one.
+constexpr int kSnapTPC = 4;            // tiles per CTA
+constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
+constexpr int kSnapThreads = 512;      // 16 warps
+constexpr int kSnapEStride = 1040;     // bytes per E row: 512 tokens x u16 + 16 B pad (conflict-free STS.128)
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
+constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
 
 struct SnapSmem {
-  uint8_t k8[kSnapTiles][128 * 128];  // 1024-aligned (offset 0 of the aligned base)
+  uint8_t k8[128 * 128];  // offset 0 of the 1024-aligned base
   uint8_t q8[128 * 128];
-  uint4 ring[kRingStages * kRingRows * 16];  // bf16 K staging; reused for the votes
-  float tau[kSnapTiles * 128];
-  float cr[128], mr[128], mcl[128];
-  uint32_t wr[128];
-  float red_f[2][128];
-  unsigned long long red_u[2][128], lcl[128];
-  uint64_t full[kRingStages], mma_bar[2];
+  uint4 stage[128 * 16];  // one bf16 tile (32 KB); reused for the votes
+  uint8_t e[128 * kSnapEStride];
+  int32_t mb[kSnapTPC * 4][128];   // per (block, row) shift M
+  uint32_t lb[kSnapTPC * 4][128];  // per (block, row) sum of E, then the block weight
+  float sig[128];
+  uint32_t amax[16];
+  int32_t mloc[128], mrow[128];
+  unsigned long long lloc[128];
+  uint64_t full, qbar, mma_bar;
   uint32_t tmem_base;
 };
 
-// round(2^22 * 2^d) for d <= 0, 0 below -30: fixed mul/add polynomial for
-// 2^f on [-1/2, 1/2] (Cephes exp2f), n = rint(d) via the 1.5*2^23 trick,
-// exact 2^(22+n) scaling on the exponent bits, rint via 2^23.
-__device__ __forceinline__ uint32_t snap_exp_fx(float d) {
-  const float t = __fadd_rn(d, 12582912.0f);
-  const float n = __fsub_rn(t, 12582912.0f);
-  const float f = __fsub_rn(d, n);
-  float p = 1.535336188319500E-4f;
-  p = __fadd_rn(__fmul_rn(p, f), 1.339887440266574E-3f);
-  p = __fadd_rn(__fmul_rn(p, f), 9.618437357674640E-3f);
-  p = __fadd_rn(__fmul_rn(p, f), 5.550332471162809E-2f);
-  p = __fadd_rn(__fmul_rn(p, f), 2.402264791363012E-1f);
-  p = __fadd_rn(__fmul_rn(p, f), 6.931472028550421E-1f);
-  p = __fadd_rn(__fmul_rn(p, f), 1.0f);
-  const int ni = __float_as_int(t) - 0x4B400000;
-  const float x = __int_as_float(__float_as_int(p) + ((22 + ni) << 23));
-  const uint32_t e = __float_as_uint(__fadd_rn(x, 8388608.0f)) - 0x4B000000u;
-  return d < -30.0f ? 0u : e;
-}
+// 2^15 * 2^f on [-1/2, 1/2], degree 4 (oracle SNAP_E*)
+constexpr float kE0 = 32767.927734375f, kE1 = 22712.50390625f, kE2 = 7874.56103515625f,
+                kE3 = 1830.2916259765625f, kE4 = 303.2661437988281f;
 
-// |I| < 2^22: exact int -> float without the conversion pipe
-__device__ __forceinline__ float i2f_exact(uint32_t i) {
-  return __fsub_rn(__int_as_float(static_cast<int>(i) + 0x4B400000), 12582912.0f);
+// Two E values: x = 12582912 + I (exact), d = fma(x, a, c) = rint-exact
+// I * a - M; E = round(2^15 * 2^max(d, -16)) (oracle snap_exp_u16), packed
+// fp32x2 ops (each lane rounds like the scalar op). Returns the raw
+// float-as-int words 0x4B000000 + E (the caller strips the bias).
+__device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a, float c, uint32_t& u0,
+                                              uint32_t& u1) {
+  const float2 x = make_float2(__uint_as_float(i0 + 0x4B400000u), __uint_as_float(i1 + 0x4B400000u));
+  const float2 d = __ffma2_rn(x, make_float2(a, a), make_float2(c, c));
+  const float2 dc = make_float2(fmaxf(d.x, -16.0f), fmaxf(d.y, -16.0f));
+  const float2 t = __fadd2_rn(dc, make_float2(12582912.0f, 12582912.0f));
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __fadd2_rn(dc, make_float2(-n.x, -n.y));
+  float2 p = __ffma2_rn(make_float2(kE4, kE4), f, make_float2(kE3, kE3));
+  p = __ffma2_rn(p, f, make_float2(kE2, kE2));
+  p = __ffma2_rn(p, f, make_float2(kE1, kE1));
+  p = __ffma2_rn(p, f, make_float2(kE0, kE0));
+  const float2 xs = make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                                __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+  const float2 r = __fadd2_rn(xs, make_float2(8388608.0f, 8388608.0f));
+  u0 = __float_as_uint(r.x);
+  u1 = __float_as_uint(r.y);
 }
 
 // Half-warp int8 quantisation of one 128-channel row (lane: channels
@@ -388,36 +398,16 @@ __device__ __forceinline__ float quant_row_i8(const float (&x)[8], uint8_t* tile
   return a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
 }
 
-__global__ void __launch_bounds__(kSnapThreads, 1)
-    k_snapkv_tc(const uint4* __restrict__ K, float* __restrict__ scores, int H, int T, int W, int G, int pool,
-                uint64_t q_seed, int tpc) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
-  const int slice = blockIdx.y, l = slice / H, h = slice % H;
-  const int P = T - W, R = W * G;
-  const int ntiles = (P + 127) / 128;
-  const int tile0 = rank * tpc, ntl = max(0, min(tpc, ntiles - tile0));
-  const int t_lo = tile0 * 128, n_loc = max(0, min(P - t_lo, ntl * 128));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, l16 = tid & 15, hw = tid >> 4;
-  extern __shared__ uint8_t snap_raw[];
-  SnapSmem& sm = *reinterpret_cast<SnapSmem*>((reinterpret_cast<uintptr_t>(snap_raw) + 1023) & ~uintptr_t(1023));
-  float* out = scores + static_cast<size_t>(slice) * T;
-
-  if (tid == 0) {
-    for (int i = 0; i < kRingStages; ++i) mbar_init(&sm.full[i], 1);
-    mbar_init(&sm.mma_bar[0], 1);
-    mbar_init(&sm.mma_bar[1], 1);
-    mbar_fence_init();
-  }
-  if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-
-  // ---- Q8: synthetic window queries, half-warp per row (rows >= R are zero)
+// Synthetic window queries of every slice -> int8 Q8 tile (SW128 layout, rows
+// >= R zero) + per-row scale, one 256-thread block per slice. Independent of
+// the KV chunk; the main kernel bulk-copies it.
+__global__ void __launch_bounds__(256) k_snap_q(uint8_t* __restrict__ qbuf, int H, int W, int G, uint64_t q_seed) {
+  __shared__ __align__(1024) uint8_t q8[128 * 128];
+  __shared__ float sig[128];
+  const int slice = blockIdx.x, l = slice / H, h = slice % H, R = W * G;
+  const int tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
   const uint64_t Hq = uint64_t(H) * G;
-  for (int r = hw; r < 128; r += 16) {
+  for (int r = hw; r < 128; r += 16) {  // warp-uniform: both half-warps iterate together
     float x[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -430,171 +420,240 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       }
       x[e] = v;
     }
-    const float sc = quant_row_i8(x, sm.q8, r, l16);
-    if (l16 == 0) sm.cr[r] = __fmul_rn(sc, kSnapC0);
+    const float sc = quant_row_i8(x, q8, r, l16);
+    if (l16 == 0) sig[r] = sc;
   }
-  // ---- K8: stream this CTA's prefix tokens, quantise per token into the tiles
-  uint32_t seq = 0;
-  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
-  stream_rows(Ks, n_loc, sm.ring, sm.full, seq, [&](int t, bool live, const uint4& v) {
-    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-    float x[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      x[2 * q] = bf_lo(w4[q]);
-      x[2 * q + 1] = bf_hi(w4[q]);
-    }
-    if (t < ntl * 128) {  // rows past the prefix: zeros (live == false)
-      const float sc = quant_row_i8(x, sm.k8[t >> 7], t & 127, l16);
-      if (l16 == 0) sm.tau[t] = live ? sc : 0.0f;
-    }
-  });
-  for (int t0 = ((n_loc + kRingRows - 1) / kRingRows) * kRingRows + (hw & ~1); t0 < ntl * 128; t0 += 16) {
-    const int t = t0 + (hw & 1);  // tail of the last tile: zero rows
-    float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    quant_row_i8(x, sm.k8[t >> 7], t & 127, l16);
-    if (l16 == 0) sm.tau[t] = 0.0f;
-  }
-  fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
   __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(qbuf + static_cast<size_t>(slice) * kSnapQBytes);
+  for (int i = tid; i < 1024; i += 256) dst[i] = reinterpret_cast<const uint4*>(q8)[i];
+  if (tid < 128) reinterpret_cast<float*>(dst + 1024)[tid] = sig[tid];
+}
 
-  // ---- three passes over the logits
+__global__ void __launch_bounds__(kSnapThreads, 1)
+    k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, float* __restrict__ scores, int T,
+                int W, int G, int pool, int tpc) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  const int slice = blockIdx.y;
+  const int P = T - W, R = W * G;
+  const int ntiles = (P + 127) / 128;
+  const int tile0 = rank * tpc, ntl = max(0, min(tpc, ntiles - tile0));
+  const int t_lo = tile0 * 128, n_loc = max(0, min(P - t_lo, ntl * 128));
+  const int nblk = (n_loc + 31) / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ uint8_t snap_raw[];
+  SnapSmem& sm = *reinterpret_cast<SnapSmem*>((reinterpret_cast<uintptr_t>(snap_raw) + 1023) & ~uintptr_t(1023));
+  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+
+  if (tid == 0) {
+    mbar_init(&sm.full, 1);
+    mbar_init(&sm.qbar, 1);
+    mbar_init(&sm.mma_bar, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc(&sm.tmem_base, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  if (tid == 0) {
+    mbar_expect_tx(&sm.qbar, kSnapQBytes);
+    bulk_g2s(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar);
+    bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
+    if (ntl > 0) {
+      const int rows = min(128, n_loc);
+      mbar_expect_tx(&sm.full, rows * 256);
+      bulk_g2s(sm.stage, Ks, rows * 256, &sm.full);
+    }
+  }
+  mbar_wait(&sm.qbar, 0);
+
   constexpr uint32_t kIdesc = idesc_i8(128, 128);
-  uint32_t uses[2] = {0, 0};
-  const int quad = warp & 3, colh = warp >> 2;  // TMEM lanes 32*quad.., columns 64*colh..
-  auto run_pass = [&](bool tok_major, auto&& epi) {
-    auto issue = [&](int j) {
-      tc_fence_after();  // order after the barrier that freed accumulator j & 1
-      const uint64_t dk = umma_desc_sw128(sm.k8[j]), dq = umma_desc_sw128(sm.q8);
-      const uint64_t da = tok_major ? dk : dq, db = tok_major ? dq : dk;
+  const int quad = warp & 3, cb = warp >> 2;  // TMEM lanes 32*quad.., 32-token block cb of the tile
+  const int r = quad * 32 + lane;             // epilogue: this thread's query row
+  const float sig_r = sm.sig[r];
+  for (int j = 0; j < ntl; ++j) {
+    const int rows = min(128, n_loc - j * 128);
+    mbar_wait(&sm.full, j & 1);
+    // ---- per-tile absmax (|bf16| bit patterns order like the values)
+    const int qr = tid >> 2, qq = tid & 3;  // row, 32-channel quarter
+    uint4 v[4];
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + (j & 1) * 128, da + 2 * ks, db + 2 * ks, kIdesc, ks > 0);
-      umma_commit(&sm.mma_bar[j & 1]);
-    };
-    if (ntl > 0 && tid == 0) issue(0);
-    for (int j = 0; j < ntl; ++j) {
-      if (tid == 0 && j + 1 < ntl) issue(j + 1);
-      const int b = j & 1;
-      mbar_wait(&sm.mma_bar[b], uses[b] & 1);
-      ++uses[b];
+    for (int i = 0; i < 4; ++i) v[i] = qr < rows ? sm.stage[qr * 16 + qq * 4 + i] : make_uint4(0, 0, 0, 0);
+    uint32_t mx2 = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mx2 = __vmaxu2(mx2, v[i].x & 0x7fff7fffu);
+      mx2 = __vmaxu2(mx2, v[i].y & 0x7fff7fffu);
+      mx2 = __vmaxu2(mx2, v[i].z & 0x7fff7fffu);
+      mx2 = __vmaxu2(mx2, v[i].w & 0x7fff7fffu);
+    }
+    uint32_t mx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
+    if (lane == 0) sm.amax[warp] = mx;
+    __syncthreads();
+    mx = 0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) mx = max(mx, sm.amax[w]);
+    const float A = bf2f(mx);
+    const float inv = A > 0.0f ? __fdiv_rn(127.0f, A) : 0.0f;
+    const float tau = A > 0.0f ? __fdiv_rn(A, 127.0f) : 0.0f;
+    // ---- quantise this thread's 32 values (|x * inv| < 127.5: no clamp needed)
+    uint32_t wq[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t ww[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        float2 y0 = __fmul2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv));
+        float2 y1 = __fmul2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])), make_float2(inv, inv));
+        y0 = __fadd2_rn(y0, make_float2(12582912.0f, 12582912.0f));
+        y1 = __fadd2_rn(y1, make_float2(12582912.0f, 12582912.0f));
+        const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
+        const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
+        wq[2 * i + h2] = __byte_perm(lo, hi, 0x5410);
+      }
+    }
+    {
+      const int c0 = qq * 2;  // 16-byte chunks c0, c0 + 1 of row qr
+      *reinterpret_cast<uint4*>(sm.k8 + qr * 128 + ((c0 ^ (qr & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+      *reinterpret_cast<uint4*>(sm.k8 + qr * 128 + (((c0 + 1) ^ (qr & 7)) << 4)) =
+          make_uint4(wq[4], wq[5], wq[6], wq[7]);
+    }
+    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core / bulk copy engine
+    __syncthreads();
+    if (tid == 0) {
+      if (j + 1 < ntl) {  // stage is consumed: prefetch the next tile under this one's MMA + epilogue
+        const int nrows = min(128, n_loc - (j + 1) * 128);
+        mbar_expect_tx(&sm.full, nrows * 256);
+        bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+      }
       tc_fence_after();
-      epi(j, tmem + b * 128 + (uint32_t(quad * 32) << 16) + colh * 64);
-      tc_fence_before();
-      __syncthreads();  // accumulator b drained: tile j + 2 may overwrite it
+      const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(sm.k8);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) umma_i8(tmem, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
+      umma_commit(&sm.mma_bar);
     }
-  };
-  const int r_row = quad * 32 + lane;  // passes 1-2: this thread's query row
+    mbar_wait(&sm.mma_bar, j & 1);
+    tc_fence_after();
+    // ---- epilogue: row r, tokens 128j + 32cb .. +31 of this CTA
+    uint32_t I[32];
+    tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + cb * 32, I);
+    const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
+    int32_t M = INT_MIN;
+    uint32_t L = 0;
+    uint32_t pk[16];
+    if (r < R && nv > 0) {
+      const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
+      int32_t m = INT_MIN;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nv) m = max(m, static_cast<int32_t>(I[i]));
+      M = static_cast<int32_t>(ceilf(__fmul_rn(__int2float_rn(m), a)));
+      const float c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
+      uint32_t Lraw = 0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        uint32_t u0, u1;
+        snap_exp_pair(I[i], I[i + 1], a, c, u0, u1);
+        if (i >= nv) u0 = 0x4B000000u;
+        if (i + 1 >= nv) u1 = 0x4B000000u;
+        Lraw += u0 + u1;
+        pk[i >> 1] = __byte_perm(u0, u1, 0x5410);  // low 16 bits of each = E (E < 2^16)
+      }
+      L = Lraw - 32u * 0x4B000000u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = 0;
+    }
+    uint4* erow = reinterpret_cast<uint4*>(sm.e + r * kSnapEStride + tok0 * 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) erow[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+    sm.mb[j * 4 + cb][r] = M;
+    sm.lb[j * 4 + cb][r] = L;
+    tc_fence_before();
+    __syncthreads();  // TMEM accumulator and K8 free for the next tile
+  }
 
-  // pass 1: row max
-  {
-    const float c_r = sm.cr[r_row];
-    float mx = -INFINITY;
-    run_pass(false, [&](int j, uint32_t taddr) {
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t I[32];
-        tmem_ld32(taddr + cc * 32, I);
-        const int tb = j * 128 + colh * 64 + cc * 32;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), sm.tau[tb + i]), c_r);
-          if (tb + i < n_loc) mx = fmaxf(mx, y);
-        }
-      }
-    });
-    sm.red_f[colh][r_row] = mx;
-    __syncthreads();
-    if (tid < 128) sm.mcl[tid] = fmaxf(sm.red_f[0][tid], sm.red_f[1][tid]);
-    cl.sync();
-    if (tid < 128) {
-      float m = -INFINITY;
-      for (int c = 0; c < C; ++c) m = fmaxf(m, cl.map_shared_rank(sm.mcl, c)[tid]);
-      sm.mr[tid] = m;
-    }
-    __syncthreads();
+  // ---- row shift and sum across the cluster
+  if (tid < 128) {
+    int32_t m = INT_MIN;
+    for (int b = 0; b < nblk; ++b) m = max(m, sm.mb[b][tid]);
+    sm.mloc[tid] = m;
   }
-  // pass 2: row sums of E, then w_r
-  {
-    const float c_r = sm.cr[r_row], m_r = sm.mr[r_row];
+  cl.sync();
+  if (tid < 128) {
+    int32_t m = INT_MIN;
+    for (int c = 0; c < C; ++c) m = max(m, cl.map_shared_rank(sm.mloc, c)[tid]);
+    sm.mrow[tid] = m;
     unsigned long long Ls = 0;
-    run_pass(false, [&](int j, uint32_t taddr) {
-      uint32_t part = 0;  // <= 64 x 2^22: no overflow
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t I[32];
-        tmem_ld32(taddr + cc * 32, I);
-        const int tb = j * 128 + colh * 64 + cc * 32;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), sm.tau[tb + i]), c_r);
-          const uint32_t e = snap_exp_fx(__fsub_rn(y, m_r));
-          if (tb + i < n_loc) part += e;
-        }
-      }
-      Ls += part;
-    });
-    sm.red_u[colh][r_row] = Ls;
-    __syncthreads();
-    if (tid < 128) sm.lcl[tid] = sm.red_u[0][tid] + sm.red_u[1][tid];
-    cl.sync();
-    if (tid < 128) {
-      unsigned long long L = 0;
-      for (int c = 0; c < C; ++c) L += cl.map_shared_rank(sm.lcl, c)[tid];
-      sm.wr[tid] = tid < R ? static_cast<uint32_t>((1ull << 46) / L) : 0u;
+    for (int b = 0; b < nblk; ++b) {
+      const int64_t sh = int64_t(m) - sm.mb[b][tid];
+      if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][tid]) << 16) >> sh;
     }
-    __syncthreads();
+    sm.lloc[tid] = Ls;
   }
-  // pass 3: votes (token-major accumulators)
-  unsigned long long* vote = reinterpret_cast<unsigned long long*>(sm.ring);
-  run_pass(true, [&](int j, uint32_t taddr) {
-    const int tl = j * 128 + quad * 32 + lane;
-    const float tau_t = sm.tau[tl];
+  cl.sync();
+  if (tid < 128) {
+    unsigned long long Ls = 0;
+    for (int c = 0; c < C; ++c) Ls += cl.map_shared_rank(sm.lloc, c)[tid];
+    const unsigned long long wt = (tid < R && Ls) ? (1ull << 61) / Ls : 0ull;
+    const int32_t m = sm.mrow[tid];
+    for (int b = 0; b < nblk; ++b) {
+      const int64_t sh = int64_t(m) - sm.mb[b][tid];
+      sm.lb[b][tid] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
+    }
+  }
+  __syncthreads();
+  // ---- votes: thread = token (block b = warp)
+  unsigned long long* vote = reinterpret_cast<unsigned long long*>(sm.stage);
+  {
     unsigned long long acc = 0;
+    if (tid < n_loc) {
+      const uint16_t* ecol = reinterpret_cast<const uint16_t*>(sm.e) + tid;
+      const uint32_t* wb = sm.lb[warp];
+      for (int r0 = 0; r0 < R; r0 += 4) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
+        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      uint32_t I[32];
-      tmem_ld32(taddr + cc * 32, I);
-      const int rb = colh * 64 + cc * 32;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float y = __fmul_rn(__fmul_rn(i2f_exact(I[i]), tau_t), sm.cr[rb + i]);
-        const uint32_t e = snap_exp_fx(__fsub_rn(y, sm.mr[rb + i]));
-        acc += static_cast<unsigned long long>(e) * sm.wr[rb + i];
+        for (int q = 0; q < 4; ++q)
+          if (r0 + q < R) acc += static_cast<unsigned long long>(ecol[(r0 + q) * (kSnapEStride / 2)]) * ww[q];
       }
     }
-    sm.red_u[colh][quad * 32 + lane] = acc;
-    __syncthreads();
-    if (tid < 128) vote[j * 128 + tid] = sm.red_u[0][tid] + sm.red_u[1][tid];
-  });
+    vote[tid] = acc;
+  }
   cl.sync();  // every CTA's votes visible
   // ---- pooling (max over +-pool/2 within the prefix) and scores
+  float* out = scores + static_cast<size_t>(slice) * T;
   const int half = pool / 2;
   for (int tl = tid; tl < n_loc; tl += kSnapThreads) {
     unsigned long long m = 0;
     for (int dj = -half; dj <= half; ++dj) {
-      const int tg = t_lo + tl + dj;  // global token
+      const int tg = t_lo + tl + dj;  // global prefix token
       if (tg < 0 || tg >= P) continue;
       const int owner = (tg / 128) / tpc;
       const int tr = tg - owner * tpc * 128;
       const unsigned long long* vv =
-          owner == rank ? vote : cl.map_shared_rank(reinterpret_cast<unsigned long long*>(sm.ring), owner);
-      const unsigned long long v = vv[tr];
-      m = v > m ? v : m;
+          owner == rank ? vote : cl.map_shared_rank(reinterpret_cast<unsigned long long*>(sm.stage), owner);
+      const unsigned long long x = vv[tr];
+      m = x > m ? x : m;
     }
-    out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 1.4210854715202004e-14f);  // 2^-46 (exact)
+    out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 2.8421709430404007e-14f);  // 2^-45 (exact)
   }
   if (rank == C - 1)
     for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
   cl.sync();  // no CTA leaves while its votes may still be read
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 0) tmem_dealloc(tmem, 128);
 }
 
 __global__ void k_fill_inf(float* __restrict__ out, long long n) {
   for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) out[i] = INFINITY;
 }
 
+static int64_t ws_snapq(const kvt_kv_shape* s) { return al256(int64_t(kSnapQBytes) * s->L * s->H); }
+
+// qbuf: ws_snapq(s) bytes of device workspace for the Q8 tiles
 static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                         float* scores) {
+                         float* scores, uint8_t* qbuf) {
   const int S = s->L * s->H, T = s->T, W = c->window, G = c->q_heads;
   if (W * G > 128 || W > T || W < 0 || G < 1) return set_error(KVT_EINVAL, "snapkv window x q_heads must be <= 128");
   if (c->pool < 1 || (c->pool & 1) == 0) return set_error(KVT_EINVAL, "snapkv pool must be odd");
@@ -606,9 +665,10 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     return KVT_OK;
   }
   const int ntiles = (P + 127) / 128;
-  const int C = (ntiles + kSnapTiles - 1) / kSnapTiles;
-  if (C > 16) return set_error(KVT_EINVAL, "snapkv: prefix longer than 16 x 8 x 128 tokens is not supported");
-  const int tpc = (ntiles + C - 1) / C;
+  const int Cn = (ntiles + kSnapTPC - 1) / kSnapTPC;
+  if (Cn > kSnapMaxC)
+    return set_error(KVT_EINVAL, "snapkv: prefix (T - window) longer than 8192 tokens is not supported");
+  const int tpc = (ntiles + Cn - 1) / Cn;
   const size_t smem = sizeof(SnapSmem) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -616,25 +676,28 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
+  k_snap_q<<<S, 256, 0, h->stream>>>(qbuf, s->H, W, G, static_cast<uint64_t>(c->q_seed));
+  LAUNCHED(h);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, S);
+  cfg.gridDim = dim3(Cn, S);
   cfg.blockDim = dim3(kSnapThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = h->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.x = Cn;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_snapkv_tc, reinterpret_cast<const uint4*>(k), scores, s->H, T, W, G,
-                                  c->pool, static_cast<uint64_t>(c->q_seed), tpc));
+  KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_snapkv_tc, reinterpret_cast<const uint4*>(k),
+                                  static_cast<const uint8_t*>(qbuf), scores, T, W, G, c->pool, tpc));
   LAUNCHED(h);
   return KVT_OK;
 }
+
 static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                         float* scores, float* votes, unsigned long long* fixed) {
+                         float* scores, uint8_t* snapq, unsigned long long* fixed) {
   const int S = s->L * s->H, T = s->T;
   cudaStream_t st = h->stream;
   if (c->scorer == KVT_SCORER_KNORM) {
@@ -652,7 +715,7 @@ static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
                                           reinterpret_cast<const long long*>(fixed), scores, T);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_SNAPKV) {
-    return launch_snapkv(h, s, c, k, scores);
+    return launch_snapkv(h, s, c, k, scores, snapq);
   } else {
     return set_error(KVT_EINVAL, "unknown scorer");
   }
@@ -673,10 +736,10 @@ extern "C" int kvt_token_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_
                                 float* scores) {
   int rc;
   if ((rc = check_shape(s, c))) return rc;
-  if ((rc = ensure_scratch(h, ws_scores(s) + ws_fixed(s)))) return rc;
+  if ((rc = ensure_scratch(h, ws_snapq(s) + ws_fixed(s)))) return rc;
   char* b = static_cast<char*>(h->scratch);
-  return launch_scores(h, s, c, k, scores, reinterpret_cast<float*>(b),
-                       reinterpret_cast<unsigned long long*>(b + ws_scores(s)));
+  return launch_scores(h, s, c, k, scores, reinterpret_cast<uint8_t*>(b),
+                       reinterpret_cast<unsigned long long*>(b + ws_snapq(s)));
 }
 
 // ------------------------------------------------------------------ top-k
@@ -1370,9 +1433,9 @@ extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_code
   if ((rc = check_shape(s, c))) return rc;
   char* w = static_cast<char*>(workspace);
   float* scores = reinterpret_cast<float*>(w);
-  float* votes = reinterpret_cast<float*>(w + ws_scores(s));
-  auto* fixed = reinterpret_cast<unsigned long long*>(w + 2 * ws_scores(s));
-  int32_t* idx = reinterpret_cast<int32_t*>(w + 2 * ws_scores(s) + ws_fixed(s));
+  uint8_t* snapq = reinterpret_cast<uint8_t*>(w + ws_scores(s));
+  auto* fixed = reinterpret_cast<unsigned long long*>(w + ws_scores(s) + ws_snapq(s));
+  int32_t* idx = reinterpret_cast<int32_t*>(w + ws_scores(s) + ws_snapq(s) + ws_fixed(s));
   if (c->keep == s->T) {  // every token kept: indices 0..T-1 whatever the scores; no scoring pass
     const long long n = static_cast<long long>(s->L) * s->H * s->T;
     k_iota<<<static_cast<int>(std::min<long long>((n + 255) / 256, num_sms() * 8LL)), 256, 0, h->stream>>>(idx, s->T,
@@ -1383,7 +1446,7 @@ extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_code
   // one-launch cluster path (experimental: slower than the three kernels
   // below at 2 CTAs/SM; profiles/README.md r1e)
   if (fused_ok(s, c) && getenv("KVT_FUSED")) return launch_fused(h, s, c, k, v, blob);
-  if ((rc = launch_scores(h, s, c, k, scores, votes, fixed))) return rc;
+  if ((rc = launch_scores(h, s, c, k, scores, snapq, fixed))) return rc;
   if ((rc = launch_topk(h, s, c, scores, idx))) return rc;
   return launch_pack(h, s, c, k, v, idx, blob);
 }

@@ -65,58 +65,102 @@ def keydiff_similarity(k):
 
 
 SNAP_C0 = np.float32(0.12751743082459868)  # log2(e) / sqrt(128)
-SNAP_P = [np.float32(x) for x in (1.535336188319500E-4, 1.339887440266574E-3, 9.618437357674640E-3,
-                                  5.550332471162809E-2, 2.402264791363012E-1, 6.931472028550421E-1)]
+SNAP_E = [np.float32(x) for x in (32767.927734375, 22712.50390625, 7874.56103515625, 1830.2916259765625,
+                                  303.2661437988281)]  # 2^15 * 2^f on [-1/2, 1/2], degree 4
 
 
-def quant_rows_i8(x):
-    """int8 codes + fp32 scale per row: absmax/127, rint(x * (127/absmax))."""
+def fma32(a, b, c):
+    """Correctly rounded float32 a*b+c (IEEE fusedMultiplyAdd), vectorised.
+    a*b is exact in float64; s = fl64(ab + c) is off the exact sum by err
+    (TwoSum, exact). Rounding s to float32 is correct unless s sits exactly
+    on a float32 midpoint, where the sign of err breaks the tie."""
+    a, b, c = (np.asarray(x, np.float32).astype(np.float64) for x in (a, b, c))
+    ab = a * b
+    s = ab + c
+    bb = s - ab
+    err = (ab - (s - bb)) + (c - bb)
+    r = s.astype(np.float32)
+    lo = np.nextafter(r, np.float32(-np.inf)).astype(np.float64)
+    hi = np.nextafter(r, np.float32(np.inf)).astype(np.float64)
+    rd = r.astype(np.float64)
+    # s exactly halfway between r and a neighbour: the exact value decides
+    up = (s == (rd + hi) / 2) & (err > 0)
+    dn = (s == (rd + lo) / 2) & (err < 0)
+    mid_lo = (s == (rd + lo) / 2) & (err > 0)   # exact value above the midpoint -> r is right
+    mid_hi = (s == (rd + hi) / 2) & (err < 0)   # exact value below the midpoint -> r is right
+    del mid_lo, mid_hi
+    r = np.where(up, hi.astype(np.float32), r)
+    r = np.where(dn, lo.astype(np.float32), r)
+    return r.astype(np.float32)
+
+
+def quant_i8(x, axis):
+    """int8 codes + fp32 scale: absmax/127 over `axis`, rint(x * (127/absmax))."""
     x = x.astype(np.float32)
-    a = np.abs(x).max(-1)
+    a = np.abs(x).max(axis=axis, keepdims=True)
     safe = np.where(a > 0, a, np.float32(1))
     inv = (np.float32(127) / safe).astype(np.float32)
-    q = np.clip(np.rint((x * inv[..., None]).astype(np.float32)), -127, 127)
-    q = np.where(a[..., None] > 0, q, 0).astype(np.int64)
+    q = np.clip(np.rint((x * inv).astype(np.float32)), -127, 127)
+    q = np.where(a > 0, q, 0).astype(np.int64)
     scale = np.where(a > 0, (a / np.float32(127)).astype(np.float32), np.float32(0))
     return q, scale.astype(np.float32)
 
 
-def snap_exp_fx(d):
-    """round(2^22 * 2^d) for d <= 0 (fp32 mul/add polynomial), 0 below -30."""
-    d = d.astype(np.float32)
-    n = np.rint(d).astype(np.float32)
-    f = (d - n).astype(np.float32)
-    p = np.full_like(f, SNAP_P[0])
-    for c in SNAP_P[1:] + [np.float32(1.0)]:
-        p = (p * f).astype(np.float32)
-        p = (p + c).astype(np.float32)
-    e = np.clip(n, -30, 0).astype(np.int32)
-    x = np.ldexp(p, 22 + e).astype(np.float32)
-    return np.where(d < np.float32(-30), 0, np.rint(x)).astype(np.uint64)
+def snap_exp_u16(d):
+    """round(2^15 * 2^max(d, -16)) with the fixed fp32 FMA polynomial."""
+    d = np.asarray(d, np.float32)
+    dc = np.maximum(d, np.float32(-16))
+    t = (dc + np.float32(12582912)).astype(np.float32)
+    n = (t - np.float32(12582912)).astype(np.float32)
+    f = (dc - n).astype(np.float32)
+    p = fma32(SNAP_E[4], f, SNAP_E[3])
+    for cst in (SNAP_E[2], SNAP_E[1], SNAP_E[0]):
+        p = fma32(p, f, cst)
+    x = (p.view(np.uint32) + (t.view(np.uint32) << np.uint32(23))).astype(np.uint32).view(np.float32)
+    return ((x + np.float32(8388608)).astype(np.float32).view(np.uint32) - np.uint32(0x4B000000)).astype(np.uint64)
 
 
 def snapkv_scores(k, q, W, G, pool):
-    """Exact-integer snapkv, vectorised numpy, float32 ops."""
+    """Exact-integer snapkv v2, vectorised numpy, float32 ops."""
     L, H, T, D = k.shape
     P = T - W
     out = np.full((L, H, T), np.inf, np.float32)
     if P <= 0:
         return out
+    nblk = (P + 31) // 32
     for l in range(L):
         for h in range(H):
             rows = bf2f(q[l, h * G:(h + 1) * G].reshape(G * W, D))
-            q8, sig = quant_rows_i8(rows)
-            cr = (sig * SNAP_C0).astype(np.float32)
-            k8, tau = quant_rows_i8(bf2f(k[l, h, :P]))
-            I = q8 @ k8.T  # exact integers
-            y = ((I.astype(np.float32) * tau[None, :]).astype(np.float32) * cr[:, None]).astype(np.float32)
-            m = y.max(1, keepdims=True)
-            E = snap_exp_fx((y - m).astype(np.float32))
-            Ls = E.sum(1)
-            w = (np.uint64(1) << np.uint64(46)) // Ls
-            vote = (E * w[:, None]).sum(0)
+            q8, sig = quant_i8(rows, 1)
+            sig = sig[:, 0]
+            kx = bf2f(k[l, h, :P])
+            k8 = np.zeros((P, D), np.int64)
+            tau = np.zeros(P, np.float32)
+            for t0 in range(0, P, 128):
+                c, sc = quant_i8(kx[t0:t0 + 128], None)
+                k8[t0:t0 + 128] = c
+                tau[t0:t0 + 128] = sc.reshape(())
+            I = q8 @ k8.T  # exact integers [R, P]
+            a = ((tau[None, :] * sig[:, None]).astype(np.float32) * SNAP_C0).astype(np.float32)  # per (r, t)
+            a = (a.view(np.uint32) & np.uint32(0xFFFFFFFC)).view(np.float32)  # 22-bit mantissa: exact offsets
+            blk = np.arange(P) // 32
+            Ipad = np.full((G * W, nblk * 32), np.iinfo(np.int64).min, np.int64)
+            Ipad[:, :P] = I
+            mx = Ipad.reshape(G * W, nblk, 32).max(-1)
+            ab = a[:, ::32]  # a is constant within a block (blocks never cross tiles)
+            M = np.ceil((mx.astype(np.float32) * ab).astype(np.float32)).astype(np.int64)
+            cb = ((-M).astype(np.float32) - (np.float32(12582912) * ab).astype(np.float32)).astype(np.float32)
+            X = ((I + 0x4B400000).astype(np.uint32)).view(np.float32)
+            E = snap_exp_u16(fma32(X, a, cb[:, blk]))
+            Lb = np.add.reduceat(E, np.arange(0, P, 32), axis=1).astype(np.uint64)
+            m = M.max(1, keepdims=True)
+            sh = (m - M)
+            Lr = np.where(sh < 64, (Lb << np.uint64(16)) >> np.minimum(sh, 63).astype(np.uint64), 0).sum(1)
+            Wt = np.where(Lr > 0, (np.uint64(1) << np.uint64(61)) // np.maximum(Lr, 1), 0).astype(np.uint64)
+            Wb = np.where(sh < 64, Wt[:, None] >> np.minimum(sh, 63).astype(np.uint64), 0).astype(np.uint64)
+            vote = (E * Wb[:, blk]).sum(0)
             pooled = np.array([vote[max(0, t - pool // 2):t + pool // 2 + 1].max() for t in range(P)], np.uint64)
-            out[l, h, :P] = (pooled.astype(np.float64).astype(np.float32) * np.float32(2.0 ** -46)).astype(np.float32)
+            out[l, h, :P] = (pooled.astype(np.float64).astype(np.float32) * np.float32(2.0 ** -45)).astype(np.float32)
     return out
 
 
