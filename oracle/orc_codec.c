@@ -253,25 +253,32 @@ int orc_parallel_threads(void) { return orc_threads(); }
 
 /* ------------------------------------------------------------------ scores */
 
-/* canonical FP64 sum of squares of one 128-channel row: 16 chunks of 8
- * consecutive channels summed sequentially, then a butterfly over the 16
- * chunk sums with strides 8, 4, 2, 1. */
-static double row_sumsq(const uint16_t* x) {
-  double p[NCHUNK];
+/* canonical fp32 dot product of two 128-channel rows:
+ * 16 chunks of 8 consecutive channels; inside a chunk an even-channel and an
+ * odd-channel fmaf chain (channel order), chunk sum = even + odd; then a
+ * butterfly over the 16 chunk sums with strides 8, 4, 2, 1. Every step is
+ * one IEEE single operation, so the CUDA half-warp (one chunk per lane,
+ * packed fp32x2 FMAs, xor shuffles) reproduces it bit for bit. */
+static float row_dot(const float* x, const float* y) {
+  float p[NCHUNK];
   for (int j = 0; j < NCHUNK; ++j) {
-    double acc = 0.0;
-    for (int i = 0; i < 8; ++i) {
-      const double v = (double)bf2f(x[8 * j + i]);
-      acc = acc + v * v;
+    float e = 0.0f, o = 0.0f;
+    for (int q = 0; q < 4; ++q) {
+      e = fmaf(x[8 * j + 2 * q], y[8 * j + 2 * q], e);
+      o = fmaf(x[8 * j + 2 * q + 1], y[8 * j + 2 * q + 1], o);
     }
-    p[j] = acc;
+    p[j] = e + o;
   }
   for (int off = 8; off > 0; off >>= 1) {
-    double q[NCHUNK];
+    float q[NCHUNK];
     for (int j = 0; j < NCHUNK; ++j) q[j] = p[j] + p[j ^ off];
     memcpy(p, q, sizeof p);
   }
   return p[0];
+}
+
+static void row_f32(const uint16_t* x, float* out) {
+  for (int d = 0; d < D_HEAD; ++d) out[d] = bf2f(x[d]);
 }
 
 typedef struct {
@@ -281,49 +288,53 @@ typedef struct {
   float* scores;
 } score_job_t;
 
+/* knorm: squared L2 norm of every key, larger = keep */
 static void knorm_slice(void* a, int64_t sl) {
   score_job_t* J = (score_job_t*)a;
   const int T = J->s->T;
   const uint16_t* K = J->k + (size_t)sl * T * D_HEAD;
-  for (int t = 0; t < T; ++t) J->scores[(size_t)sl * T + t] = (float)row_sumsq(K + (size_t)t * D_HEAD);
+  float x[D_HEAD];
+  for (int t = 0; t < T; ++t) {
+    row_f32(K + (size_t)t * D_HEAD, x);
+    J->scores[(size_t)sl * T + t] = row_dot(x, x);
+  }
 }
 
-#define FX_SCALE 1099511627776.0 /* 2^40 */
+#define KD_FX 2097152.0f  /* 2^21: fixed-point scale of the unit directions */
+#define KD_MIN_N2 0x1p-100f /* 2^-100: rows with a smaller squared norm count as zero */
 
+/* inverse norm of a row from its squared norm: 1 / sqrt(n2), two correctly
+ * rounded single ops; 0 for (near-)zero rows */
+static float kd_inv(float n2) {
+  if (!(n2 >= KD_MIN_N2)) return 0.0f;
+  const float s = sqrtf(n2);
+  return 1.0f / s;
+}
+
+/* keydiff: minus the cosine similarity of each key to the
+ * sum of all unit keys of its (layer, head). The sum is exact: every unit
+ * component is rounded to a 2^-21 fixed-point integer (rint of one fp32
+ * product, |value| <= 2^21 + 1) and summed in int64. */
 static void keydiff_slice(void* a, int64_t sl) {
   score_job_t* J = (score_job_t*)a;
   const int T = J->s->T;
   const uint16_t* K = J->k + (size_t)sl * T * D_HEAD;
   int64_t S[D_HEAD];
   memset(S, 0, sizeof S);
-  double* inv = (double*)malloc(sizeof(double) * (size_t)T);
+  float* inv = (float*)malloc(sizeof(float) * (size_t)T);
+  float x[D_HEAD];
   for (int t = 0; t < T; ++t) {
-    const double n2 = row_sumsq(K + (size_t)t * D_HEAD);
-    inv[t] = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;
-    for (int d = 0; d < D_HEAD; ++d) {
-      const double xn = (double)bf2f(K[(size_t)t * D_HEAD + d]) * inv[t];
-      S[d] += llrint(xn * FX_SCALE);
-    }
+    row_f32(K + (size_t)t * D_HEAD, x);
+    inv[t] = kd_inv(row_dot(x, x));
+    const float c = inv[t] * KD_FX;
+    /* rint of the exact product x * c (one fused rounding: fma with 1.5 * 2^23) */
+    for (int d = 0; d < D_HEAD; ++d) S[d] += (int64_t)(fmaf(x[d], c, 12582912.0f) - 12582912.0f);
   }
-  double Sd[D_HEAD];
-  for (int d = 0; d < D_HEAD; ++d) Sd[d] = (double)S[d] * (1.0 / FX_SCALE);
+  float sd[D_HEAD];
+  for (int d = 0; d < D_HEAD; ++d) sd[d] = (float)S[d] * (1.0f / KD_FX);
   for (int t = 0; t < T; ++t) {
-    double p[NCHUNK];
-    for (int j = 0; j < NCHUNK; ++j) {
-      double acc = 0.0;
-      for (int i = 0; i < 8; ++i) {
-        const int d = 8 * j + i;
-        const double xn = (double)bf2f(K[(size_t)t * D_HEAD + d]) * inv[t];
-        acc = acc + xn * Sd[d];
-      }
-      p[j] = acc;
-    }
-    for (int off = 8; off > 0; off >>= 1) {
-      double q[NCHUNK];
-      for (int j = 0; j < NCHUNK; ++j) q[j] = p[j] + p[j ^ off];
-      memcpy(p, q, sizeof p);
-    }
-    J->scores[(size_t)sl * T + t] = (float)(-p[0]); /* drop high similarity */
+    row_f32(K + (size_t)t * D_HEAD, x);
+    J->scores[(size_t)sl * T + t] = -(row_dot(x, sd) * inv[t]); /* drop high similarity */
   }
   free(inv);
 }
@@ -371,8 +382,8 @@ static float quant_i8(const float* x, int n, int8_t* q) {
     return 0.0f;
   }
   const float inv = 127.0f / a;
-  for (int d = 0; d < n; ++d) {
-    float r = nearbyintf(x[d] * inv);
+  for (int d = 0; d < n; ++d) { /* rint of the exact product x * inv, clamped to +-127 */
+    float r = fmaf(x[d], inv, 12582912.0f) - 12582912.0f;
     r = r > 127.0f ? 127.0f : (r < -127.0f ? -127.0f : r);
     q[d] = (int8_t)r;
   }

@@ -187,23 +187,32 @@ __device__ __forceinline__ void stream_rows(const uint4* __restrict__ src, int n
 
 // --------------------------------------------------------------- scores
 
-// Sum of squares of one lane's 8 channels (chunk of the canonical order).
-__device__ __forceinline__ double chunk_sumsq(const uint4& v) {
+// Canonical fp32 row dot product (oracle row_dot): lane
+// l16 of a half-warp owns chunk l16 = channels 8*l16..8*l16+7 (one 16-byte
+// bf16 load); even/odd channel fma chains as one packed fp32x2 FMA chain,
+// chunk = even + odd, then the half-warp butterfly (strides 8, 4, 2, 1).
+__device__ __forceinline__ float chunk_dot(const uint4& v, const float2 (&y)[4]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  double acc = 0.0;
+  float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const double a = double(bf2f(w[j] & 0xffffu)), b = double(bf2f(w[j] >> 16));
-    acc = __dadd_rn(acc, __dmul_rn(a, a));
-    acc = __dadd_rn(acc, __dmul_rn(b, b));
-  }
-  return acc;
+  for (int q = 0; q < 4; ++q) acc = __ffma2_rn(make_float2(bf_lo(w[q]), bf_hi(w[q])), y[q], acc);
+  return __fadd_rn(acc.x, acc.y);
 }
-
-// butterfly over the 16 chunk sums of a half-warp (strides 8, 4, 2, 1)
-__device__ __forceinline__ double half_butterfly(double p) {
+__device__ __forceinline__ float chunk_sumsq(const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-  for (int off = 8; off > 0; off >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
+  for (int q = 0; q < 4; ++q) {
+    const float2 x = make_float2(bf_lo(w[q]), bf_hi(w[q]));
+    acc = __ffma2_rn(x, x, acc);
+  }
+  return __fadd_rn(acc.x, acc.y);
+}
+// butterfly over the 16 chunk sums of a half-warp (strides 8, 4, 2, 1);
+// warp-uniform (full-mask shuffles; both half-warps call)
+__device__ __forceinline__ float half_butterfly(float p) {
+#pragma unroll
+  for (int off = 8; off > 0; off >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
   return p;
 }
 
@@ -226,23 +235,36 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const long long t = t0 + u * nhw;
-      const double n2 = half_butterfly(chunk_sumsq(v[u]));
-      if (t < ntok && l16 == 0) out[t] = __double2float_rn(n2);
+      const float n2 = half_butterfly(chunk_sumsq(v[u]));
+      if (t < ntok && l16 == 0) out[t] = n2;
     }
   }
 }
 
-constexpr double kFx = 1099511627776.0;  // 2^40 fixed-point scale
-
-// llrint for |x| < 2^51 without the (slow) F2I.S64 conversion pipe: adding
-// 1.5 * 2^52 rounds to an integer (ties-to-even) in the mantissa.
-__device__ __forceinline__ long long fx_round(double x) {
-  constexpr double kMagic = 6755399441055744.0;
-  return __double_as_longlong(__dadd_rn(x, kMagic)) - 0x4338000000000000LL;
+// keydiff spec v2: inv = 1/sqrt(n2) (two RN ops; 0 below
+// 2^-100); unit components rint(x * inv * 2^21) summed exactly in int64;
+// score = -(dot(x, S * 2^-21) * inv).
+constexpr float kKdFx = 2097152.0f;  // 2^21
+__device__ __forceinline__ float kd_inv(float n2) {
+  return n2 >= 0x1p-100f ? __frcp_rn(__fsqrt_rn(n2)) : 0.0f;
 }
-constexpr int kKdTokens = 256;           // tokens per block (16 half-warps x 16)
+// rint(x * c) of this lane's 8 channels, biased by 0x4B400000 each (the
+// float-as-int of 1.5 * 2^23 + v): |v| < 2^22, so sums of < 512 biased words
+// wrap-add to (count * bias + sum v) mod 2^32 exactly.
+__device__ __forceinline__ void kd_fix_add(const uint4& v, float c, uint32_t (&acc)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // rint of the exact product: one fused rounding (ptxas fuses a packed mul + add anyway)
+    const float2 y = __ffma2_rn(make_float2(bf_lo(w[q]), bf_hi(w[q])), make_float2(c, c),
+                                make_float2(12582912.0f, 12582912.0f));
+    acc[2 * q] += __float_as_uint(y.x);
+    acc[2 * q + 1] += __float_as_uint(y.y);
+  }
+}
+constexpr int kKdTokens = 256;  // tokens per block (16 half-warps x 16)
 
-// keydiff pass 1: S[slice][d] = sum_t rint(x_td / |x_t| * 2^40) (exact int64)
+// keydiff pass 1: S[slice][d] += sum_t rint(x_td * inv_t * 2^21) (exact int64)
 __global__ void __launch_bounds__(256) k_keydiff_sum(const uint4* __restrict__ K, unsigned long long* __restrict__ S,
                                                      int T) {
   __shared__ long long part[16][kD];
@@ -250,24 +272,20 @@ __global__ void __launch_bounds__(256) k_keydiff_sum(const uint4* __restrict__ K
   const int slice = blockIdx.y;
   const int t_begin = blockIdx.x * kKdTokens;
   const uint4* Ks = K + static_cast<size_t>(slice) * T * 16;
-  long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t cnt = 0;
   const int t_end = min(T, t_begin + kKdTokens);
   for (int b = t_begin + (hw & ~1); b < t_end; b += 16) {  // warp-uniform trip count
     const int t = b + (hw & 1);
     const uint4 v = t < t_end ? Ks[static_cast<size_t>(t) * 16 + l16] : make_uint4(0, 0, 0, 0);
-    const double n2 = half_butterfly(chunk_sumsq(v));
-    const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-      const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-      acc[2 * j] += fx_round(__dmul_rn(a, kFx));
-      acc[2 * j + 1] += fx_round(__dmul_rn(b, kFx));
+    const float c = __fmul_rn(kd_inv(half_butterfly(chunk_sumsq(v))), kKdFx);
+    if (t < t_end) {
+      kd_fix_add(v, c, acc);
+      ++cnt;
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = acc[i];
+  for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = static_cast<int32_t>(acc[i] - cnt * 0x4B400000u);
   __syncthreads();
   if (threadIdx.x < kD) {
     long long s = 0;
@@ -277,7 +295,7 @@ __global__ void __launch_bounds__(256) k_keydiff_sum(const uint4* __restrict__ K
   }
 }
 
-// keydiff pass 2: score_t = -(khat_t . S) in the canonical FP64 order.
+// keydiff pass 2: score_t = -(dot(x_t, S * 2^-21) * inv_t) in the canonical order.
 __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__ K,
                                                        const long long* __restrict__ S, float* __restrict__ out,
                                                        int T) {
@@ -285,27 +303,19 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
   const int slice = blockIdx.y;
   const int t_begin = blockIdx.x * kKdTokens;
   const uint4* Ks = K + static_cast<size_t>(slice) * T * 16;
-  double sd[8];
+  float2 sd[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    sd[i] = __dmul_rn(__ll2double_rn(S[static_cast<size_t>(slice) * kD + l16 * 8 + i]), 1.0 / kFx);
+  for (int q = 0; q < 4; ++q) {
+    const long long* Sq = S + static_cast<size_t>(slice) * kD + l16 * 8 + 2 * q;
+    sd[q] = make_float2(__fmul_rn(__ll2float_rn(Sq[0]), 1.0f / kKdFx), __fmul_rn(__ll2float_rn(Sq[1]), 1.0f / kKdFx));
+  }
   const int t_end = min(T, t_begin + kKdTokens);
   for (int b = t_begin + (hw & ~1); b < t_end; b += 16) {  // warp-uniform trip count
     const int t = b + (hw & 1);
     const uint4 v = t < t_end ? __ldcs(Ks + static_cast<size_t>(t) * 16 + l16) : make_uint4(0, 0, 0, 0);
-    const double n2 = half_butterfly(chunk_sumsq(v));
-    const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-      const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-      acc = __dadd_rn(acc, __dmul_rn(a, sd[2 * j]));
-      acc = __dadd_rn(acc, __dmul_rn(b, sd[2 * j + 1]));
-    }
-    const double p = half_butterfly(acc);
-    if (l16 == 0 && t < t_end) out[static_cast<size_t>(slice) * T + t] = __double2float_rn(-p);
+    const float inv = kd_inv(half_butterfly(chunk_sumsq(v)));
+    const float p = half_butterfly(chunk_dot(v, sd));
+    if (l16 == 0 && t < t_end) out[static_cast<size_t>(slice) * T + t] = -__fmul_rn(p, inv);
   }
 }
 
@@ -375,6 +385,31 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a,
   u1 = __float_as_uint(r.y);
 }
 
+// One (row, 32-token block) of the epilogue: block shift M, E values packed
+// as u16 pairs, returns the block sum L. Ragged blocks mask tokens >= nv.
+template <bool kRagged>
+__device__ __forceinline__ uint32_t snap_block(uint32_t (&I)[32], int nv, float a, int32_t& M, uint32_t (&pk)[16]) {
+  int32_t m = INT_MIN;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (!kRagged || i < nv) m = max(m, static_cast<int32_t>(I[i]));
+  M = static_cast<int32_t>(ceilf(__fmul_rn(__int2float_rn(m), a)));
+  const float c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
+  uint32_t Lraw = 0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    uint32_t u0, u1;
+    snap_exp_pair(I[i], I[i + 1], a, c, u0, u1);
+    if (kRagged) {
+      if (i >= nv) u0 = 0x4B000000u;
+      if (i + 1 >= nv) u1 = 0x4B000000u;
+    }
+    Lraw += u0 + u1;
+    pk[i >> 1] = __byte_perm(u0, u1, 0x5410);  // low 16 bits of each = E (E < 2^16)
+  }
+  return Lraw - 32u * 0x4B000000u;
+}
+
 // Half-warp int8 quantisation of one 128-channel row (lane: channels
 // 8*l16..8*l16+7): absmax/127 scale, rint(x * (127/absmax)) codes written to
 // row r of a SW128 K-major tile. Returns the scale. Warp-uniform.
@@ -387,9 +422,9 @@ __device__ __forceinline__ float quant_row_i8(const float (&x)[8], uint8_t* tile
   const float inv = a > 0.0f ? __fdiv_rn(127.0f, a) : 0.0f;
   uint32_t lo = 0, hi = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const float y = fminf(fmaxf(__fmul_rn(x[e], inv), -127.0f), 127.0f);
-    const uint32_t c = (__float_as_uint(__fadd_rn(y, 12582912.0f)) - 0x4B400000u) & 0xffu;
+  for (int e = 0; e < 8; ++e) {  // rint of the exact product x * inv, clamped to +-127
+    const int q = static_cast<int>(__float_as_uint(__fmaf_rn(x[e], inv, 12582912.0f)) - 0x4B400000u);
+    const uint32_t c = static_cast<uint32_t>(min(127, max(-127, q))) & 0xffu;
     if (e < 4) lo |= c << (8 * e);
     else hi |= c << (8 * (e - 4));
   }
@@ -441,8 +476,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   const int t_lo = tile0 * 128, n_loc = max(0, min(P - t_lo, ntl * 128));
   const int nblk = (n_loc + 31) / 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  extern __shared__ uint8_t snap_raw[];
-  SnapSmem& sm = *reinterpret_cast<SnapSmem*>((reinterpret_cast<uintptr_t>(snap_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) uint8_t snap_raw[];
+  // 1024-align by offset (keeps the shared address space visible: LDS/STS, not generic LD/ST)
+  SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + ((1024u - (smem_u32(snap_raw) & 1023u)) & 1023u));
   const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
 
   if (tid == 0) {
@@ -491,6 +527,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     uint32_t mx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
     if (lane == 0) sm.amax[warp] = mx;
     __syncthreads();
+    if (tid == 0 && j + 1 < ntl) {  // every thread holds its slice of the tile: prefetch the next one now
+      const int nrows = min(128, n_loc - (j + 1) * 128);
+      fence_async_smem();
+      mbar_expect_tx(&sm.full, nrows * 256);
+      bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+    }
     mx = 0;
 #pragma unroll
     for (int w = 0; w < 16; ++w) mx = max(mx, sm.amax[w]);
@@ -504,10 +546,11 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       const uint32_t ww[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        float2 y0 = __fmul2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv));
-        float2 y1 = __fmul2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])), make_float2(inv, inv));
-        y0 = __fadd2_rn(y0, make_float2(12582912.0f, 12582912.0f));
-        y1 = __fadd2_rn(y1, make_float2(12582912.0f, 12582912.0f));
+        // rint of the exact product x * inv (fused rounding, oracle quant_i8)
+        const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
+                                     make_float2(12582912.0f, 12582912.0f));
+        const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])), make_float2(inv, inv),
+                                     make_float2(12582912.0f, 12582912.0f));
         const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
         const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
         wq[2 * i + h2] = __byte_perm(lo, hi, 0x5410);
@@ -522,11 +565,6 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core / bulk copy engine
     __syncthreads();
     if (tid == 0) {
-      if (j + 1 < ntl) {  // stage is consumed: prefetch the next tile under this one's MMA + epilogue
-        const int nrows = min(128, n_loc - (j + 1) * 128);
-        mbar_expect_tx(&sm.full, nrows * 256);
-        bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
-      }
       tc_fence_after();
       const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(sm.k8);
 #pragma unroll
@@ -544,23 +582,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     uint32_t pk[16];
     if (r < R && nv > 0) {
       const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
-      int32_t m = INT_MIN;
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < nv) m = max(m, static_cast<int32_t>(I[i]));
-      M = static_cast<int32_t>(ceilf(__fmul_rn(__int2float_rn(m), a)));
-      const float c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
-      uint32_t Lraw = 0;
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        uint32_t u0, u1;
-        snap_exp_pair(I[i], I[i + 1], a, c, u0, u1);
-        if (i >= nv) u0 = 0x4B000000u;
-        if (i + 1 >= nv) u1 = 0x4B000000u;
-        Lraw += u0 + u1;
-        pk[i >> 1] = __byte_perm(u0, u1, 0x5410);  // low 16 bits of each = E (E < 2^16)
-      }
-      L = Lraw - 32u * 0x4B000000u;
+      L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) pk[i] = 0;
@@ -574,54 +596,81 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     __syncthreads();  // TMEM accumulator and K8 free for the next tile
   }
 
-  // ---- row shift and sum across the cluster
-  if (tid < 128) {
+  // ---- row shift and sum across the cluster (4 threads per row, blocks split 4 ways)
+  const int crow = tid >> 2, cq = tid & 3;
+  {
     int32_t m = INT_MIN;
-    for (int b = 0; b < nblk; ++b) m = max(m, sm.mb[b][tid]);
-    sm.mloc[tid] = m;
+    for (int b = cq; b < nblk; b += 4) m = max(m, sm.mb[b][crow]);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if (cq == 0) sm.mloc[crow] = m;
   }
-  cl.sync();
-  if (tid < 128) {
+  cluster_sync_smem();
+  {
     int32_t m = INT_MIN;
-    for (int c = 0; c < C; ++c) m = max(m, cl.map_shared_rank(sm.mloc, c)[tid]);
-    sm.mrow[tid] = m;
+    for (int c = cq; c < C; c += 4) m = max(m, cl.map_shared_rank(sm.mloc, c)[crow]);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
     unsigned long long Ls = 0;
-    for (int b = 0; b < nblk; ++b) {
-      const int64_t sh = int64_t(m) - sm.mb[b][tid];
-      if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][tid]) << 16) >> sh;
+    for (int b = cq; b < nblk; b += 4) {
+      const int64_t sh = int64_t(m) - sm.mb[b][crow];
+      if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][crow]) << 16) >> sh;
     }
-    sm.lloc[tid] = Ls;
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+    if (cq == 0) {
+      sm.mrow[crow] = m;
+      sm.lloc[crow] = Ls;
+    }
   }
-  cl.sync();
-  if (tid < 128) {
+  cluster_sync_smem();
+  {
     unsigned long long Ls = 0;
-    for (int c = 0; c < C; ++c) Ls += cl.map_shared_rank(sm.lloc, c)[tid];
-    const unsigned long long wt = (tid < R && Ls) ? (1ull << 61) / Ls : 0ull;
-    const int32_t m = sm.mrow[tid];
-    for (int b = 0; b < nblk; ++b) {
-      const int64_t sh = int64_t(m) - sm.mb[b][tid];
-      sm.lb[b][tid] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
+    for (int c = cq; c < C; c += 4) Ls += cl.map_shared_rank(sm.lloc, c)[crow];
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
+    Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+    const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
+    const int32_t m = sm.mrow[crow];
+    for (int b = cq; b < nblk; b += 4) {
+      const int64_t sh = int64_t(m) - sm.mb[b][crow];
+      sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
     }
   }
   __syncthreads();
-  // ---- votes: thread = token (block b = warp)
+  // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows; rows
+  // >= R have zero weight, so every loop runs the full (padded) row range
   unsigned long long* vote = reinterpret_cast<unsigned long long*>(sm.stage);
   {
-    unsigned long long acc = 0;
-    if (tid < n_loc) {
-      const uint16_t* ecol = reinterpret_cast<const uint16_t*>(sm.e) + tid;
-      const uint32_t* wb = sm.lb[warp];
-      for (int r0 = 0; r0 < R; r0 += 4) {
+    const int p = tid & 255, rh = tid >> 8, b = p >> 4;
+    const uint32_t* erow = reinterpret_cast<const uint32_t*>(sm.e + rh * 64 * kSnapEStride) + p;
+    const uint32_t* wb = sm.lb[b] + rh * 64;
+    unsigned long long a0 = 0, a1 = 0;
+    if (2 * p < n_loc) {
+#pragma unroll 4
+      for (int r0 = 0; r0 < 64; r0 += 4) {
         const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
         const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (r0 + q < R) acc += static_cast<unsigned long long>(ecol[(r0 + q) * (kSnapEStride / 2)]) * ww[q];
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t e2 = erow[(r0 + q) * (kSnapEStride / 4)];
+          a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
+          a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+        }
       }
     }
-    vote[tid] = acc;
+    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm.e);  // E fully consumed below
+    __syncthreads();
+    if (rh == 1) {
+      part[2 * p] = a0;
+      part[2 * p + 1] = a1;
+    }
+    __syncthreads();
+    if (rh == 0) {
+      vote[2 * p] = a0 + part[2 * p];
+      vote[2 * p + 1] = a1 + part[2 * p + 1];
+    }
   }
-  cl.sync();  // every CTA's votes visible
+  cluster_sync_smem();  // every CTA's votes visible
   // ---- pooling (max over +-pool/2 within the prefix) and scores
   float* out = scores + static_cast<size_t>(slice) * T;
   const int half = pool / 2;
@@ -641,7 +690,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   }
   if (rank == C - 1)
     for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
-  cl.sync();  // no CTA leaves while its votes may still be read
+  cluster_sync_smem();  // no CTA leaves while its votes may still be read
   if (warp == 0) tmem_dealloc(tmem, 128);
 }
 
@@ -1208,7 +1257,7 @@ using FuseScan = cub::BlockScan<int, kFuseThreads>;
 
 static size_t fuse_smem_bytes(int T) {
   const size_t per = (T + kFuseC - 1) / kFuseC;
-  return kFuseUnion + al256(4 * per);
+  return kFuseUnion + 2 * al256(4 * per);
 }
 
 __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2)
@@ -1223,10 +1272,11 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
   PackKSmem& pk = *reinterpret_cast<PackKSmem*>(fsm);
   long long(*part)[kD] = reinterpret_cast<long long(*)[kD]>(fsm);
   uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFuseUnion);
+  float* kinv = reinterpret_cast<float*>(fsm + kFuseUnion + ((4 * per + 255) & ~255));  // keydiff: per-token 1/|k|
   __shared__ int hist[2][256];
   __shared__ int tot[256];
   __shared__ long long sfix[kD];
-  __shared__ double sdir[kD];
+  __shared__ float sdir[kD];
   __shared__ int cnt[2];
   __shared__ int s_rem, s_bucket;
   __shared__ typename FuseScan::TempStorage scan_tmp;
@@ -1248,25 +1298,22 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
   // ---- phase 1: token scores of [t_lo, t_hi) as orderable keys
   if (scorer == KVT_SCORER_KNORM) {
     stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
-      const double n2 = half_butterfly(chunk_sumsq(v));
-      if (live && l16 == 0) keys[t] = score_key(__double2float_rn(n2));
+      const float n2 = half_butterfly(chunk_sumsq(v));
+      if (live && l16 == 0) keys[t] = score_key(n2);
     });
-  } else {  // keydiff: exact fixed-point mean direction over the whole slice, then cosine
-    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    stream_rows(Ks, n_loc, ring, full, seq, [&](int, bool, const uint4& v) {
-      const double n2 = half_butterfly(chunk_sumsq(v));  // zero rows add nothing
-      const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double a = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-        const double b = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-        acc[2 * j] += fx_round(__dmul_rn(a, kFx));
-        acc[2 * j + 1] += fx_round(__dmul_rn(b, kFx));
+  } else {  // keydiff: exact fixed-point sum of unit keys over the whole slice, then cosine
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t cnt_t = 0;  // <= per / 16 tokens per lane: biased u32 sums cannot wrap
+    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
+      const float inv = kd_inv(half_butterfly(chunk_sumsq(v)));
+      if (live) {
+        kd_fix_add(v, __fmul_rn(inv, kKdFx), acc);
+        ++cnt_t;
+        if (l16 == 0) kinv[t] = inv;
       }
     });
 #pragma unroll
-    for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = acc[i];
+    for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = static_cast<int32_t>(acc[i] - cnt_t * 0x4B400000u);
     __syncthreads();
     if (tid < kD) {
       long long sum = 0;
@@ -1274,30 +1321,19 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
       for (int i = 0; i < 16; ++i) sum += part[i][tid];
       sfix[tid] = sum;
     }
-    cl.sync();
+    cluster_sync_smem();
     if (tid < kD) {
       long long sum = 0;
       for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(sfix, c)[tid];
-      sdir[tid] = __dmul_rn(__ll2double_rn(sum), 1.0 / kFx);
+      sdir[tid] = __fmul_rn(__ll2float_rn(sum), 1.0f / kKdFx);
     }
     __syncthreads();
-    double sd[8];
+    float2 sd[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sd[i] = sdir[l16 * 8 + i];
+    for (int q = 0; q < 4; ++q) sd[q] = make_float2(sdir[l16 * 8 + 2 * q], sdir[l16 * 8 + 2 * q + 1]);
     stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {  // second pass: L2 hits
-      const double n2 = half_butterfly(chunk_sumsq(v));
-      const double inv = n2 > 0.0 ? __drcp_rn(__dsqrt_rn(n2)) : 0.0;
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-      double a = 0.0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double x0 = __dmul_rn(double(bf2f(w[j] & 0xffffu)), inv);
-        const double x1 = __dmul_rn(double(bf2f(w[j] >> 16)), inv);
-        a = __dadd_rn(a, __dmul_rn(x0, sd[2 * j]));
-        a = __dadd_rn(a, __dmul_rn(x1, sd[2 * j + 1]));
-      }
-      const double p = half_butterfly(a);
-      if (live && l16 == 0) keys[t] = score_key(__double2float_rn(-p));
+      const float p = half_butterfly(chunk_dot(v, sd));
+      if (live && l16 == 0) keys[t] = score_key(-__fmul_rn(p, kinv[t]));
     });
   }
   __syncthreads();
@@ -1313,7 +1349,7 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
       const uint32_t key = keys[t];
       if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255], 1);
     }
-    cl.sync();
+    cluster_sync_smem();
     {
       int sum = 0;
       for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(h, c)[tid];
@@ -1346,7 +1382,7 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
     cnt[0] = above_all;
     cnt[1] = eq_all;
   }
-  cl.sync();
+  cluster_sync_smem();
   int a_base = 0, e_base = 0;
   for (int c = 0; c < rank; ++c) {
     const int* rc = cl.map_shared_rank(cnt, c);

@@ -90,6 +90,17 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Cluster barrier for DSMEM exchange only: release/acquire restricted to
+// shared memory (MEMBAR.CTA instead of the MEMBAR.GPU a full cluster-scope
+// release costs). Global-memory writes are NOT ordered by it.
+__device__ __forceinline__ void cluster_sync_smem() {
+  asm volatile(
+      "fence.release.sync_restrict::shared::cta.cluster;\n\t"
+      "barrier.cluster.arrive.relaxed.aligned;\n\t"
+      "barrier.cluster.wait.aligned;\n\t"
+      "fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+}
+
 // 32 consecutive 32-bit TMEM columns of this warp's 32 lanes -> registers.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(

@@ -50,9 +50,45 @@ def gen_q(L, H, G, W, D, q_seed):
     return synth_bf16(q_seed, 0x51, i, d % 16 == 3).reshape(L, Hq, W, D)
 
 
+def row_dot32(x, y):
+    """Canonical fp32 row dot product: per 8-channel chunk an
+    even- and an odd-channel fma chain, chunk = even + odd, then a butterfly
+    over the 16 chunk sums (strides 8, 4, 2, 1)."""
+    x = x.astype(np.float32)
+    y = np.broadcast_to(y.astype(np.float32), x.shape)
+    sh = x.shape[:-1] + (16, 8)
+    xc, yc = x.reshape(sh), y.reshape(sh)
+    e = np.zeros(sh[:-1], np.float32)
+    o = np.zeros(sh[:-1], np.float32)
+    for q in range(4):
+        e = fma32(xc[..., 2 * q], yc[..., 2 * q], e)
+        o = fma32(xc[..., 2 * q + 1], yc[..., 2 * q + 1], o)
+    p = (e + o).astype(np.float32)
+    idx = np.arange(16)
+    for off in (8, 4, 2, 1):
+        p = (p + p[..., idx ^ off]).astype(np.float32)
+    return p[..., 0]
+
+
 def knorm_scores(k):
-    x = bf2f(k).astype(np.float64)
-    return (x * x).sum(-1).astype(np.float32)  # exact in float64 for the synthetic range
+    x = bf2f(k)
+    return row_dot32(x, x)
+
+
+def keydiff_scores(k):
+    """Exact keydiff v2: inverse norms 1/sqrt(n2) (two RN fp32
+    ops, 0 below 2^-100), unit components rounded to 2^-21 fixed point and
+    summed in int64, then -(dot(x, S * 2^-21) * inv)."""
+    x = bf2f(k)
+    n2 = row_dot32(x, x)
+    ok = n2 >= np.float32(2.0 ** -100)
+    inv = np.where(ok, (np.float32(1) / np.sqrt(np.where(ok, n2, 1)).astype(np.float32)).astype(np.float32), 0)
+    inv = inv.astype(np.float32)
+    c = (inv * np.float32(2.0 ** 21)).astype(np.float32)
+    f = np.rint(x.astype(np.float64) * c[..., None].astype(np.float64)).astype(np.int64)  # exact product
+    S = f.sum(-2, keepdims=True)
+    sd = (S.astype(np.float32) * np.float32(2.0 ** -21)).astype(np.float32)
+    return (-(row_dot32(x, sd) * inv).astype(np.float32)).astype(np.float32)
 
 
 def keydiff_similarity(k):
@@ -84,11 +120,8 @@ def fma32(a, b, c):
     hi = np.nextafter(r, np.float32(np.inf)).astype(np.float64)
     rd = r.astype(np.float64)
     # s exactly halfway between r and a neighbour: the exact value decides
-    up = (s == (rd + hi) / 2) & (err > 0)
-    dn = (s == (rd + lo) / 2) & (err < 0)
-    mid_lo = (s == (rd + lo) / 2) & (err > 0)   # exact value above the midpoint -> r is right
-    mid_hi = (s == (rd + hi) / 2) & (err < 0)   # exact value below the midpoint -> r is right
-    del mid_lo, mid_hi
+    up = (s == (rd + hi) / 2) & (err > 0)  # exact value just above the upper midpoint
+    dn = (s == (rd + lo) / 2) & (err < 0)  # exact value just below the lower midpoint
     r = np.where(up, hi.astype(np.float32), r)
     r = np.where(dn, lo.astype(np.float32), r)
     return r.astype(np.float32)
@@ -100,7 +133,7 @@ def quant_i8(x, axis):
     a = np.abs(x).max(axis=axis, keepdims=True)
     safe = np.where(a > 0, a, np.float32(1))
     inv = (np.float32(127) / safe).astype(np.float32)
-    q = np.clip(np.rint((x * inv).astype(np.float32)), -127, 127)
+    q = np.clip(np.rint(x.astype(np.float64) * inv.astype(np.float64)), -127, 127)  # rint of the exact product
     q = np.where(a > 0, q, 0).astype(np.int64)
     scale = np.where(a > 0, (a / np.float32(127)).astype(np.float32), np.float32(0))
     return q, scale.astype(np.float32)

@@ -118,7 +118,15 @@ def test_keydiff_scores_track_cosine_similarity(lib):
     k, _ = _kv(1, 2, 300)
     got = _scores(lib, s, plan(lib, "keydiff", 0.5, s), k).astype(np.float64)
     sim = R.keydiff_similarity(k)
-    np.testing.assert_allclose(-got, sim, rtol=1e-5, atol=1e-6)
+    # fp32 dot of a unit key with a sum of 300 unit keys: absolute error ~ 1e-7 * T
+    np.testing.assert_allclose(-got, sim, rtol=1e-5, atol=1e-7 * 300)
+
+
+def test_keydiff_scores_exact(lib):
+    s = shape(2, 2, 333)
+    k, _ = _kv(2, 2, 333)
+    got = _scores(lib, s, plan(lib, "keydiff", 0.5, s), k)
+    assert np.array_equal(got.view(np.uint32), R.keydiff_scores(k).view(np.uint32))
 
 
 def test_snapkv_scores_match_numpy(lib):
