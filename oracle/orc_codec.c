@@ -594,11 +594,13 @@ static qparam_t make_param(float mn, float mx, int bits) {
   return p;
 }
 
+/* code = clamp(rint(exact((x - z) * inv)), 0, 2^b - 1): the difference is
+ * one fp32 op, the product is exact (double) and rounded once, ties to even */
 static uint32_t quant(float x, const qparam_t* p, int bits) {
-  const float y = (x - p->zf) * p->inv;
-  float r = nearbyintf(y);
-  const float hi = (float)((1 << bits) - 1);
-  if (!(r >= 0.0f)) r = 0.0f;
+  const double y = (double)(x - p->zf) * (double)p->inv;
+  double r = nearbyint(y);
+  const double hi = (double)((1 << bits) - 1);
+  if (!(r >= 0.0)) r = 0.0;
   if (r > hi) r = hi;
   return (uint32_t)r;
 }

@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <string>
 
@@ -941,19 +942,28 @@ __global__ void __launch_bounds__(256) k_gather16(const uint4* __restrict__ K, c
 // K quantisation: per channel over a group of <=128 kept tokens, one
 // 256-thread block per group. Thread (rs, cg) = rows 8rs..8rs+7 x channels
 // 8cg..8cg+7 held in registers (8 independent 16-byte loads in flight per
-// thread, no smem staging). Channel min/max: packed bf16x2 mins (max as the
-// min of negated values, exact) -> lane^16 shuffle -> smem over the 8 warps.
-// 128 threads make the per-channel fp16 params, then every thread quantises
-// its 64 values with packed fp32x2 math and writes whole code words.
-// Block-uniform: call from every thread of a 256-thread block.
+// thread, no smem staging). Channel min/max: packed bf16x2 min/max ->
+// lane^16 shuffle -> smem over the 8 warps. 128 threads make the
+// per-channel fp16 params, then every thread quantises its 64 values
+// (quant8_fast: 2 packed fp32 ops + 3 integer lane ops per channel pair,
+// exact FP64 fallback for groups whose parameters do not bound the codes)
+// and writes whole code words. Block-uniform: every thread of a 256-thread
+// block calls it.
 struct PackKSmem {
-  uint32_t red[8][16][8];  // [warp][cg][pair: 4 min | 4 -max] bf16x2
+  uint32_t red[8][16][8];  // [warp][cg][4 min | 4 max] bf16x2
   float zf[kD], inv[kD];
+  int fast[kD];
 };
 
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+template <int BITS>
 __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
                                              uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
-                                             uint16_t* __restrict__ kz, int T, int k, int bits, int slice, int g,
+                                             uint16_t* __restrict__ kz, int T, int k, int slice, int g,
                                              PackKSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rs = tid >> 4, cg = tid & 15;
@@ -965,31 +975,44 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = rs * 8 + i;
-    v[i] = r < nr ? __ldcs(Ks + static_cast<size_t>(ix[r]) * 16) : make_uint4(0, 0, 0, 0);
+    v[i] = r < nr ? __ldcs(Ks + static_cast<uint32_t>(ix[r]) * 16u) : make_uint4(0, 0, 0, 0);
   }
-  const uint32_t kInf2 = 0x7f807f80u, kNeg = 0x80008000u;
-  uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, nmx[4] = {kInf2, kInf2, kInf2, kInf2};
+  const uint32_t kInf2 = 0x7f807f80u, kNInf2 = 0xff80ff80u;
+  uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, mx[4] = {kNInf2, kNInf2, kNInf2, kNInf2};
+  const int nmine = max(0, min(8, nr - rs * 8));
+  if (nmine == 8) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (rs * 8 + i < nr) {
+    for (int i = 0; i < 8; ++i) {
       const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         mn[q] = bmin2(mn[q], w[q]);
-        nmx[q] = bmin2(nmx[q], w[q] ^ kNeg);
+        mx[q] = bmax2(mx[q], w[q]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < nmine) {
+        const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mn[q] = bmin2(mn[q], w[q]);
+          mx[q] = bmax2(mx[q], w[q]);
+        }
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     mn[q] = bmin2(mn[q], __shfl_xor_sync(0xffffffffu, mn[q], 16));
-    nmx[q] = bmin2(nmx[q], __shfl_xor_sync(0xffffffffu, nmx[q], 16));
+    mx[q] = bmax2(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], 16));
   }
   if (lane < 16) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       sm.red[warp][cg][q] = mn[q];
-      sm.red[warp][cg][4 + q] = nmx[q];
+      sm.red[warp][cg][4 + q] = mx[q];
     }
   }
   __syncthreads();
@@ -999,76 +1022,74 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
 #pragma unroll
     for (int w = 1; w < 8; ++w) {
       a = bmin2(a, sm.red[w][c][q]);
-      b = bmin2(b, sm.red[w][c][4 + q]);
+      b = bmax2(b, sm.red[w][c][4 + q]);
     }
-    const float fmn = hi ? bf_hi(a) : bf_lo(a);
-    const float fmx = -(hi ? bf_hi(b) : bf_lo(b));
-    const QParam p = make_param(fmn, fmx, bits);
+    const QParam p = make_param(hi ? bf_hi(a) : bf_lo(a), hi ? bf_hi(b) : bf_lo(b), BITS);
     sm.zf[tid] = p.zf;
     sm.inv[tid] = p.inv;
+    sm.fast[tid] = p.fast;
     const size_t po = (static_cast<size_t>(slice) * ng + g) * kD + tid;
     ks[po] = p.s16;
     kz[po] = p.z16;
   }
   __syncthreads();
   float z[8], iv[8];
+  bool fast = true;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     z[e] = sm.zf[cg * 8 + e];
     iv[e] = sm.inv[cg * 8 + e];
+    fast &= sm.fast[cg * 8 + e] != 0;
   }
-  const float hiv = float((1 << bits) - 1);
-  const int wpr = kD * bits / 32;
+  constexpr int wpr = kD * BITS / 32;
   uint32_t* out = kc + static_cast<size_t>(slice) * k * wpr;
+  float2 nz[4], iv2[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    nz[q] = make_float2(-z[2 * q], -z[2 * q + 1]);
+    iv2[q] = make_float2(iv[2 * q], iv[2 * q + 1]);
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = rs * 8 + i;
-    const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-    uint32_t c[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      quant2(bf_lo(w[q]), bf_hi(w[q]), z[2 * q], z[2 * q + 1], iv[2 * q], iv[2 * q + 1], hiv, c[2 * q], c[2 * q + 1]);
+    uint32_t lanes[4];
+    if (fast) quant8_fast<BITS>(v[i], nz, iv2, lanes);
+    else quant8_exact<BITS>(v[i], z, iv, lanes);
+    const uint2 c = pack8<BITS>(lanes);
     uint32_t* orow = out + static_cast<size_t>(j0 + r) * wpr;
-    if (bits == 8) {
-      if (r < nr)
-        __stcs(reinterpret_cast<uint2*>(orow) + cg,
-               make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
-                          c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
-    } else if (bits == 4) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) word |= c[e] << (4 * e);
-      if (r < nr) __stcs(orow + cg, word);
+    if (BITS == 8) {
+      if (r < nr) __stcs(reinterpret_cast<uint2*>(orow) + cg, c);
+    } else if (BITS == 4) {
+      if (r < nr) __stcs(orow + cg, c.x);
     } else {  // 2 bits: channels 16w..16w+15 = lanes cg (even) and cg + 1
-      uint32_t h = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) h |= c[e] << (2 * e);
-      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
-      if (r < nr && (cg & 1) == 0) __stcs(orow + (cg >> 1), h | (other << 16));
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, c.x, 1);
+      if (r < nr && (cg & 1) == 0) __stcs(orow + (cg >> 1), c.x | (other << 16));
     }
   }
   __syncthreads();  // smem reused by the next group
 }
 
+template <int BITS>
 __global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
                                                 uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
-                                                uint16_t* __restrict__ kz, int T, int k, int bits) {
+                                                uint16_t* __restrict__ kz, int T, int k) {
   __shared__ PackKSmem sm;
-  pack_k_group(K, idx, kc, ks, kz, T, k, bits, blockIdx.y, blockIdx.x, sm);
+  pack_k_group<BITS>(K, idx, kc, ks, kz, T, k, blockIdx.y, blockIdx.x, sm);
 }
 
 // V quantisation: per kept token over its 128 channels. A half-warp packs
 // kVRows rows: loads all of them first (kVRows 16-byte loads in flight per
-// lane), reduces each row's (min, -max) as one bf16x2 butterfly, lane i
+// lane), reduces each row's (min, max) as one bf16x2 butterfly, lane i
 // makes row i's fp16 params (one division per row, not per lane), then the
-// params are shuffled back for the packed fp32x2 quantisation.
+// params are shuffled back for quant8_fast.
 // Warp-uniform: both half-warps must call (shuffles use the full mask).
 constexpr int kVRows = 8;
 
+template <int BITS>
 __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
                                             int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
                                             uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
-                                            int bits, int slice, int j_first) {
+                                            int slice, int j_first) {
   const int l16 = threadIdx.x & 15, base = threadIdx.x & 16;
   const int32_t* ix = idx + static_cast<size_t>(slice) * k;
   const uint4* Vs = V + static_cast<size_t>(slice) * T * 16 + l16;
@@ -1078,67 +1099,81 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
   for (int i = 0; i < kVRows; ++i) tok[i] = j_first + i < k ? ix[j_first + i] : 0;
 #pragma unroll
   for (int i = 0; i < kVRows; ++i)
-    v[i] = j_first + i < k ? __ldcs(Vs + static_cast<size_t>(tok[i]) * 16) : make_uint4(0, 0, 0, 0);
-  const uint32_t kNeg = 0x80008000u;
-  uint32_t mm_mine = 0;  // lane i < kVRows: (min, -max) of row i as bf16 pair
+    v[i] = j_first + i < k ? __ldcs(Vs + static_cast<uint32_t>(tok[i]) * 16u) : make_uint4(0, 0, 0, 0);
+  uint32_t mm_mine = 0;  // lane i < kVRows: (min, max) of row i as a bf16 pair
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
-    const uint32_t a = bmin2(v[i].x, v[i].y), b = bmin2(v[i].z, v[i].w);
-    const uint32_t m2 = bmin2(a, b);  // per-lane mins of even / odd channels
-    const uint32_t n2 = bmin2(bmin2(v[i].x ^ kNeg, v[i].y ^ kNeg), bmin2(v[i].z ^ kNeg, v[i].w ^ kNeg));
-    // (min, -max) of the lane's 8 channels as one bf16 pair
-    uint32_t mm = bmin2(__byte_perm(m2, n2, 0x5410), __byte_perm(m2, n2, 0x7632));
+    const uint32_t m2 = bmin2(bmin2(v[i].x, v[i].y), bmin2(v[i].z, v[i].w));  // mins of even / odd channels
+    const uint32_t x2 = bmax2(bmax2(v[i].x, v[i].y), bmax2(v[i].z, v[i].w));
+    // (min of the lane's 8 channels, max of them) as one bf16 pair
+    uint32_t lo = bmin2(m2, m2 >> 16), hi = bmax2(x2, x2 >> 16);
+    uint32_t mm = __byte_perm(lo, hi, 0x5410);
 #pragma unroll
-    for (int off = 8; off > 0; off >>= 1) mm = bmin2(mm, __shfl_xor_sync(0xffffffffu, mm, off));
+    for (int off = 8; off > 0; off >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, mm, off);
+      mm = __byte_perm(bmin2(mm, o), bmax2(mm, o), 0x7610);
+    }
     if (l16 == i) mm_mine = mm;
   }
   QParam p{};
-  if (l16 < kVRows) p = make_param(bf_lo(mm_mine), -bf_hi(mm_mine), bits);
+  if (l16 < kVRows) p = make_param(bf_lo(mm_mine), bf_hi(mm_mine), BITS);
   const int j_mine = j_first + l16;
   if (l16 < kVRows && j_mine < k) {
     vs[static_cast<size_t>(slice) * k + j_mine] = p.s16;
     vz[static_cast<size_t>(slice) * k + j_mine] = p.z16;
     if (oidx) oidx[static_cast<size_t>(slice) * k + j_mine] = ix[j_mine];
   }
-  const float hiv = float((1 << bits) - 1);
-  const int wpr = kD * bits / 32;
+  constexpr int wpr = kD * BITS / 32;
+  const int fast_mine = p.fast ? 1 : 0;
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
     const int j = j_first + i;
     const float zf = __shfl_sync(0xffffffffu, p.zf, base + i), inv = __shfl_sync(0xffffffffu, p.inv, base + i);
-    const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-    uint32_t c[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) quant2(bf_lo(w[q]), bf_hi(w[q]), zf, zf, inv, inv, hiv, c[2 * q], c[2 * q + 1]);
+    const int fast = __shfl_sync(0xffffffffu, fast_mine, base + i);
+    uint32_t lanes[4];
+    if (fast) {
+      const float2 nz[4] = {make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf)};
+      const float2 iv[4] = {make_float2(inv, inv), make_float2(inv, inv), make_float2(inv, inv), make_float2(inv, inv)};
+      quant8_fast<BITS>(v[i], nz, iv, lanes);
+    } else {
+      const float z8[8] = {zf, zf, zf, zf, zf, zf, zf, zf}, i8[8] = {inv, inv, inv, inv, inv, inv, inv, inv};
+      quant8_exact<BITS>(v[i], z8, i8, lanes);
+    }
+    const uint2 c = pack8<BITS>(lanes);
     uint32_t* out = vc + (static_cast<size_t>(slice) * k + j) * wpr;
     const bool live = j < k;
-    if (bits == 8) {
-      if (live)
-        __stcs(reinterpret_cast<uint2*>(out) + l16,
-               make_uint2(c[0] | (c[1] << 8) | (c[2] << 16) | (c[3] << 24),
-                          c[4] | (c[5] << 8) | (c[6] << 16) | (c[7] << 24)));
-    } else if (bits == 4) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) word |= c[e] << (4 * e);
-      if (live) __stcs(out + l16, word);
+    if (BITS == 8) {
+      if (live) __stcs(reinterpret_cast<uint2*>(out) + l16, c);
+    } else if (BITS == 4) {
+      if (live) __stcs(out + l16, c.x);
     } else {
-      uint32_t h = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) h |= c[e] << (2 * e);
-      const uint32_t other = __shfl_xor_sync(0xffffffffu, h, 1);
-      if (live && (l16 & 1) == 0) __stcs(out + (l16 >> 1), h | (other << 16));
+      const uint32_t other = __shfl_xor_sync(0xffffffffu, c.x, 1);
+      if (live && (l16 & 1) == 0) __stcs(out + (l16 >> 1), c.x | (other << 16));
     }
   }
 }
 
 // grid (ceil(k / (16 * kVRows)), S): 16 half-warps x kVRows rows per block
+template <int BITS>
 __global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
                                                 int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
-                                                uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
-                                                int bits) {
-  pack_v_rows(V, idx, oidx, vc, vs, vz, T, k, bits, blockIdx.y,
-              (blockIdx.x * 16 + (threadIdx.x >> 4)) * kVRows);
+                                                uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k) {
+  pack_v_rows<BITS>(V, idx, oidx, vc, vs, vz, T, k, blockIdx.y, (blockIdx.x * 16 + (threadIdx.x >> 4)) * kVRows);
+}
+
+template <int BITS>
+static void launch_pack_bits(cudaStream_t st, const kvt_blob_map& m, char* b, const uint16_t* k, const uint16_t* v,
+                             const int32_t* idx, int S, int T, int kk) {
+  dim3 kgrid((kk + KVT_QGROUP - 1) / KVT_QGROUP, S);
+  k_pack_k<BITS><<<kgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), idx,
+                                        reinterpret_cast<uint32_t*>(b + m.kcode_off),
+                                        reinterpret_cast<uint16_t*>(b + m.kscale_off),
+                                        reinterpret_cast<uint16_t*>(b + m.kzero_off), T, kk);
+  dim3 vgrid((kk + 16 * kVRows - 1) / (16 * kVRows), S);
+  k_pack_v<BITS><<<vgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(v), idx, reinterpret_cast<int32_t*>(b + m.idx_off),
+                                        reinterpret_cast<uint32_t*>(b + m.vcode_off),
+                                        reinterpret_cast<uint16_t*>(b + m.vscale_off),
+                                        reinterpret_cast<uint16_t*>(b + m.vzero_off), T, kk);
 }
 
 static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
@@ -1148,8 +1183,8 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
   char* b = static_cast<char*>(blob);
   const int S = s->L * s->H, kk = c->keep;
   cudaStream_t st = h->stream;
-  dim3 rows_grid((kk + 15) / 16, S);
   if (c->bits == 16) {
+    dim3 rows_grid((kk + 15) / 16, S);
     k_gather16<<<rows_grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
                                           reinterpret_cast<int32_t*>(b + m.idx_off),
                                           reinterpret_cast<uint4*>(b + m.kcode_off),
@@ -1157,17 +1192,11 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
     LAUNCHED(h);
     return KVT_OK;
   }
-  dim3 kgrid((kk + KVT_QGROUP - 1) / KVT_QGROUP, S);
-  k_pack_k<<<kgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), idx, reinterpret_cast<uint32_t*>(b + m.kcode_off),
-                                  reinterpret_cast<uint16_t*>(b + m.kscale_off),
-                                  reinterpret_cast<uint16_t*>(b + m.kzero_off), s->T, kk, c->bits);
-  LAUNCHED(h);
-  dim3 vgrid((kk + 16 * kVRows - 1) / (16 * kVRows), S);
-  k_pack_v<<<vgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(v), idx, reinterpret_cast<int32_t*>(b + m.idx_off),
-                                      reinterpret_cast<uint32_t*>(b + m.vcode_off),
-                                      reinterpret_cast<uint16_t*>(b + m.vscale_off),
-                                      reinterpret_cast<uint16_t*>(b + m.vzero_off), s->T, kk, c->bits);
-  LAUNCHED(h);
+  if (c->bits == 8) launch_pack_bits<8>(st, m, b, k, v, idx, S, s->T, kk);
+  else if (c->bits == 4) launch_pack_bits<4>(st, m, b, k, v, idx, S, s->T, kk);
+  else launch_pack_bits<2>(st, m, b, k, v, idx, S, s->T, kk);
+  h->launches += 2;
+  KVT_CUDA_TRY(cudaGetLastError());
   return KVT_OK;
 }
 
@@ -1422,16 +1451,22 @@ __global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2
       }
     }
   } else {
-    const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
-    for (int g = rank; g < ng; g += kFuseC)
-      pack_k_group(K, bidx, reinterpret_cast<uint32_t*>(blob + m.kcode_off),
-                   reinterpret_cast<uint16_t*>(blob + m.kscale_off), reinterpret_cast<uint16_t*>(blob + m.kzero_off),
-                   T, k, bits, slice, g, pk);
-    // warp-uniform trip count: both half-warps of a warp run every iteration
-    for (int wb = (rank * 16 + (hw & ~1)) * kVRows; wb < k; wb += kFuseC * 16 * kVRows)
-      pack_v_rows(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
-                  reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off),
-                  T, k, bits, slice, wb + (hw & 1) * kVRows);
+    auto pack = [&](auto bits_c) {
+      constexpr int B = decltype(bits_c)::value;
+      const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
+      for (int g = rank; g < ng; g += kFuseC)
+        pack_k_group<B>(K, bidx, reinterpret_cast<uint32_t*>(blob + m.kcode_off),
+                        reinterpret_cast<uint16_t*>(blob + m.kscale_off), reinterpret_cast<uint16_t*>(blob + m.kzero_off),
+                        T, k, slice, g, pk);
+      // warp-uniform trip count: both half-warps of a warp run every iteration
+      for (int wb = (rank * 16 + (hw & ~1)) * kVRows; wb < k; wb += kFuseC * 16 * kVRows)
+        pack_v_rows<B>(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
+                       reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off),
+                       T, k, slice, wb + (hw & 1) * kVRows);
+    };
+    if (bits == 8) pack(std::integral_constant<int, 8>{});
+    else if (bits == 4) pack(std::integral_constant<int, 4>{});
+    else pack(std::integral_constant<int, 2>{});
   }
 }
 

@@ -84,6 +84,7 @@ __device__ __forceinline__ uint32_t score_key(float f) {
 struct QParam {
   float sf, zf, inv;
   uint16_t s16, z16;
+  bool fast;  // |(x - zf) * inv| <= 16000 for every x of the group: int16-lane fast path is exact
 };
 
 // asymmetric min/max group parameters stored as fp16 scale + zero
@@ -99,29 +100,67 @@ __device__ __forceinline__ QParam make_param(float mn, float mx, int bits) {
   p.sf = __half2float(hs);
   p.zf = __half2float(hz);
   p.inv = p.sf > 0.0f ? __frcp_rn(p.sf) : 0.0f;
+  // x in [mn, mx] -> |fl(x - zf)| <= b and |y| <= fl(b * inv) (monotone rounding); NaN/inf -> slow path
+  const float b = fmaxf(fabsf(__fsub_rn(mn, p.zf)), fabsf(__fsub_rn(mx, p.zf)));
+  p.fast = __fmul_rn(b, p.inv) <= 16000.0f;
   return p;
 }
 
-__device__ __forceinline__ uint32_t quant(float x, const QParam& p, int bits) {
-  float r = rintf(__fmul_rn(__fsub_rn(x, p.zf), p.inv));
-  const float hi = float((1 << bits) - 1);
-  if (!(r >= 0.0f)) r = 0.0f;
-  if (r > hi) r = hi;
-  return uint32_t(r);
+// code = clamp(rint(exact((x - zf) * inv)), 0, 2^b - 1) (oracle quant): the
+// difference is one fp32 op, the product is exact in FP64 and rounded once.
+// Valid for any input (the slow path of the fast lanes below).
+__device__ __forceinline__ uint32_t quant_exact(float x, float zf, float inv, int bits) {
+  const double r = rint(double(__fsub_rn(x, zf)) * double(inv));
+  const double hi = double((1 << bits) - 1);
+  return r >= 0.0 ? uint32_t(r > hi ? hi : r) : 0u;
 }
 
-// Two codes at once with packed fp32x2 arithmetic (FADD2/FMUL2; each lane
-// rounds exactly like the scalar ops): clamp(rint((x - z) * inv), 0, hi).
-// Clamping before rounding is equivalent because 0 and hi are integers;
-// fmaxf maps NaN to 0 like quant(). rint = add 1.5*2^23 (round-half-even).
-__device__ __forceinline__ void quant2(float x0, float x1, float z0, float z1, float i0, float i1, float hi,
-                                       uint32_t& c0, uint32_t& c1) {
-  float2 y = __fmul2_rn(__fadd2_rn(make_float2(x0, x1), make_float2(-z0, -z1)), make_float2(i0, i1));
-  y.x = fminf(fmaxf(y.x, 0.0f), hi);
-  y.y = fminf(fmaxf(y.y, 0.0f), hi);
-  const float2 r = __fadd2_rn(y, make_float2(12582912.0f, 12582912.0f));
-  c0 = __float_as_uint(r.x) - 0x4B400000u;
-  c1 = __float_as_uint(r.y) - 0x4B400000u;
+// Fast path of quant_exact for 8 channels (one 16-byte bf16 chunk, words
+// q = channel pairs (2q, 2q+1)): one packed fp32x2 subtract and one fused
+// multiply-add with 1.5 * 2^23 (= rint of the exact product, |y| < 2^22),
+// then both codes clamped as int16 lanes. Lane word q: code 2q in bits
+// 0..15, code 2q+1 in bits 16..31. Exact when QParam::fast holds.
+template <int BITS>
+__device__ __forceinline__ void quant8_fast(const uint4& v, const float2 (&nz)[4], const float2 (&iv)[4],
+                                            uint32_t (&p)[4]) {
+  constexpr uint32_t hi2 = ((1u << BITS) - 1u) * 0x00010001u;
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 d = __fadd2_rn(make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)), nz[q]);
+    const float2 r = __ffma2_rn(d, iv[q], make_float2(12582912.0f, 12582912.0f));
+    uint32_t c = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x5410);
+    c = __vmaxs2(c, 0u);
+    p[q] = __vminu2(c, hi2);
+  }
+}
+// same lane layout through quant_exact (any parameters)
+template <int BITS>
+__device__ __forceinline__ void quant8_exact(const uint4& v, const float (&z)[8], const float (&iv)[8],
+                                             uint32_t (&p)[4]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    p[q] = quant_exact(__uint_as_float(w[q] << 16), z[2 * q], iv[2 * q], BITS) |
+           (quant_exact(__uint_as_float(w[q] & 0xffff0000u), z[2 * q + 1], iv[2 * q + 1], BITS) << 16);
+}
+
+// 8 codes (lane words) -> the blob's bit packing of those 8 channels:
+// BITS 8: two words (byte e = channel e); 4: one word (nibble e); 2: the
+// low 16 bits (2-bit field e).
+template <int BITS>
+__device__ __forceinline__ uint2 pack8(const uint32_t (&p)[4]) {
+  if (BITS == 8) return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
+  if (BITS == 4) {
+    uint32_t t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = p[q] | (p[q] >> 12);  // byte 0 = code 2q | code 2q+1 << 4
+    return make_uint2(__byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410), 0u);
+  }
+  uint32_t t[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) t[q] = p[q] | (p[q] >> 14);  // bits 0..3 = code 2q | code 2q+1 << 2
+  return make_uint2((t[0] | (t[1] << 4) | (t[2] << 8) | (t[3] << 12)) & 0xffffu, 0u);
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }

@@ -206,3 +206,67 @@ def topk_indices(scores, k):
         order = np.lexsort((np.arange(len(row)), -row.astype(np.float64)))
         out.append(np.sort(order[:k]))
     return np.array(out, np.int32).reshape(scores.shape[:-1] + (k,))
+
+
+def _params(mn, mx, bits):
+    """make_param: fp16 scale (max-min)/levels and zero = min."""
+    mn = (mn.astype(np.float32) + np.float32(0)).astype(np.float32)  # -0 -> +0
+    mx = (mx.astype(np.float32) + np.float32(0)).astype(np.float32)
+    levels = np.float32((1 << bits) - 1)
+    with np.errstate(over="ignore", invalid="ignore"):
+        scale = ((mx - mn) / levels).astype(np.float32)
+        s16 = scale.astype(np.float16)
+        z16 = mn.astype(np.float16)
+        sf = s16.astype(np.float32)
+        inv = np.where(sf > 0, (np.float32(1) / np.where(sf > 0, sf, 1)).astype(np.float32), np.float32(0))
+    return s16, z16, z16.astype(np.float32), inv.astype(np.float32)
+
+
+def _codes(x, zf, inv, bits):
+    """clamp(rint(exact((x - zf) * inv)), 0, 2^b - 1); NaN -> 0."""
+    with np.errstate(over="ignore", invalid="ignore"):
+        d = (x.astype(np.float32) - zf).astype(np.float32)
+        r = np.rint(d.astype(np.float64) * inv.astype(np.float64))
+        r = np.where(r >= 0, np.minimum(r, (1 << bits) - 1), 0)
+    return r.astype(np.uint32)
+
+
+def _pack_words(codes, bits):
+    """codes [..., 128] -> u32 words, code of channel d at bit b * (d % (32 / b))."""
+    per = 32 // bits
+    c = codes.reshape(codes.shape[:-1] + (128 // per, per)).astype(np.uint64)
+    sh = (np.arange(per, dtype=np.uint64) * np.uint64(bits))
+    return (c << sh).sum(-1).astype(np.uint32)
+
+
+def pack_blob(k, v, idx, bits, m):
+    """Exact numpy restatement of pack (K per channel over groups of 128 kept
+    tokens, V per kept token), returned as the blob byte array for layout m."""
+    L, H, T, D = k.shape
+    keep = idx.shape[-1]
+    blob = np.zeros(m.total_bytes, np.uint8)
+    blob[m.idx_off:m.idx_off + m.idx_bytes] = idx.astype(np.int32).reshape(-1).view(np.uint8)
+    kx = np.take_along_axis(bf2f(k), idx[..., None].astype(np.int64), axis=2)  # [L,H,keep,D]
+    vx = np.take_along_axis(bf2f(v), idx[..., None].astype(np.int64), axis=2)
+    if bits == 16:
+        blob[m.kcode_off:m.kcode_off + m.kcode_bytes] = np.take_along_axis(
+            k, idx[..., None].astype(np.int64), axis=2).reshape(-1).view(np.uint8)
+        blob[m.vcode_off:m.vcode_off + m.vcode_bytes] = np.take_along_axis(
+            v, idx[..., None].astype(np.int64), axis=2).reshape(-1).view(np.uint8)
+        return blob
+    ng = (keep + 127) // 128
+    kc = np.zeros((L, H, keep, 128 * bits // 32), np.uint32)
+    ks = np.zeros((L, H, ng, D), np.float16)
+    kz = np.zeros((L, H, ng, D), np.float16)
+    for g in range(ng):
+        seg = kx[:, :, g * 128:(g + 1) * 128]
+        s16, z16, zf, inv = _params(seg.min(2), seg.max(2), bits)
+        ks[:, :, g], kz[:, :, g] = s16, z16
+        kc[:, :, g * 128:(g + 1) * 128] = _pack_words(_codes(seg, zf[:, :, None], inv[:, :, None], bits), bits)
+    vs16, vz16, vzf, vinv = _params(vx.min(3), vx.max(3), bits)
+    vc = _pack_words(_codes(vx, vzf[..., None], vinv[..., None], bits), bits)
+    for off, arr in ((m.kcode_off, kc), (m.kscale_off, ks), (m.kzero_off, kz), (m.vcode_off, vc),
+                     (m.vscale_off, vs16), (m.vzero_off, vz16)):
+        b = arr.reshape(-1).view(np.uint8)
+        blob[off:off + b.size] = b
+    return blob

@@ -155,6 +155,43 @@ def test_topk_rule_ties_and_order(lib):
     assert np.array_equal(idx, R.topk_indices(sc, cfg.keep))
 
 
+def _extreme_kv(L, H, T, seed=5):
+    """KV with outliers that defeat the fast quantisation path: huge rows,
+    fp16-overflowing groups, tiny ranges far from zero, exact zeros."""
+    k, v = _kv(L, H, T, seed=seed)
+    rng = np.random.default_rng(seed)
+    x = R.bf2f(k).copy()
+    y = R.bf2f(v).copy()
+    x[:, :, ::7] *= np.float32(3e5)            # whole rows beyond fp16 range
+    y[:, :, 1::5] = np.float32(1000.0) + y[:, :, 1::5] * np.float32(1e-3)  # tiny range, large offset
+    y[:, :, 2::9] = 0.0
+    x[:, :, :, 5] = -x[:, :, :, 5] * np.float32(7e4)
+    rr = rng.integers(0, T, size=3)
+    x[:, :, rr] = np.float32(-0.0)
+    to_bf = lambda a: (a.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)  # truncation is fine: any bf16
+    return to_bf(x), to_bf(y)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+@pytest.mark.parametrize("extreme", [False, True])
+def test_pack_matches_numpy_exactly(lib, bits, extreme):
+    """The oracle's pack (codes, fp16 params, index copy) == the numpy
+    restatement, byte for byte, including groups that need the exact path."""
+    s = shape(2, 2, 300)
+    k, v = _extreme_kv(2, 2, 300) if extreme else _kv(2, 2, 300)
+    cfg = plan(lib, f"knorm-q{bits}" if bits < 16 else "knorm", 0.3 if bits < 16 else 0.5, s)
+    cfg.bits = bits
+    m = A.BlobMap()
+    lib.check(lib.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    rng = np.random.default_rng(bits)
+    idx = np.sort(np.stack([np.stack([rng.choice(300, cfg.keep, replace=False) for _ in range(2)]) for _ in range(2)]),
+                  axis=-1).astype(np.int32)
+    blob = np.zeros(m.total_bytes, np.uint8)
+    lib.check(lib.pack(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(blob)))
+    want = R.pack_blob(k.reshape(2, 2, 300, 128), v.reshape(2, 2, 300, 128), idx, bits, m)
+    assert np.array_equal(blob, want)
+
+
 @pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.25), ("keydiff-q4", 0.2), ("knorm-q2", 0.1),
                                           ("snapkv", 0.3), ("knorm-q4", 0.05)])
 def test_pack_unpack_roundtrip(lib, method, ratio):

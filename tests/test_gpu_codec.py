@@ -231,3 +231,29 @@ def test_full_llama_chunk_knorm_q4_properties(gpu, orc):
         seg = kk[:, g0:g0 + 128]
         kstep = (seg.amax(1, keepdim=True) - seg.amin(1, keepdim=True)) / 15
         assert bool(((kd[:, g0:g0 + 128] - seg).abs() <= 0.51 * kstep * 1.002 + seg.abs() * 2 ** -7 + 1e-3).all())
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8, 16])
+def test_pack_extreme_values_bitexact(gpu, orc, bits):
+    """Outlier KV (rows beyond fp16 range, tiny ranges far from zero, zeros,
+    -0): groups whose parameters do not bound the codes take the exact FP64
+    path; the blob still equals the oracle's byte for byte."""
+    from test_codec_oracle import _extreme_kv
+    s = A.KvShape(2, 2, 300, 128)
+    k, v = _extreme_kv(2, 2, 300)
+    cfg = plan(orc.abi, f"knorm-q{bits}" if bits < 16 else "knorm", 0.3 if bits < 16 else 0.5, s)
+    cfg.bits = bits
+    m = A.BlobMap()
+    orc.abi.check(orc.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    rng = np.random.default_rng(bits)
+    idx = np.sort(np.stack([np.stack([rng.choice(300, cfg.keep, replace=False) for _ in range(2)]) for _ in range(2)]),
+                  axis=-1).astype(np.int32)
+    bo = np.zeros(m.total_bytes, np.uint8)
+    orc.abi.check(orc.abi.pack(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(bo)))
+    bg = torch.zeros(m.total_bytes, dtype=torch.uint8, device="cuda")
+    kd, vd, idd = dev(k.view(np.int16)), dev(v.view(np.int16)), dev(idx)
+    gpu.abi.check(gpu.abi.pack(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kd), A.ptr(vd), A.ptr(idd), A.ptr(bg)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    sg, so = blob_sections(bg.cpu().numpy(), m, bits), blob_sections(bo, m, bits)
+    for name in so:
+        assert np.array_equal(sg[name], so[name]), name
