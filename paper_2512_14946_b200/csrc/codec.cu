@@ -320,6 +320,73 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
   }
 }
 
+// keydiff in one launch: one 8-CTA cluster per (layer, kv-head) slice, each
+// CTA streams its T/8 tokens through the bulk-copy ring twice. Pass 1 (HBM)
+// sums the fixed-point unit keys and keeps 1/|k| per token in smem; the
+// slice's sum is combined over the cluster through DSMEM; pass 2 re-reads
+// the same rows (~18 slices x 2 MiB in flight: L2 hits) for the dot
+// products. Bit-identical to k_keydiff_sum + k_keydiff_score.
+constexpr int kKdC = 8;
+__global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
+    k_keydiff_cluster(const uint4* __restrict__ K, float* __restrict__ out, int T) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int slice = blockIdx.y, tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
+  const int per = (T + kKdC - 1) / kKdC;
+  const int t_lo = min(T, rank * per), n_loc = min(T, t_lo + per) - t_lo;
+  extern __shared__ __align__(16) uint8_t kd_raw[];
+  uint4* ring = reinterpret_cast<uint4*>(kd_raw);
+  float* kinv = reinterpret_cast<float*>(kd_raw + kRingBytes);
+  __shared__ long long part[16][kD];
+  __shared__ long long sfix[kD];
+  __shared__ float sdir[kD];
+  __shared__ __align__(8) uint64_t full[kRingStages];
+  if (tid == 0) {
+    for (int i = 0; i < kRingStages; ++i) mbar_init(&full[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+  uint32_t seq = 0;
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t cnt = 0;  // <= per / 16 tokens per lane: the biased u32 sums cannot wrap for T < 2^16
+  stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
+    const float inv = kd_inv(half_butterfly(chunk_sumsq(v)));
+    if (live) {
+      kd_fix_add(v, __fmul_rn(inv, kKdFx), acc);
+      ++cnt;
+      if (l16 == 0) kinv[t] = inv;
+    }
+  });
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = static_cast<int32_t>(acc[i] - cnt * 0x4B400000u);
+  __syncthreads();
+  if (tid < kD) {
+    long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sum += part[i][tid];
+    sfix[tid] = sum;
+  }
+  cluster_sync_smem();
+  if (tid < kD) {
+    long long sum = 0;
+    for (int c = 0; c < kKdC; ++c) sum += cl.map_shared_rank(sfix, c)[tid];
+    sdir[tid] = __fmul_rn(__ll2float_rn(sum), 1.0f / kKdFx);
+  }
+  __syncthreads();
+  float2 sd[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sd[q] = make_float2(sdir[l16 * 8 + 2 * q], sdir[l16 * 8 + 2 * q + 1]);
+  float* o = out + static_cast<size_t>(slice) * T + t_lo;
+  stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
+    const float p = half_butterfly(chunk_dot(v, sd));
+    if (live && l16 == 0) o[t] = -__fmul_rn(p, kinv[t]);
+  });
+  cluster_sync_smem();  // no CTA exits while a peer may still read its sfix
+}
+
+static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKdC - 1) / kKdC)); }
+
 // snapkv on the integer tensor cores, exact-integer spec v2
 // of DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): window queries
 // quantised to int8 per row, prefix keys to int8 per 128-token tile, so every
@@ -339,25 +406,37 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
 // and epilogue of the current one.
 constexpr int kSnapTPC = 4;            // tiles per CTA
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
-constexpr int kSnapThreads = 512;      // 16 warps
-constexpr int kSnapEStride = 1040;     // bytes per E row: 512 tokens x u16 + 16 B pad (conflict-free STS.128)
+constexpr int kSnapProd = 8;           // producer warps: K tile absmax + int8 quantisation + MMA issue
+constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
+constexpr int kSnapThreads = (kSnapProd + kSnapCons) * 32;
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
 constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
 
+// E is [row][512 tokens] u16, 1 KiB per row, 16-byte chunk c of row r stored
+// at chunk c ^ (r & 7): conflict-free row-wise STS.128 and token-wise LDS.32.
 struct SnapSmem {
-  uint8_t k8[128 * 128];  // offset 0 of the 1024-aligned base
+  uint8_t k8[2][128 * 128];  // offset 0 of the 1024-aligned base; double-buffered
   uint8_t q8[128 * 128];
-  uint4 stage[128 * 16];  // one bf16 tile (32 KB); reused for the votes
-  uint8_t e[128 * kSnapEStride];
+  uint4 stage[128 * 16];     // one bf16 tile (32 KB); after the tile loop: combine scratch + votes
+  uint8_t e[128 * 1024];
   int32_t mb[kSnapTPC * 4][128];   // per (block, row) shift M
   uint32_t lb[kSnapTPC * 4][128];  // per (block, row) sum of E, then the block weight
   float sig[128];
-  uint32_t amax[16];
-  int32_t mloc[128], mrow[128];
-  unsigned long long lloc[128];
-  uint64_t full, qbar, mma_bar;
+  float tau[kSnapTPC];
+  uint32_t amax[kSnapProd];
+  uint64_t full, qbar, tfull[2], tempty[2];
   uint32_t tmem_base;
 };
+struct SnapScratch {  // aliases SnapSmem::stage after the tile loop
+  unsigned long long vote[512];
+  unsigned long long lloc[128];
+  int32_t mloc[128], mrow[128];
+};
+static_assert(sizeof(SnapScratch) <= 128 * 16 * sizeof(uint4), "scratch fits the stage");
+
+__device__ __forceinline__ uint32_t snap_e_off(int r, int byte) {  // swizzled byte offset of E[r][byte / 2]
+  return static_cast<uint32_t>(r) * 1024u + ((((byte >> 4) ^ r) & 7) | ((byte >> 4) & ~7)) * 16u + (byte & 15);
+}
 
 // 2^15 * 2^f on [-1/2, 1/2], degree 4 (oracle SNAP_E*)
 constexpr float kE0 = 32767.927734375f, kE1 = 22712.50390625f, kE2 = 7874.56103515625f,
@@ -465,6 +544,11 @@ __global__ void __launch_bounds__(256) k_snap_q(uint8_t* __restrict__ qbuf, int 
   if (tid < 128) reinterpret_cast<float*>(dst + 1024)[tid] = sig[tid];
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
 __global__ void __launch_bounds__(kSnapThreads, 1)
     k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, float* __restrict__ scores, int T,
                 int W, int G, int pool, int tpc) {
@@ -485,10 +569,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   if (tid == 0) {
     mbar_init(&sm.full, 1);
     mbar_init(&sm.qbar, 1);
-    mbar_init(&sm.mma_bar, 1);
+    mbar_init(&sm.tfull[0], 2);  // tcgen05.commit + the issuing producer thread (orders sm.tau)
+    mbar_init(&sm.tfull[1], 2);
+    mbar_init(&sm.tempty[0], kSnapCons);
+    mbar_init(&sm.tempty[1], kSnapCons);
     mbar_fence_init();
   }
-  if (warp == 0) tmem_alloc(&sm.tmem_base, 128);
+  if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -505,111 +592,137 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   }
   mbar_wait(&sm.qbar, 0);
 
-  constexpr uint32_t kIdesc = idesc_i8(128, 128);
-  const int quad = warp & 3, cb = warp >> 2;  // TMEM lanes 32*quad.., 32-token block cb of the tile
-  const int r = quad * 32 + lane;             // epilogue: this thread's query row
-  const float sig_r = sm.sig[r];
-  for (int j = 0; j < ntl; ++j) {
-    const int rows = min(128, n_loc - j * 128);
-    mbar_wait(&sm.full, j & 1);
-    // ---- per-tile absmax (|bf16| bit patterns order like the values)
-    const int qr = tid >> 2, qq = tid & 3;  // row, 32-channel quarter
-    uint4 v[4];
+  if (warp < kSnapProd) {
+    // ================= producers: absmax, int8 quantisation, MMA issue
+    constexpr uint32_t kIdesc = idesc_i8(128, 128);
+    constexpr int kRowsPT = 128 * 4 / (kSnapProd * 32);  // rows per producer thread
+    const int ptid = tid;  // rows ptid/4 + (kSnapProd * 8) * i, 32-channel quarter ptid & 3
+    const int q4 = ptid & 3, rbase = ptid >> 2;
+    for (int j = 0; j < ntl; ++j) {
+      const int buf = j & 1;
+      const int rows = min(128, n_loc - j * 128);
+      mbar_wait(&sm.full, j & 1);
+      uint4 v[kRowsPT][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = qr < rows ? sm.stage[qr * 16 + qq * 4 + i] : make_uint4(0, 0, 0, 0);
-    uint32_t mx2 = 0;
+      for (int i = 0; i < kRowsPT; ++i) {
+        const int row = rbase + kSnapProd * 8 * i;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      mx2 = __vmaxu2(mx2, v[i].x & 0x7fff7fffu);
-      mx2 = __vmaxu2(mx2, v[i].y & 0x7fff7fffu);
-      mx2 = __vmaxu2(mx2, v[i].z & 0x7fff7fffu);
-      mx2 = __vmaxu2(mx2, v[i].w & 0x7fff7fffu);
-    }
-    uint32_t mx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
-    if (lane == 0) sm.amax[warp] = mx;
-    __syncthreads();
-    if (tid == 0 && j + 1 < ntl) {  // every thread holds its slice of the tile: prefetch the next one now
-      const int nrows = min(128, n_loc - (j + 1) * 128);
-      fence_async_smem();
-      mbar_expect_tx(&sm.full, nrows * 256);
-      bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
-    }
-    mx = 0;
+        for (int u = 0; u < 4; ++u) v[i][u] = row < rows ? sm.stage[row * 16 + q4 * 4 + u] : make_uint4(0, 0, 0, 0);
+      }
+      uint32_t mx2 = 0;
 #pragma unroll
-    for (int w = 0; w < 16; ++w) mx = max(mx, sm.amax[w]);
-    const float A = bf2f(mx);
-    const float inv = A > 0.0f ? __fdiv_rn(127.0f, A) : 0.0f;
-    const float tau = A > 0.0f ? __fdiv_rn(A, 127.0f) : 0.0f;
-    // ---- quantise this thread's 32 values (|x * inv| < 127.5: no clamp needed)
-    uint32_t wq[8];
+      for (int i = 0; i < kRowsPT; ++i)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t ww[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+        for (int u = 0; u < 4; ++u) {
+          mx2 = __vmaxu2(mx2, v[i][u].x & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i][u].y & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i][u].z & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i][u].w & 0x7fff7fffu);
+        }
+      const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
+      if (lane == 0) sm.amax[warp] = wmx;
+      named_bar_sync(1, kSnapProd * 32);  // stage consumed into registers, amax complete
+      if (ptid == 0 && j + 1 < ntl) {  // prefetch the next tile
+        const int nrows = min(128, n_loc - (j + 1) * 128);
+        fence_async_smem();
+        mbar_expect_tx(&sm.full, nrows * 256);
+        bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+      }
+      uint32_t mx = 0;
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        // rint of the exact product x * inv (fused rounding, oracle quant_i8)
-        const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
-                                     make_float2(12582912.0f, 12582912.0f));
-        const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])), make_float2(inv, inv),
-                                     make_float2(12582912.0f, 12582912.0f));
-        const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
-        const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
-        wq[2 * i + h2] = __byte_perm(lo, hi, 0x5410);
+      for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
+      const float Af = bf2f(mx);
+      const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
+      if (ptid == 0) sm.tau[j] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;
+      if (j >= 2) mbar_wait(&sm.tfull[buf], ((j >> 1) - 1) & 1);  // MMA of tile j - 2 done reading k8[buf]
+      uint8_t* k8 = sm.k8[buf];
+#pragma unroll
+      for (int i = 0; i < kRowsPT; ++i) {
+        const int row = rbase + kSnapProd * 8 * i;
+        uint32_t wq[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t ww[4] = {v[i][u].x, v[i][u].y, v[i][u].z, v[i][u].w};
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            // rint of the exact product x * inv (fused rounding, oracle quant_i8)
+            const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
+                                         make_float2(12582912.0f, 12582912.0f));
+            const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])),
+                                         make_float2(inv, inv), make_float2(12582912.0f, 12582912.0f));
+            const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
+            const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
+            wq[2 * u + h2] = __byte_perm(lo, hi, 0x5410);
+          }
+        }
+        const int c0 = q4 * 2;  // 16-byte chunks c0, c0 + 1 of the row (SW128 K-major)
+        *reinterpret_cast<uint4*>(k8 + row * 128 + ((c0 ^ (row & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+        *reinterpret_cast<uint4*>(k8 + row * 128 + (((c0 + 1) ^ (row & 7)) << 4)) =
+            make_uint4(wq[4], wq[5], wq[6], wq[7]);
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      named_bar_sync(1, kSnapProd * 32);
+      if (ptid == 0) {
+        if (j >= 2) mbar_wait(&sm.tempty[buf], ((j >> 1) - 1) & 1);  // consumers drained acc[buf]
+        tc_fence_after();
+        mbar_arrive(&sm.tfull[buf]);  // release: sm.tau[j] visible to the consumers
+        const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
+        umma_commit(&sm.tfull[buf]);
       }
     }
-    {
-      const int c0 = qq * 2;  // 16-byte chunks c0, c0 + 1 of row qr
-      *reinterpret_cast<uint4*>(sm.k8 + qr * 128 + ((c0 ^ (qr & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
-      *reinterpret_cast<uint4*>(sm.k8 + qr * 128 + (((c0 + 1) ^ (qr & 7)) << 4)) =
-          make_uint4(wq[4], wq[5], wq[6], wq[7]);
-    }
-    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core / bulk copy engine
-    __syncthreads();
-    if (tid == 0) {
+  } else {
+    // ================= consumers: row r, tokens 128j + 32cb .. +31
+    const int cw = warp - kSnapProd;
+    const int quad = cw & 3, cb = cw >> 2;  // TMEM lane quadrant (warp % 4 == cw % 4), 32-token block
+    const int r = quad * 32 + lane;
+    const float sig_r = sm.sig[r];
+    for (int j = 0; j < ntl; ++j) {
+      const int buf = j & 1;
+      mbar_wait(&sm.tfull[buf], (j >> 1) & 1);
       tc_fence_after();
-      const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(sm.k8);
+      uint32_t I[32];
+      tmem_ld32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + cb * 32, I);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile j + 2 may overwrite it
+      const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
+      int32_t M = INT_MIN;
+      uint32_t L = 0;
+      uint32_t pk[16];
+      if (r < R && nv > 0) {
+        const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(sm.tau[j], sig_r), kSnapC0)) & ~3u);
+        L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
+      } else {
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) umma_i8(tmem, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
-      umma_commit(&sm.mma_bar);
+        for (int i = 0; i < 16; ++i) pk[i] = 0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
+            make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      sm.mb[j * 4 + cb][r] = M;
+      sm.lb[j * 4 + cb][r] = L;
     }
-    mbar_wait(&sm.mma_bar, j & 1);
-    tc_fence_after();
-    // ---- epilogue: row r, tokens 128j + 32cb .. +31 of this CTA
-    uint32_t I[32];
-    tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + cb * 32, I);
-    const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
-    int32_t M = INT_MIN;
-    uint32_t L = 0;
-    uint32_t pk[16];
-    if (r < R && nv > 0) {
-      const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
-      L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) pk[i] = 0;
-    }
-    uint4* erow = reinterpret_cast<uint4*>(sm.e + r * kSnapEStride + tok0 * 2);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) erow[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-    sm.mb[j * 4 + cb][r] = M;
-    sm.lb[j * 4 + cb][r] = L;
-    tc_fence_before();
-    __syncthreads();  // TMEM accumulator and K8 free for the next tile
   }
+  __syncthreads();  // all tiles done; stage is free
 
+  SnapScratch& xs = *reinterpret_cast<SnapScratch*>(sm.stage);
   // ---- row shift and sum across the cluster (4 threads per row, blocks split 4 ways)
-  const int crow = tid >> 2, cq = tid & 3;
-  {
+  const int crow = (tid >> 2) & 127, cq = tid & 3;
+  const bool cworker = tid < 512;
+  if (cworker) {
     int32_t m = INT_MIN;
     for (int b = cq; b < nblk; b += 4) m = max(m, sm.mb[b][crow]);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-    if (cq == 0) sm.mloc[crow] = m;
+    if (cq == 0) xs.mloc[crow] = m;
   }
   cluster_sync_smem();
-  {
+  if (cworker) {
     int32_t m = INT_MIN;
-    for (int c = cq; c < C; c += 4) m = max(m, cl.map_shared_rank(sm.mloc, c)[crow]);
+    for (int c = cq; c < C; c += 4) m = max(m, cl.map_shared_rank(xs.mloc, c)[crow]);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
     unsigned long long Ls = 0;
@@ -620,55 +733,53 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
     if (cq == 0) {
-      sm.mrow[crow] = m;
-      sm.lloc[crow] = Ls;
+      xs.mrow[crow] = m;
+      xs.lloc[crow] = Ls;
     }
   }
   cluster_sync_smem();
-  {
+  if (cworker) {
     unsigned long long Ls = 0;
-    for (int c = cq; c < C; c += 4) Ls += cl.map_shared_rank(sm.lloc, c)[crow];
+    for (int c = cq; c < C; c += 4) Ls += cl.map_shared_rank(xs.lloc, c)[crow];
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
     const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
-    const int32_t m = sm.mrow[crow];
+    const int32_t m = xs.mrow[crow];
     for (int b = cq; b < nblk; b += 4) {
       const int64_t sh = int64_t(m) - sm.mb[b][crow];
       sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
     }
   }
-  __syncthreads();
-  // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows; rows
-  // >= R have zero weight, so every loop runs the full (padded) row range
-  unsigned long long* vote = reinterpret_cast<unsigned long long*>(sm.stage);
+  // every peer has read this CTA's mloc / lloc before the votes overwrite them
+  cluster_sync_smem();
+  // ---- votes: thread = token pair (2p, 2p + 1) x a quarter... of the rows; rows >= R have zero weight
   {
-    const int p = tid & 255, rh = tid >> 8, b = p >> 4;
-    const uint32_t* erow = reinterpret_cast<const uint32_t*>(sm.e + rh * 64 * kSnapEStride) + p;
-    const uint32_t* wb = sm.lb[b] + rh * 64;
+    const int p = tid % 256, rq = tid / 256;  // 640 threads: rq 0, 1 take 64 rows each, rq 2 idles
     unsigned long long a0 = 0, a1 = 0;
-    if (2 * p < n_loc) {
+    if (rq < 2 && 2 * p < n_loc) {
+      const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
 #pragma unroll 4
       for (int r0 = 0; r0 < 64; r0 += 4) {
         const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
         const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint32_t e2 = erow[(r0 + q) * (kSnapEStride / 4)];
+          const int r = rq * 64 + r0 + q;
+          const uint32_t e2 = *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(r, 4 * p));
           a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
           a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
         }
       }
     }
-    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm.e);  // E fully consumed below
-    __syncthreads();
-    if (rh == 1) {
+    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm.k8);  // K8 no longer needed
+    if (rq == 1) {
       part[2 * p] = a0;
       part[2 * p + 1] = a1;
     }
     __syncthreads();
-    if (rh == 0) {
-      vote[2 * p] = a0 + part[2 * p];
-      vote[2 * p + 1] = a1 + part[2 * p + 1];
+    if (rq == 0) {
+      xs.vote[2 * p] = a0 + part[2 * p];
+      xs.vote[2 * p + 1] = a1 + part[2 * p + 1];
     }
   }
   cluster_sync_smem();  // every CTA's votes visible
@@ -680,10 +791,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     for (int dj = -half; dj <= half; ++dj) {
       const int tg = t_lo + tl + dj;  // global prefix token
       if (tg < 0 || tg >= P) continue;
-      const int owner = (tg / 128) / tpc;
-      const int tr = tg - owner * tpc * 128;
-      const unsigned long long* vv =
-          owner == rank ? vote : cl.map_shared_rank(reinterpret_cast<unsigned long long*>(sm.stage), owner);
+      const int span = tpc * 128;  // tokens per CTA; |dj| <= pool / 2 < span: neighbours live in rank +- 1
+      const int owner = tg < t_lo ? rank - 1 : (tg >= t_lo + span ? rank + 1 : rank);
+      const int tr = tg - owner * span;
+      const unsigned long long* vv = owner == rank ? xs.vote : cl.map_shared_rank(xs.vote, owner);
       const unsigned long long x = vv[tr];
       m = x > m ? x : m;
     }
@@ -692,7 +803,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   if (rank == C - 1)
     for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
   cluster_sync_smem();  // no CTA leaves while its votes may still be read
-  if (warp == 0) tmem_dealloc(tmem, 128);
+  if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
 __global__ void k_fill_inf(float* __restrict__ out, long long n) {
@@ -755,6 +866,14 @@ static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     const long long want = (ntok * 16 + 255) / 256;
     const int blocks = static_cast<int>(std::min<long long>(want, num_sms() * 16LL));
     k_knorm<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), scores, ntok);
+    LAUNCHED(h);
+  } else if (c->scorer == KVT_SCORER_KEYDIFF && kd_cluster_smem(T) <= 100 * 1024 && T <= kKdC * 16000) {
+    static bool attr = false;
+    if (!attr) {
+      KVT_CUDA_TRY(cudaFuncSetAttribute(k_keydiff_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      attr = true;
+    }
+    k_keydiff_cluster<<<dim3(kKdC, S), 256, kd_cluster_smem(T), st>>>(reinterpret_cast<const uint4*>(k), scores, T);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_KEYDIFF) {
     KVT_CUDA_TRY(cudaMemsetAsync(fixed, 0, 8LL * S * kD, st));
