@@ -157,7 +157,10 @@ def run_b200(args):
     eng = Engine(pkg.product(), device=local, stream=stream.cuda_stream)
     max_T = int(arrays.orig.max() // bpt)
     pool = KVPool(eng, L, H, max_T, D, n_chunks=args.pool)
-    codec = Codec(eng, L, H, D)
+    # codec lanes: contexts round-robin over `--streams` CUDA streams (one kvt handle each)
+    lane_streams = [torch.cuda.Stream() for _ in range(args.streams)]
+    lanes = [Engine(pkg.product(), device=local, stream=ls.cuda_stream) for ls in lane_streams]
+    codec = Codec(lanes, L, H, D)
     codec.reserve(max_T, n_out=2)
     ps = eng.pset(arrays)
     store = eng.store(tiers, arrays.n, space)
@@ -167,11 +170,20 @@ def run_b200(args):
         n = n_local
         orig = arrays.orig[my_lo:my_hi]
 
+    def fork():  # codec lanes start after everything queued on the main stream
+        for ls in lane_streams:
+            ls.wait_stream(stream)
+
+    def join():  # the main stream (timing events) waits for every lane
+        for ls in lane_streams:
+            stream.wait_stream(ls)
+
     def step():
         acts = place(store, ps, space, params, order)
         snap_full = store.snapshot()
         names = space.method_names
         in_b = out_b = 0
+        fork()
         for c in range(my_lo, my_hi):
             if snap_full["tier_index"][c] < 0:
                 continue
@@ -179,6 +191,7 @@ def run_b200(args):
             k, v = pool.chunk(c)
             out_b += codec.compress(names[snap_full["method"][c]], float(snap_full["ratio"][c]), k, v, T, c)
             in_b += int(arrays.orig[c])
+        join()
         return len(acts), in_b, out_b
 
     def barrier():
@@ -190,7 +203,7 @@ def run_b200(args):
     for _ in range(args.warmup):
         step()
     barrier()
-    l0 = eng.abi.launch_count(eng.h)
+    l0 = eng.abi.launch_count(eng.h) + codec.launches()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -201,7 +214,7 @@ def run_b200(args):
             n_act, in_b, out_b = step()
         t1.record(stream)
         barrier()
-    launches = eng.abi.launch_count(eng.h) - l0
+    launches = eng.abi.launch_count(eng.h) + codec.launches() - l0
     ms = t0.elapsed_time(t1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -224,10 +237,12 @@ def run_b200(args):
         acts = place(store, ps_e, space, params, order)  # actions D2H
         snap_full = store.snapshot()  # placement D2H
         names = space.method_names
+        fork()
         for c in range(my_lo, my_hi):
             T = int(arrays.orig[c] // bpt)
             k, v = pool.chunk(c)
             codec.compress(names[snap_full["method"][c]], float(snap_full["ratio"][c]), k, v, T, c)
+        join()
         d2h = acts.nbytes + snap_full.nbytes
         del ps_e
     e1.record(stream)
@@ -431,6 +446,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--n-ctx", type=int, default=None)
     ap.add_argument("--pool", type=int, default=8, help="distinct resident KV chunks")
+    ap.add_argument("--streams", type=int, default=2, help="codec CUDA streams (contexts round-robin)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

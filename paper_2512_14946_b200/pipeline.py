@@ -38,13 +38,21 @@ class KVPool:
 
 
 class Codec:
-    """Plans and launches compress for (method, ratio, T) configurations."""
+    """Plans and launches compress for (method, ratio, T) configurations.
 
-    def __init__(self, eng: Engine, L: int, H: int, D: int = 128):
-        self.eng, self.L, self.H, self.D = eng, L, H, D
+    With several engines (`lanes`, each a kvt handle on its own CUDA stream
+    with its own workspace and output ring), consecutive contexts go to
+    different streams so one context's kernels fill the SMs another leaves
+    idle (e.g. snapkv's 16-CTA clusters occupy 112 of 148 SMs)."""
+
+    def __init__(self, eng, L: int, H: int, D: int = 128):
+        self.lanes = list(eng) if isinstance(eng, (list, tuple)) else [eng]
+        self.eng, self.L, self.H, self.D = self.lanes[0], L, H, D
         self._plans: Dict[Tuple[str, float, int], Tuple[A.CodecCfg, A.BlobMap, int]] = {}
         self.ws = None
         self.out: List[torch.Tensor] = []
+        self._ws: List[torch.Tensor] = []
+        self._out: List[List[torch.Tensor]] = []
 
     def plan(self, method: str, ratio: float, T: int):
         key = (method, ratio, T)
@@ -61,22 +69,29 @@ class Codec:
         return p
 
     def reserve(self, max_T: int, n_out: int = 2):
-        """Workspace + output ring for chunks up to max_T tokens."""
+        """Workspace + output ring (per lane) for chunks up to max_T tokens."""
         s = A.KvShape(self.L, self.H, max_T, self.D)
         cfg = A.CodecCfg(0, 16, max_T, 32, 4, 7, 0)
         wsb = self.eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg))
         m = A.BlobMap()
         self.eng.abi.check(self.eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
-        self.ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-        self.out = [torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda") for _ in range(n_out)]
+        self._ws = [torch.empty(wsb, dtype=torch.uint8, device="cuda") for _ in self.lanes]
+        self._out = [[torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda") for _ in range(n_out)]
+                     for _ in self.lanes]
+        self.ws, self.out = self._ws[0], self._out[0]
 
     def compress(self, method: str, ratio: float, k, v, T: int, slot: int) -> int:
         cfg, m, _ = self.plan(method, ratio, T)
         s = A.KvShape(self.L, self.H, T, self.D)
-        out = self.out[slot % len(self.out)]
-        self.eng.abi.check(self.eng.abi.compress(self.eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v),
-                                                 A.ptr(self.ws), A.ptr(out)))
+        li = slot % len(self.lanes)
+        eng, outs = self.lanes[li], self._out[li]
+        out = outs[(slot // len(self.lanes)) % len(outs)]
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(self._ws[li]),
+                                       A.ptr(out)))
         return m.total_bytes
+
+    def launches(self) -> int:
+        return sum(int(e.abi.launch_count(e.h)) for e in self.lanes)
 
 
 def place(store: StoreState, ps: PSet, space: CandidateSpace, params: UtilityParams, order) -> np.ndarray:
