@@ -116,7 +116,7 @@ def run_b200(args):
 
     import paper_2512_14946_b200 as pkg
     from paper_2512_14946_b200 import _abi as A
-    from paper_2512_14946_b200 import workload
+    from paper_2512_14946_b200 import distributed, workload
     from paper_2512_14946_b200.kvtier import Engine, ProfileArrays
     from paper_2512_14946_b200.pipeline import Codec, KVPool, compress_placed, place
 
@@ -133,25 +133,11 @@ def run_b200(args):
     bpt = W["bytes_per_token"]
     n_local = mine.n
 
-    # global profile set: all-gather every rank's profile rows (NCCL)
-    if world > 1:
-        def gather(a):
-            t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
-            out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device="cuda")
-            dist.all_gather_into_tensor(out, t)
-            return out.cpu().numpy().reshape((-1,) + tuple(a.shape[1:]))
-        G = len(mine.grid) // mine.n
-        orig = gather(mine.orig)
-        freq = gather(mine.freq)
-        qual = gather(mine.qual.reshape(mine.n, -1)).reshape(-1)
-        has = gather(mine.has)
-        ids = [f"r{r:03d}-{i:07d}" for r in range(world) for i in range(n_local)]
-        arrays = ProfileArrays.uniform_grid(ids, orig, freq, mine.grid[:G],
-                                            qual.reshape(world * n_local, len(space.methods), G), has)
-    else:
-        arrays = mine
+    # global profile set: all-gather every rank's profile rows (NCCL), then
+    # the replicated deterministic greedy over all contexts (distributed.py)
+    arrays = distributed.gather_profiles(mine, device=f"cuda:{local}") if world > 1 else mine
     tiers = workload.three_tiers(int(arrays.orig.sum()), cfg["gpu_frac"], 0.30)
-    my_lo, my_hi = rank * n_local, (rank + 1) * n_local
+    my_lo, my_hi = distributed.shard(arrays.n, world, rank)
 
     stream = torch.cuda.Stream()
     eng = Engine(pkg.product(), device=local, stream=stream.cuda_stream)
