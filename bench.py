@@ -110,6 +110,86 @@ def algorithmic_bytes(L, H, T, cfg, m):
     }
 
 
+SCORER_KERNEL = {0: "k_knorm", 1: "k_keydiff_cluster", 2: "k_snapkv_tc"}
+
+
+def traffic_table():
+    """ncu-measured DRAM bytes per launch (dram__bytes_read.sum +
+    dram__bytes_write.sum, one --set full capture per kernel on one full
+    Llama-3.1-8B chunk), committed under profiles/; None when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, lo, hi):
+    """One instrumented pass over this rank's contexts, every codec phase
+    its own C-ABI call bracketed by CUDA events on the launching stream:
+    time and algorithmic bytes per kernel (scores per scorer, top-k, pack per
+    bit width), the dominant kernel's roofline, and per-phase shares."""
+    import torch
+
+    from paper_2512_14946_b200 import _abi as A
+
+    snap = store.snapshot()
+    names = space.method_names
+    recs = []
+    for c in range(lo, hi):
+        if snap["tier_index"][c] < 0:
+            continue
+        T = int(arrays.orig[c] // bpt)
+        cfgc, m, wsb = codec.plan(names[snap["method"][c]], float(snap["ratio"][c]), T)
+        s = A.KvShape(L, H, T, D)
+        k, v = pool.chunk(c)
+        sc = codec.ws  # scores at offset 0
+        idx = codec.ws.data_ptr() + wsb - ((4 * L * H * cfgc.keep + 255) // 256) * 256
+        ab = algorithmic_bytes(L, H, T, cfgc, m)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        evs[0].record(stream)
+        full = cfgc.keep == T  # every token kept: compress skips scoring and selection
+        if not full:
+            eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(sc)))
+        evs[1].record(stream)
+        if not full:
+            eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfgc), A.ptr(sc), idx))
+        evs[2].record(stream)
+        eng.abi.check(eng.abi.pack(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), idx, A.ptr(codec.out[0])))
+        evs[3].record(stream)
+        keys = [None if full else SCORER_KERNEL[cfgc.scorer], None if full else "k_topk",
+                "k_gather16" if cfgc.bits == 16 else f"k_pack_k+v<{cfgc.bits}>"]
+        recs.append((evs, keys, [ab["scores"], ab["topk"], ab["pack"]]))
+    torch.cuda.synchronize()
+    per = {}
+    phase = {"scores": 0.0, "topk": 0.0, "pack": 0.0}
+    for evs, keys, abs_ in recs:
+        for i, (key, ph) in enumerate(zip(keys, ("scores", "topk", "pack"))):
+            if key is None:
+                continue
+            dt = evs[i].elapsed_time(evs[i + 1])
+            e = per.setdefault(key, [0.0, 0, 0])
+            e[0] += dt
+            e[1] += abs_[i]
+            e[2] += 1
+            phase[ph] += dt
+    tot = sum(phase.values())
+    dom = max(per, key=lambda k_: per[k_][0])
+    t_ms, alg, n = per[dom]
+    pk, how = peaks()
+    achieved = alg / (t_ms / 1e3) / 1e9
+    traffic = traffic_table().get(dom)
+    return {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4),
+            "traffic": traffic, "traffic_note": "ncu dram read+write bytes per launch (profiles/traffic.json)",
+            "alg_bytes_per_launch": int(alg // n), "avg_launch_ms": round(t_ms / n, 4), "launches": n,
+            "peak_source": how, "time_share": round(t_ms / tot, 4),
+            "phase_share": {ph: round(v / tot, 4) for ph, v in phase.items()},
+            "kernels": {k_: {"ms": round(v[0], 2), "n": v[2], "GBps": round(v[1] / (v[0] / 1e3) / 1e9, 1),
+                             "frac": round(v[1] / (v[0] / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
+                        for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -242,58 +322,8 @@ def run_b200(args):
 
     # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
     roof = None
-    phases = {}
     if rank == 0:
-        snap_full = store.snapshot()
-        names = space.method_names
-        ev = {}
-        acc = {"scores": 0.0, "topk": 0.0, "pack": 0.0}
-        alg = {"scores": 0, "topk": 0, "pack": 0}
-        nl = {"scores": 0, "topk": 0, "pack": 0}
-        by_scorer = {}
-        for c in range(my_lo, my_hi):
-            T = int(arrays.orig[c] // bpt)
-            cfgc, m, _ = codec.plan(names[snap_full["method"][c]], float(snap_full["ratio"][c]), T)
-            s = A.KvShape(L, H, T, D)
-            k, v = pool.chunk(c)
-            ws = codec.ws
-            sc = ws  # scores at offset 0
-            idx_off = eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfgc)) - ((4 * L * H * cfgc.keep + 255) // 256) * 256
-            idx = ws.data_ptr() + idx_off
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            evs[0].record(stream)
-            eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(sc)))
-            evs[1].record(stream)
-            eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfgc), A.ptr(sc), idx))
-            evs[2].record(stream)
-            eng.abi.check(eng.abi.pack(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), idx,
-                                       A.ptr(codec.out[c % 2])))
-            evs[3].record(stream)
-            ab = algorithmic_bytes(L, H, T, cfgc, m)
-            ev[c] = (evs, ab, cfgc.scorer)
-        torch.cuda.synchronize()
-        for c, (evs, ab, scorer) in ev.items():
-            for i, ph in enumerate(("scores", "topk", "pack")):
-                dt = evs[i].elapsed_time(evs[i + 1])
-                acc[ph] += dt
-                alg[ph] += ab[ph]
-                nl[ph] += 1
-                if ph == "scores":
-                    b = by_scorer.setdefault(scorer, [0.0, 0, 0])
-                    b[0] += dt
-                    b[1] += ab[ph]
-                    b[2] += 1
-        tot = sum(acc.values())
-        phases = {ph: round(acc[ph] / tot, 4) for ph in acc}
-        dom = max(acc, key=acc.get)
-        pk, how = peaks()
-        achieved = alg[dom] / (acc[dom] / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": None,
-                "peak_source": how, "avg_launch_ms": round(acc[dom] / max(1, nl[dom]), 4),
-                "phase_share": phases,
-                "scores_by_scorer_gbs": {["knorm", "keydiff", "snapkv"][s_]: round(b[1] / (b[0] / 1e3) / 1e9, 1)
-                                         for s_, b in by_scorer.items()}}
+        roof = kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, my_lo, my_hi)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -84,10 +84,10 @@ def main():
             if r == 0:
                 continue  # warm-up
             for i, p in enumerate(("scores", "topk", "pack", "compress")):
-                acc[p] += ev[i].elapsed_time(ev[i + 1]) / args.reps
+                acc[p] += ev[i].elapsed_time(ev[i + 1]) / max(1, args.reps)
         out = {"method": meth, "ratio": float(ratio), "bits": cfg.bits, "keep": kk, "T": s.T, "L": s.L}
         for p in alg:
-            gbs = alg[p] / (acc[p] / 1e3) / 1e9
+            gbs = alg[p] / (acc[p] / 1e3) / 1e9 if acc[p] > 0 else 0.0
             out[p] = {"ms": round(acc[p], 4), "alg_bytes": alg[p], "GBps": round(gbs, 1), "frac": round(gbs / peak, 4)}
         print(json.dumps(out), flush=True)
 
