@@ -296,6 +296,34 @@ typedef struct {
 
 KVT_DECLARE_CODEC(kvt_)
 
+/* ------------------------------------------------------------------------
+ * Tier-move executor: turns placement decisions
+ * (PlacementAction, proj/include/kvtier/core.hpp:96-103; built at
+ * proj/src/placement.cpp:213-221, only modelled by the reference)
+ * into byte movement between the GPU tier (HBM) and the CPU tier (a pinned
+ * host arena). A batch of moves is split into <= 8 MiB pieces spread over the
+ * handle's copy streams (D2H and H2D use different copy engines, so the two
+ * directions overlap); the batch starts after everything already queued on
+ * the handle's stream (e.g. the compress that produced the blob) and the
+ * handle's stream waits for its completion.
+ * ------------------------------------------------------------------------ */
+typedef enum { KVT_MOVE_D2H = 0, KVT_MOVE_H2D = 1, KVT_MOVE_D2D = 2, KVT_MOVE_H2H = 3 } kvt_move_kind;
+
+typedef struct {
+  const void* src;
+  void* dst;
+  int64_t bytes;
+  int32_t kind; /* kvt_move_kind */
+  int32_t pad_;
+} kvt_move;
+
+/* pinned (page-locked) host arena for the CPU tier */
+int kvt_tier_host_alloc(int64_t bytes, void** out);
+int kvt_tier_host_free(void* p);
+int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
+/* the CPU restatement: plain memcpy (host pointers only) */
+int orc_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
+
 /* Device-pointer variants and timing helpers used by the bench. */
 /* Synchronise the handle's stream. */
 int kvt_sync(kvt_handle* h);

@@ -799,3 +799,14 @@ int orc_store_bind_space(kvt_store* s, const kvt_space* space) {
   (void)s;
   return resolve_space(space, &sp);
 }
+
+/* tier moves, CPU restatement: every move is a plain memcpy of host memory
+ * (test infrastructure: the same batch semantics as kvt_tier_moves) */
+int orc_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n) {
+  (void)h;
+  for (int64_t i = 0; i < n; ++i) {
+    if (moves[i].bytes < 0 || (moves[i].bytes > 0 && (!moves[i].src || !moves[i].dst))) return KVT_EINVAL;
+    if (moves[i].bytes) memcpy(moves[i].dst, moves[i].src, (size_t)moves[i].bytes);
+  }
+  return KVT_OK;
+}

@@ -84,6 +84,13 @@ class BlobMap(C.Structure):
         "total_bytes")]
 
 
+class Move(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("bytes", C.c_int64), ("kind", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+KVT_MOVE_D2H, KVT_MOVE_H2D, KVT_MOVE_D2D, KVT_MOVE_H2H = 0, 1, 2, 3
+
 ACTION_DTYPE = np.dtype([("kind", "<i4"), ("ctx", "<i4"), ("tier_id", "<i4"), ("method", "<i4"),
                          ("ratio", "<f8")])
 ENTRY_DTYPE = np.dtype([("tier_index", "<i4"), ("method", "<i4"), ("ratio", "<f8"),
@@ -146,7 +153,10 @@ PRODUCT_EXTRA_SIGS = {
     "sync": (C.c_int, [P]),
     "set_stream": (C.c_int, [P, P]),
     "launch_count": (i64, [P]),
+    "tier_host_alloc": (C.c_int, [i64, PP]),
+    "tier_host_free": (C.c_int, [P]),
 }
+TIER_SIGS = {"tier_moves": (C.c_int, [P, C.POINTER(Move), i64])}
 
 
 class AbiError(RuntimeError):
@@ -174,6 +184,8 @@ class Abi:
             sigs.update(CODEC_SIGS)
         if extra:
             sigs.update(PRODUCT_EXTRA_SIGS)
+        if hasattr(self.lib, prefix + "tier_moves"):
+            sigs.update(TIER_SIGS)
         for name, (res, args) in sigs.items():
             fn = getattr(self.lib, prefix + name)
             fn.restype = res

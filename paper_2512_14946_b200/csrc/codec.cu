@@ -837,8 +837,25 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
-  k_snap_q<<<S, 256, 0, h->stream>>>(qbuf, s->H, W, G, static_cast<uint64_t>(c->q_seed));
-  LAUNCHED(h);
+  (void)qbuf;  // Q8 tiles live in the handle's cache (same for every chunk of this shape)
+  const unsigned long long key[5] = {static_cast<unsigned long long>(s->L), static_cast<unsigned long long>(s->H),
+                                     static_cast<unsigned long long>(W), static_cast<unsigned long long>(G),
+                                     static_cast<unsigned long long>(c->q_seed)};
+  const size_t qbytes = size_t(kSnapQBytes) * S;
+  if (!h->snapq || h->snapq_bytes < qbytes || std::memcmp(key, h->snapq_key, sizeof key) != 0) {
+    if (h->snapq_bytes < qbytes) {
+      if (h->snapq) KVT_CUDA_TRY(cudaFree(h->snapq));
+      h->snapq = nullptr;
+      h->snapq_bytes = 0;
+      KVT_CUDA_TRY(cudaMalloc(&h->snapq, qbytes));
+      h->snapq_bytes = qbytes;
+    }
+    k_snap_q<<<S, 256, 0, h->stream>>>(static_cast<uint8_t*>(h->snapq), s->H, W, G, static_cast<uint64_t>(c->q_seed));
+    LAUNCHED(h);
+    KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));  // once per shape: safe for later launches on any stream
+    std::memcpy(h->snapq_key, key, sizeof key);
+  }
+  qbuf = static_cast<uint8_t*>(h->snapq);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(Cn, S);
   cfg.blockDim = dim3(kSnapThreads);

@@ -112,6 +112,11 @@ struct kvt_handle {
   long long launches = 0;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // snapkv Q8 tiles depend only on (L, H, W, G, q_seed), not on the KV
+  // chunk: generated once per key and reused by every chunk of that shape
+  void* snapq = nullptr;
+  size_t snapq_bytes = 0;
+  unsigned long long snapq_key[5] = {0, 0, 0, 0, 0};
 };
 
 namespace kvt {

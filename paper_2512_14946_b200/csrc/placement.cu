@@ -22,6 +22,8 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -78,6 +80,7 @@ extern "C" int kvt_create(int device, void* stream, kvt_handle** out) {
 extern "C" int kvt_destroy(kvt_handle* h) {
   if (!h) return KVT_OK;
   if (h->scratch) cudaFree(h->scratch);
+  if (h->snapq) cudaFree(h->snapq);
   delete h;
   return KVT_OK;
 }
@@ -1540,5 +1543,82 @@ extern "C" int kvt_placement_utility(kvt_store* s, const kvt_pset* p, const kvt_
   KVT_CUDA_TRY(cudaStreamSynchronize(st));
   if (h_bad) return set_error(KVT_EVALIDATION, "resident " + std::to_string(h_bad - 1) +
                                                    " has a configuration its profile cannot score");
+  return KVT_OK;
+}
+
+// ------------------------------------------------------------ tier moves
+// Tier-move executor (include/kvt_b200.h). Each handle owns
+// two copy streams per direction; a batch is split into <= 8 MiB pieces
+// dealt round-robin over the streams of its direction, fenced after the
+// handle's stream (input ready) and joined back into it (completion).
+namespace {
+constexpr int64_t kMovePiece = 8LL << 20;
+struct MoveStreams {
+  cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};  // d2h x2, h2d x2
+  cudaEvent_t start = nullptr, done[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+std::mutex g_move_mu;
+std::unordered_map<kvt_handle*, MoveStreams> g_moves;
+
+int move_streams(kvt_handle* h, MoveStreams** out) {
+  std::lock_guard<std::mutex> lk(g_move_mu);
+  MoveStreams& m = g_moves[h];
+  if (!m.s[0]) {
+    for (int i = 0; i < 4; ++i) {
+      KVT_CUDA_TRY(cudaStreamCreateWithFlags(&m.s[i], cudaStreamNonBlocking));
+      KVT_CUDA_TRY(cudaEventCreateWithFlags(&m.done[i], cudaEventDisableTiming));
+    }
+    KVT_CUDA_TRY(cudaEventCreateWithFlags(&m.start, cudaEventDisableTiming));
+  }
+  *out = &m;
+  return KVT_OK;
+}
+}  // namespace
+
+extern "C" int kvt_tier_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return set_error(KVT_EINVAL, "bad host arena request");
+  *out = nullptr;
+  KVT_CUDA_TRY(cudaHostAlloc(out, static_cast<size_t>(bytes > 0 ? bytes : 1), cudaHostAllocDefault));
+  return KVT_OK;
+}
+
+extern "C" int kvt_tier_host_free(void* p) {
+  if (p) KVT_CUDA_TRY(cudaFreeHost(p));
+  return KVT_OK;
+}
+
+extern "C" int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n) {
+  if (!h || (n > 0 && !moves)) return set_error(KVT_EINVAL, "null argument");
+  if (n <= 0) return KVT_OK;
+  MoveStreams* ms;
+  int rc;
+  if ((rc = move_streams(h, &ms))) return rc;
+  KVT_CUDA_TRY(cudaEventRecord(ms->start, h->stream));
+  bool used[4] = {false, false, false, false};
+  int next[2] = {0, 0};  // round-robin per direction class (0: to host, 1: to device)
+  for (int64_t i = 0; i < n; ++i) {
+    const kvt_move& mv = moves[i];
+    if (mv.bytes < 0 || (mv.bytes > 0 && (!mv.src || !mv.dst)) || mv.kind < 0 || mv.kind > KVT_MOVE_H2H)
+      return set_error(KVT_EINVAL, "bad move " + std::to_string(i));
+    static const cudaMemcpyKind kinds[4] = {cudaMemcpyDeviceToHost, cudaMemcpyHostToDevice, cudaMemcpyDeviceToDevice,
+                                            cudaMemcpyHostToHost};
+    const int cls = (mv.kind == KVT_MOVE_H2D || mv.kind == KVT_MOVE_D2D) ? 1 : 0;
+    for (int64_t off = 0; off < mv.bytes; off += kMovePiece) {
+      const int si = cls * 2 + next[cls];
+      next[cls] ^= 1;
+      if (!used[si]) {
+        KVT_CUDA_TRY(cudaStreamWaitEvent(ms->s[si], ms->start, 0));
+        used[si] = true;
+      }
+      const size_t len = static_cast<size_t>(std::min(kMovePiece, mv.bytes - off));
+      KVT_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(mv.dst) + off, static_cast<const char*>(mv.src) + off, len,
+                                   kinds[mv.kind], ms->s[si]));
+    }
+  }
+  for (int i = 0; i < 4; ++i)
+    if (used[i]) {
+      KVT_CUDA_TRY(cudaEventRecord(ms->done[i], ms->s[i]));
+      KVT_CUDA_TRY(cudaStreamWaitEvent(h->stream, ms->done[i], 0));
+    }
   return KVT_OK;
 }
