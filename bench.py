@@ -190,6 +190,61 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
                         for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
 
 
+def tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, lo, hi, n_ctx=4, reps=3):
+    """SURVEY §8 f1 evidence: pinned cudaMemcpyAsync GB/s of the tier-move
+    executor (kvt_tier_moves) moving the compressed blobs of contexts the
+    greedy placed below the GPU tier to the pinned CPU-tier arena (D2H) and
+    back (H2D), CUDA events on the handle stream. PCIe-bound; reported beside
+    the HBM-bound codec, not folded into `value`."""
+    import torch
+
+    from paper_2512_14946_b200 import _abi as A
+    from paper_2512_14946_b200.tiers import HostArena, TierExecutor, host_moves_bytes
+
+    snap = store.snapshot()
+    names = space.method_names
+    blobs, placed = [], []
+    for c in range(lo, hi):
+        if snap["tier_index"][c] <= 0 or len(blobs) >= n_ctx:
+            continue
+        T = int(arrays.orig[c] // bpt)
+        cfgc, m, _ = codec.plan(names[snap["method"][c]], float(snap["ratio"][c]), T)
+        s = A.KvShape(L, H, T, D)
+        k, v = pool.chunk(c)
+        b = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), A.ptr(codec.ws),
+                                       A.ptr(b)))
+        blobs.append(b)
+        placed.append((c, int(snap["tier_index"][c]), b.data_ptr(), b.numel()))
+    if not blobs:
+        return None
+    arena = HostArena(eng.abi, sum(b.numel() for b in blobs) + (1 << 20))
+    ex = TierExecutor(eng, arena)
+    down = ex.moves_for(placed)
+    up = ex.reverse(down)
+    nbytes = host_moves_bytes(down)
+    rates = {}
+    for name, mv in (("d2h", down), ("h2d", up)):
+        ex.run(mv)  # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            ex.run(mv)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rates[name] = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    ok = True  # the host copies equal the device blobs (after the last D2H + H2D round trip)
+    for b, mv in zip(blobs, down):
+        host = np.ctypeslib.as_array((C.c_uint8 * mv.bytes).from_address(mv.dst))
+        ok &= bool(np.array_equal(host, b.cpu().numpy()))
+    arena.close()
+    return {"d2h_gbs": round(rates["d2h"], 1), "h2d_gbs": round(rates["h2d"], 1), "bytes": nbytes,
+            "contexts": len(blobs), "verified": bool(ok),
+            "note": "kvt_tier_moves: compressed blobs of CPU/SSD-tier contexts, device <-> pinned host, "
+                    "8 MiB pieces over 2 copy streams per direction"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -322,8 +377,10 @@ def run_b200(args):
 
     # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
     roof = None
+    tier_move = None
     if rank == 0:
         roof = kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, my_lo, my_hi)
+        tier_move = tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, my_lo, my_hi)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -348,6 +405,7 @@ def run_b200(args):
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "tier_move": tier_move,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
