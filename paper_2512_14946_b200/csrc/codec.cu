@@ -404,35 +404,44 @@ static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKd
 // thread votes one token from the stored E (no second exp), and pooling reads
 // neighbour CTAs' votes through DSMEM. The next tile's copy overlaps the MMA
 // and epilogue of the current one.
-constexpr int kSnapTPC = 4;            // tiles per CTA
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
 constexpr int kSnapProd = 8;           // producer warps: K tile absmax + int8 quantisation + MMA issue
 constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
 constexpr int kSnapThreads = (kSnapProd + kSnapCons) * 32;
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
 constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
+// Two configurations of one kernel: prefixes up to 16 x 4 tiles (8192
+// tokens) keep the u16 E matrix in smem (TPC = 4, 218 KB); longer ones
+// (up to 16 x 16 tiles) keep it in a global scratch slot per SM (TPC = 16,
+// E [128 rows][2048 tokens] = 512 KB per CTA, one CTA per SM).
+constexpr int kSnapTpcSmem = 4, kSnapTpcGlobal = 16;
+constexpr int kSnapESlots = 256;  // >= %nsmid on B200
+constexpr int64_t kSnapESlotBytes = 128LL * kSnapTpcGlobal * 128 * 2;
 
-// E is [row][512 tokens] u16, 1 KiB per row, 16-byte chunk c of row r stored
-// at chunk c ^ (r & 7): conflict-free row-wise STS.128 and token-wise LDS.32.
-struct SnapSmem {
+// E in smem is [row][512 tokens] u16, 1 KiB per row, 16-byte chunk c of row
+// r stored at chunk c ^ (r & 7): conflict-free row-wise STS.128 and
+// token-wise LDS.32.
+template <int TPC, bool EG>
+struct SnapSmemT {
   uint8_t k8[2][128 * 128];  // offset 0 of the 1024-aligned base; double-buffered
   uint8_t q8[128 * 128];
   uint4 stage[128 * 16];     // one bf16 tile (32 KB); after the tile loop: combine scratch + votes
-  uint8_t e[128 * 1024];
-  int32_t mb[kSnapTPC * 4][128];   // per (block, row) shift M
-  uint32_t lb[kSnapTPC * 4][128];  // per (block, row) sum of E, then the block weight
+  uint8_t e[EG ? 16 : 128 * 1024];
+  int32_t mb[TPC * 4][128];   // per (block, row) shift M
+  uint32_t lb[TPC * 4][128];  // per (block, row) sum of E, then the block weight
   float sig[128];
-  float tau[kSnapTPC];
+  float tau[TPC];
   uint32_t amax[kSnapProd];
   uint64_t full, qbar, tfull[2], tempty[2];
   uint32_t tmem_base;
 };
-struct SnapScratch {  // aliases SnapSmem::stage after the tile loop
-  unsigned long long vote[512];
+template <int TPC>
+struct SnapScratchT {  // aliases SnapSmemT::stage after the tile loop
+  unsigned long long vote[TPC * 128];
   unsigned long long lloc[128];
   int32_t mloc[128], mrow[128];
 };
-static_assert(sizeof(SnapScratch) <= 128 * 16 * sizeof(uint4), "scratch fits the stage");
+static_assert(sizeof(SnapScratchT<kSnapTpcGlobal>) <= 128 * 16 * sizeof(uint4), "scratch fits the stage");
 
 __device__ __forceinline__ uint32_t snap_e_off(int r, int byte) {  // swizzled byte offset of E[r][byte / 2]
   return static_cast<uint32_t>(r) * 1024u + ((((byte >> 4) ^ r) & 7) | ((byte >> 4) & ~7)) * 16u + (byte & 15);
@@ -549,9 +558,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
+template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
-    k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, float* __restrict__ scores, int T,
-                int W, int G, int pool, int tpc) {
+    k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, uint8_t* __restrict__ escr,
+                float* __restrict__ scores, int T, int W, int G, int pool, int tpc) {
+  using SnapSmem = SnapSmemT<TPC, EG>;
+  using SnapScratch = SnapScratchT<TPC>;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int slice = blockIdx.y;
@@ -565,6 +577,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   // 1024-align by offset (keeps the shared address space visible: LDS/STS, not generic LD/ST)
   SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + ((1024u - (smem_u32(snap_raw) & 1023u)) & 1023u));
   const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+  uint16_t* Eg = nullptr;  // EG: E[r][t] at Eg[r * TPC * 128 + t] (this SM's slot; one CTA per SM)
+  if (EG) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= kSnapESlots) __trap();
+    Eg = reinterpret_cast<uint16_t*>(escr + smid * kSnapESlotBytes);
+  }
 
   if (tid == 0) {
     mbar_init(&sm.full, 1);
@@ -698,10 +717,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = 0;
       }
+      if (EG) {
+        uint4* erow = reinterpret_cast<uint4*>(Eg + r * (TPC * 128) + tok0);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
-            make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < 4; ++i) __stcg(erow + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
+              make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
       sm.mb[j * 4 + cb][r] = M;
       sm.lb[j * 4 + cb][r] = L;
     }
@@ -752,9 +777,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   }
   // every peer has read this CTA's mloc / lloc before the votes overwrite them
   cluster_sync_smem();
-  // ---- votes: thread = token pair (2p, 2p + 1) x a quarter... of the rows; rows >= R have zero weight
-  {
-    const int p = tid % 256, rq = tid / 256;  // 640 threads: rq 0, 1 take 64 rows each, rq 2 idles
+  // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows (rq 0, 1; rq 2 idles);
+  // TPC / 4 rounds of 256 pairs; rows >= R have zero weight
+  for (int round = 0; round < TPC / 4; ++round) {
+    const int p = (tid % 256) + 256 * round, rq = tid / 256;
     unsigned long long a0 = 0, a1 = 0;
     if (rq < 2 && 2 * p < n_loc) {
       const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
@@ -765,7 +791,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int r = rq * 64 + r0 + q;
-          const uint32_t e2 = *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(r, 4 * p));
+          const uint32_t e2 = EG ? __ldcg(reinterpret_cast<const uint32_t*>(Eg + r * (TPC * 128)) + p)
+                                 : *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(r, 4 * p));
           a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
           a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
         }
@@ -773,14 +800,15 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     }
     unsigned long long* part = reinterpret_cast<unsigned long long*>(sm.k8);  // K8 no longer needed
     if (rq == 1) {
-      part[2 * p] = a0;
-      part[2 * p + 1] = a1;
+      part[2 * (p % 256)] = a0;
+      part[2 * (p % 256) + 1] = a1;
     }
     __syncthreads();
     if (rq == 0) {
-      xs.vote[2 * p] = a0 + part[2 * p];
-      xs.vote[2 * p + 1] = a1 + part[2 * p + 1];
+      xs.vote[2 * p] = a0 + part[2 * (p % 256)];
+      xs.vote[2 * p + 1] = a1 + part[2 * (p % 256) + 1];
     }
+    __syncthreads();
   }
   cluster_sync_smem();  // every CTA's votes visible
   // ---- pooling (max over +-pool/2 within the prefix) and scores
@@ -826,16 +854,31 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     return KVT_OK;
   }
   const int ntiles = (P + 127) / 128;
-  const int Cn = (ntiles + kSnapTPC - 1) / kSnapTPC;
+  const bool eg = ntiles > kSnapMaxC * kSnapTpcSmem;  // E no longer fits the cluster's smem
+  const int tpc_max = eg ? kSnapTpcGlobal : kSnapTpcSmem;
+  const int Cn = (ntiles + tpc_max - 1) / tpc_max;
   if (Cn > kSnapMaxC)
-    return set_error(KVT_EINVAL, "snapkv: prefix (T - window) longer than 8192 tokens is not supported");
+    return set_error(KVT_EINVAL, "snapkv: prefix (T - window) longer than 32768 tokens is not supported");
   const int tpc = (ntiles + Cn - 1) / Cn;
-  const size_t smem = sizeof(SnapSmem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    KVT_CUDA_TRY(cudaFuncSetAttribute(k_snapkv_tc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
+  const size_t smem = (eg ? sizeof(SnapSmemT<kSnapTpcGlobal, true>) : sizeof(SnapSmemT<kSnapTpcSmem, false>)) + 1024;
+  auto kern = eg ? k_snapkv_tc<kSnapTpcGlobal, true> : k_snapkv_tc<kSnapTpcSmem, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[eg]) {
+    KVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    KVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[eg] = true;
+  }
+  uint8_t* escr = nullptr;
+  if (eg) {  // E scratch slots (one per SM) live with the handle
+    const size_t need = size_t(kSnapESlots) * kSnapESlotBytes;
+    if (h->snape_bytes < need) {
+      if (h->snape) KVT_CUDA_TRY(cudaFree(h->snape));
+      h->snape = nullptr;
+      h->snape_bytes = 0;
+      KVT_CUDA_TRY(cudaMalloc(&h->snape, need));
+      h->snape_bytes = need;
+    }
+    escr = static_cast<uint8_t*>(h->snape);
   }
   (void)qbuf;  // Q8 tiles live in the handle's cache (same for every chunk of this shape)
   const unsigned long long key[5] = {static_cast<unsigned long long>(s->L), static_cast<unsigned long long>(s->H),
@@ -868,8 +911,8 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_snapkv_tc, reinterpret_cast<const uint4*>(k),
-                                  static_cast<const uint8_t*>(qbuf), scores, T, W, G, c->pool, tpc));
+  KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(k), static_cast<const uint8_t*>(qbuf), escr,
+                                  scores, T, W, G, c->pool, tpc));
   LAUNCHED(h);
   return KVT_OK;
 }

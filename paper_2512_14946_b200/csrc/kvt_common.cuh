@@ -117,6 +117,8 @@ struct kvt_handle {
   void* snapq = nullptr;
   size_t snapq_bytes = 0;
   unsigned long long snapq_key[5] = {0, 0, 0, 0, 0};
+  void* snape = nullptr;  // snapkv E scratch slots for prefixes beyond 8192 tokens
+  size_t snape_bytes = 0;
 };
 
 namespace kvt {

@@ -81,6 +81,7 @@ extern "C" int kvt_destroy(kvt_handle* h) {
   if (!h) return KVT_OK;
   if (h->scratch) cudaFree(h->scratch);
   if (h->snapq) cudaFree(h->snapq);
+  if (h->snape) cudaFree(h->snape);
   delete h;
   return KVT_OK;
 }

@@ -101,10 +101,12 @@ def topk(eng, s, cfg, sc, on_gpu):
 
 # snapkv prefix lengths: one tile, 1 token, several tiles in one CTA, a
 # 16-CTA (non-portable) cluster (T = 8192), a 9-CTA cluster with a ragged
-# last tile and block, the longest prefix (8192 tokens, 16 full CTAs), and
-# prefixes of length 0 (all window)
+# last tile and block, the longest smem-E prefix (8192 tokens, 16 full CTAs),
+# the global-E configuration (8193 tokens: 5 CTAs x 13 tiles; 16352: 8 x 16),
+# and prefixes of length 0 (all window)
 SNAP_SHAPES = SHAPES + [A.KvShape(1, 1, 33, 128), A.KvShape(1, 2, 8192, 128), A.KvShape(2, 1, 4097, 128),
-                        A.KvShape(1, 1, 8224, 128), A.KvShape(1, 2, 32, 128), A.KvShape(1, 1, 20, 128)]
+                        A.KvShape(1, 1, 8224, 128), A.KvShape(1, 1, 8225, 128), A.KvShape(1, 2, 16384, 128),
+                        A.KvShape(1, 2, 32, 128), A.KvShape(1, 1, 20, 128)]
 
 
 @pytest.mark.parametrize("si", range(len(SNAP_SHAPES)))
@@ -119,7 +121,7 @@ def test_snapkv_scores_bitexact(gpu, orc, si):
 
 
 def test_snapkv_rejects_too_long_prefix(gpu):
-    s = A.KvShape(1, 1, 8192 + 32 + 1, 128)  # prefix of 8193 tokens
+    s = A.KvShape(1, 1, 32768 + 32 + 1, 128)  # prefix of 32769 tokens
     cfg = plan(gpu.abi, "snapkv", 0.3, s)
     k = torch.zeros(s.L * s.H * s.T * s.D, dtype=torch.int16, device="cuda")
     out = torch.empty(s.L * s.H * s.T, dtype=torch.float32, device="cuda")
