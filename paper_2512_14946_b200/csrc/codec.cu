@@ -440,6 +440,7 @@ struct SnapScratchT {  // aliases SnapSmemT::stage after the tile loop
   unsigned long long vote[TPC * 128];
   unsigned long long lloc[128];
   int32_t mloc[128], mrow[128];
+  unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
 };
 static_assert(sizeof(SnapScratchT<kSnapTpcGlobal>) <= 128 * 16 * sizeof(uint4), "scratch fits the stage");
 
@@ -810,27 +811,29 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     }
     __syncthreads();
   }
-  cluster_sync_smem();  // every CTA's votes visible
+  // push this CTA's boundary votes into the neighbours' halos (non-last CTAs are full: n_loc = tpc * 128)
+  const int half = pool / 2;
+  if (tid < half) {
+    if (rank > 0 && tid < n_loc) cl.map_shared_rank(xs.rhalo, rank - 1)[tid] = xs.vote[tid];
+    if (rank < C - 1) cl.map_shared_rank(xs.lhalo, rank + 1)[tid] = xs.vote[n_loc - half + tid];
+  }
+  // halos visible; after this barrier no CTA touches another's smem, so CTAs retire independently
+  cluster_sync_smem();
   // ---- pooling (max over +-pool/2 within the prefix) and scores
   float* out = scores + static_cast<size_t>(slice) * T;
-  const int half = pool / 2;
   for (int tl = tid; tl < n_loc; tl += kSnapThreads) {
     unsigned long long m = 0;
     for (int dj = -half; dj <= half; ++dj) {
       const int tg = t_lo + tl + dj;  // global prefix token
       if (tg < 0 || tg >= P) continue;
-      const int span = tpc * 128;  // tokens per CTA; |dj| <= pool / 2 < span: neighbours live in rank +- 1
-      const int owner = tg < t_lo ? rank - 1 : (tg >= t_lo + span ? rank + 1 : rank);
-      const int tr = tg - owner * span;
-      const unsigned long long* vv = owner == rank ? xs.vote : cl.map_shared_rank(xs.vote, owner);
-      const unsigned long long x = vv[tr];
+      const int li = tl + dj;
+      const unsigned long long x = li < 0 ? xs.lhalo[li + half] : (li >= n_loc ? xs.rhalo[li - n_loc] : xs.vote[li]);
       m = x > m ? x : m;
     }
     out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 2.8421709430404007e-14f);  // 2^-45 (exact)
   }
   if (rank == C - 1)
     for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
-  cluster_sync_smem();  // no CTA leaves while its votes may still be read
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
@@ -845,7 +848,8 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
                          float* scores, uint8_t* qbuf) {
   const int S = s->L * s->H, T = s->T, W = c->window, G = c->q_heads;
   if (W * G > 128 || W > T || W < 0 || G < 1) return set_error(KVT_EINVAL, "snapkv window x q_heads must be <= 128");
-  if (c->pool < 1 || (c->pool & 1) == 0) return set_error(KVT_EINVAL, "snapkv pool must be odd");
+  if (c->pool < 1 || (c->pool & 1) == 0 || c->pool > 15)
+    return set_error(KVT_EINVAL, "snapkv pool must be odd and <= 15");
   const int P = T - W;
   if (P <= 0) {
     const long long n = static_cast<long long>(S) * T;
