@@ -1253,7 +1253,7 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(256) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(256, 4) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
                                                 uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
                                                 uint16_t* __restrict__ kz, int T, int k) {
   __shared__ PackKSmem sm;
@@ -1338,7 +1338,7 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
 
 // grid (ceil(k / (16 * kVRows)), S): 16 half-warps x kVRows rows per block
 template <int BITS>
-__global__ void __launch_bounds__(256) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(256, 4) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
                                                 int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
                                                 uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k) {
   pack_v_rows<BITS>(V, idx, oidx, vc, vs, vz, T, k, blockIdx.y, (blockIdx.x * 16 + (threadIdx.x >> 4)) * kVRows);
