@@ -186,6 +186,48 @@ __device__ __forceinline__ void stream_rows(const uint4* __restrict__ src, int n
   seq += nch;
 }
 
+// stream_rows with the half-warp's kRingRows / 16 rows of a ring chunk handed
+// over together: f(t[], live[], v[]) can batch per-row work across them.
+template <class F>
+__device__ __forceinline__ void stream_rows4(const uint4* __restrict__ src, int n, uint4* ring, uint64_t* full,
+                                             uint32_t& seq, F&& f) {
+  constexpr int kU = kRingRows / 16;
+  const int tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
+  const int nch = (n + kRingRows - 1) / kRingRows;
+  auto issue = [&](int c) {
+    const int st = (seq + c) % kRingStages;
+    const int rows = min(kRingRows, n - c * kRingRows);
+    mbar_expect_tx(&full[st], rows * 256);
+    bulk_g2s(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
+             rows * 256, &full[st]);
+  };
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int c = 0; c < min(nch, kRingStages); ++c) issue(c);
+  }
+  for (int c = 0; c < nch; ++c) {
+    const uint32_t g = seq + c;
+    const int st = g % kRingStages;
+    mbar_wait(&full[st], (g / kRingStages) & 1);
+    const int rows = min(kRingRows, n - c * kRingRows);
+    const uint4* base = ring + static_cast<size_t>(st) * kRingRows * 16;
+    int t[kU];
+    bool live[kU];
+    uint4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int r = (hw & ~1) * kU + 2 * u + (hw & 1);
+      t[u] = c * kRingRows + r;
+      live[u] = r < rows;
+      v[u] = live[u] ? base[r * 16 + l16] : make_uint4(0, 0, 0, 0);
+    }
+    f(t, live, v);
+    __syncthreads();
+    if (tid == 0 && c + kRingStages < nch) issue(c + kRingStages);
+  }
+  seq += nch;
+}
+
 // --------------------------------------------------------------- scores
 
 // Canonical fp32 row dot product (oracle row_dot): lane
@@ -350,12 +392,20 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
   uint32_t seq = 0;
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   uint32_t cnt = 0;  // <= per / 16 tokens per lane: the biased u32 sums cannot wrap for T < 2^16
-  stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
-    const float inv = kd_inv(half_butterfly(chunk_sumsq(v)));
-    if (live) {
-      kd_fix_add(v, __fmul_rn(inv, kKdFx), acc);
-      ++cnt;
-      if (l16 == 0) kinv[t] = inv;
+  stream_rows4(Ks, n_loc, ring, full, seq, [&](const int (&t)[4], const bool (&live)[4], const uint4 (&v)[4]) {
+    float n2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) n2[u] = half_butterfly(chunk_sumsq(v[u]));
+    // one sqrt + reciprocal sequence for the half-warp's 4 rows: lane u computes row u
+    const float mine = kd_inv(l16 == 0 ? n2[0] : (l16 == 1 ? n2[1] : (l16 == 2 ? n2[2] : n2[3])));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float inv = __shfl_sync(0xffffffffu, mine, (threadIdx.x & 16) + u);
+      if (live[u]) {
+        kd_fix_add(v[u], __fmul_rn(inv, kKdFx), acc);
+        ++cnt;
+        if (l16 == 0) kinv[t[u]] = inv;
+      }
     }
   });
 #pragma unroll
