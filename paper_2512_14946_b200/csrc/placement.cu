@@ -499,16 +499,40 @@ __device__ __forceinline__ bool key_better(const Key& a, const Key& b) {
   return a.idx < b.idx;
 }
 
+// Warp argmin under key_better's total order as five 32-bit warp reductions
+// (REDUX) over order-preserving key words: drop (IEEE order, -0 folded into
+// +0 like the reference's !=), then bytes (larger first), then idx. Empty
+// keys (idx < 0) map to all-ones and lose to any real key.
 __device__ __forceinline__ Key warp_min(Key k) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    Key o;
-    o.drop = __shfl_xor_sync(0xffffffffu, k.drop, off);
-    o.bytes = __shfl_xor_sync(0xffffffffu, k.bytes, off);
-    o.idx = __shfl_xor_sync(0xffffffffu, k.idx, off);
-    if (key_better(o, k)) k = o;
+  const bool v = k.idx >= 0;
+  unsigned long long a = ~0ull, b = ~0ull;
+  unsigned c = ~0u;
+  if (v) {
+    const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(k.drop, 0.0)));
+    a = (d & 0x8000000000000000ull) ? ~d : (d | 0x8000000000000000ull);
+    b = ~(static_cast<unsigned long long>(k.bytes) ^ 0x8000000000000000ull);
+    c = static_cast<unsigned>(k.idx);
   }
-  return k;
+  const unsigned lane_bit = 1u << (threadIdx.x & 31);
+  unsigned cand = 0xffffffffu;
+  auto step = [&](unsigned x) {
+    const unsigned m = __reduce_min_sync(0xffffffffu, (cand & lane_bit) ? x : ~0u);
+    cand &= __ballot_sync(0xffffffffu, x == m);
+    return m;
+  };
+  const unsigned ah = step(static_cast<unsigned>(a >> 32)), al = step(static_cast<unsigned>(a));
+  const unsigned bh = step(static_cast<unsigned>(b >> 32)), bl = step(static_cast<unsigned>(b));
+  const unsigned cm = step(c);
+  Key r{0.0, 0, -1};
+  if (cm != ~0u) {
+    const unsigned long long ak = (static_cast<unsigned long long>(ah) << 32) | al;
+    const unsigned long long d = (ak & 0x8000000000000000ull) ? (ak & 0x7fffffffffffffffull) : ~ak;
+    r.drop = __longlong_as_double(static_cast<long long>(d));
+    const unsigned long long bk = (static_cast<unsigned long long>(bh) << 32) | bl;
+    r.bytes = static_cast<long long>(~bk ^ 0x8000000000000000ull);
+    r.idx = static_cast<int>(cm);
+  }
+  return r;
 }
 
 // score_candidate proj/src/utility.cpp:65-79 for an arbitrary ratio.
