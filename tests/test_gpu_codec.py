@@ -88,6 +88,23 @@ def test_scores_bitexact(gpu, orc, si, method):
     assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
 
 
+# keydiff prefix lengths: 1 token, 49 rows per cluster CTA, Llama chunk,
+# ragged lengths, 2,048 rows per CTA
+KD_SHAPES = [A.KvShape(1, 2, 1, 128), A.KvShape(2, 3, 385, 128), A.KvShape(1, 3, 8192, 128),
+             A.KvShape(2, 1, 9216, 128), A.KvShape(1, 2, 9217, 128), A.KvShape(3, 2, 4097, 128),
+             A.KvShape(1, 1, 16384, 128), A.KvShape(1, 1, 6657, 128)]
+
+
+@pytest.mark.parametrize("si", range(len(KD_SHAPES)))
+def test_keydiff_lengths_bitexact(gpu, orc, si):
+    s = KD_SHAPES[si]
+    kg, _ = gen(gpu, s)
+    ko, _ = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, "keydiff", 0.3, s)
+    sg, so = scores(gpu, s, cfg, kg, True), scores(orc, s, cfg, ko, False)
+    assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
+
+
 def topk(eng, s, cfg, sc, on_gpu):
     if on_gpu:
         out = torch.empty(s.L * s.H * cfg.keep, dtype=torch.int32, device="cuda")
