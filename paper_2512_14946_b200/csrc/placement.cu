@@ -466,7 +466,9 @@ struct DevStore {
   int* copt;       // enumeration index relative to the resident's tier; -1 none, -2 error
   int* mem;        // tree membership: tier index if in that tier's tree, else -1
   // 32-ary tournament trees, one per tier: tree[t*tree_stride + lvl_off[k] + node]
+  // = winning resident (-1 none), tkey[same] = its (drop, bytes) key words
   int* tree;
+  ulonglong2* tkey;
   int tree_stride;
   int nlev;
   int lvl_off[8];
@@ -499,20 +501,39 @@ __device__ __forceinline__ bool key_better(const Key& a, const Key& b) {
   return a.idx < b.idx;
 }
 
-// Warp argmin under key_better's total order as five 32-bit warp reductions
-// (REDUX) over order-preserving key words: drop (IEEE order, -0 folded into
-// +0 like the reference's !=), then bytes (larger first), then idx. Empty
-// keys (idx < 0) map to all-ones and lose to any real key.
-__device__ __forceinline__ Key warp_min(Key k) {
-  const bool v = k.idx >= 0;
-  unsigned long long a = ~0ull, b = ~0ull;
-  unsigned c = ~0u;
-  if (v) {
-    const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(k.drop, 0.0)));
-    a = (d & 0x8000000000000000ull) ? ~d : (d | 0x8000000000000000ull);
-    b = ~(static_cast<unsigned long long>(k.bytes) ^ 0x8000000000000000ull);
-    c = static_cast<unsigned>(k.idx);
+// Keys as order-preserving unsigned words: a = drop (IEEE order, -0 folded
+// into +0 like the reference's !=), b = bytes freed (larger first), c =
+// index; the empty key (idx < 0) is all-ones and loses to any real key.
+struct WKey {
+  unsigned long long a, b;
+  unsigned c;
+};
+__device__ __forceinline__ WKey wkey_empty() { return WKey{~0ull, ~0ull, ~0u}; }
+__device__ __forceinline__ unsigned long long drop_word(double drop) {
+  const unsigned long long d = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(drop, 0.0)));
+  return (d & 0x8000000000000000ull) ? ~d : (d | 0x8000000000000000ull);
+}
+__device__ __forceinline__ unsigned long long bytes_word(long long bytes) {
+  return ~(static_cast<unsigned long long>(bytes) ^ 0x8000000000000000ull);
+}
+__device__ __forceinline__ WKey to_wkey(const Key& k) {
+  if (k.idx < 0) return wkey_empty();
+  return WKey{drop_word(k.drop), bytes_word(k.bytes), static_cast<unsigned>(k.idx)};
+}
+__device__ __forceinline__ Key from_wkey(const WKey& w) {
+  Key r{0.0, 0, -1};
+  if (w.c != ~0u) {
+    const unsigned long long d = (w.a & 0x8000000000000000ull) ? (w.a & 0x7fffffffffffffffull) : ~w.a;
+    r.drop = __longlong_as_double(static_cast<long long>(d));
+    r.bytes = static_cast<long long>(~w.b ^ 0x8000000000000000ull);
+    r.idx = static_cast<int>(w.c);
   }
+  return r;
+}
+
+// Warp argmin under key_better's total order: five 32-bit warp min
+// reductions (REDUX) over the key words, each narrowing the candidate lanes.
+__device__ __forceinline__ WKey warp_min_w(const WKey& k) {
   const unsigned lane_bit = 1u << (threadIdx.x & 31);
   unsigned cand = 0xffffffffu;
   auto step = [&](unsigned x) {
@@ -520,20 +541,17 @@ __device__ __forceinline__ Key warp_min(Key k) {
     cand &= __ballot_sync(0xffffffffu, x == m);
     return m;
   };
-  const unsigned ah = step(static_cast<unsigned>(a >> 32)), al = step(static_cast<unsigned>(a));
-  const unsigned bh = step(static_cast<unsigned>(b >> 32)), bl = step(static_cast<unsigned>(b));
-  const unsigned cm = step(c);
-  Key r{0.0, 0, -1};
-  if (cm != ~0u) {
-    const unsigned long long ak = (static_cast<unsigned long long>(ah) << 32) | al;
-    const unsigned long long d = (ak & 0x8000000000000000ull) ? (ak & 0x7fffffffffffffffull) : ~ak;
-    r.drop = __longlong_as_double(static_cast<long long>(d));
-    const unsigned long long bk = (static_cast<unsigned long long>(bh) << 32) | bl;
-    r.bytes = static_cast<long long>(~bk ^ 0x8000000000000000ull);
-    r.idx = static_cast<int>(cm);
+  step(static_cast<unsigned>(k.a >> 32));
+  if (__popc(cand) != 1) {  // ties on the high drop word (or no key at all): narrow on the rest
+    step(static_cast<unsigned>(k.a));
+    step(static_cast<unsigned>(k.b >> 32));
+    step(static_cast<unsigned>(k.b));
+    step(k.c);
   }
-  return r;
+  const int src = __ffs(cand) - 1;  // the winner (lowest lane among equal keys: all words equal)
+  return WKey{__shfl_sync(0xffffffffu, k.a, src), __shfl_sync(0xffffffffu, k.b, src), __shfl_sync(0xffffffffu, k.c, src)};
 }
+__device__ __forceinline__ Key warp_min(const Key& k) { return from_wkey(warp_min_w(to_wkey(k))); }
 
 // score_candidate proj/src/utility.cpp:65-79 for an arbitrary ratio.
 __device__ __forceinline__ bool score_fly(const StepCtx& X, int c, int t, int m, double ratio, double* u,
@@ -551,22 +569,44 @@ __device__ __forceinline__ bool score_fly(const StepCtx& X, int c, int t, int m,
 
 // K2: best update of one resident (enumerate_updates proj/src/utility.cpp:
 // 81-127 scored against its current candidate, placement.cpp:179-197).
-// Whole warp; lane 0 writes the cache. Returns the tree membership.
-__device__ int compute_cache(const StepCtx& X, int c, int cur, int me, int re, double rate, long long eorig) {
+// Whole warp; lane 0 writes the cache. Returns the best key (idx = the
+// option's enumeration index, -1 none); *member = the tree membership.
+// Every table load of a step is issued before any of them is consumed.
+__device__ Key compute_cache(const StepCtx& X, int c, int cur, int me, int re, double rate, long long eorig,
+                             int* member = nullptr) {
   const int lane = threadIdx.x & 31;
   const int M = X.S.M, R = X.S.R, T = X.st.TT.T, MR = M * R;
   const size_t qb = static_cast<size_t>(c) * MR;
-  double ucur;
-  long long scur;
-  bool ok;
-  const bool covered = re >= 0 && X.tb.valid[qb + static_cast<size_t>(me) * R + re];
-  if (covered) {
-    ucur = X.tb.u[(static_cast<size_t>(c) * T + cur) * MR + static_cast<size_t>(me) * R + re];
-    scur = X.tb.size[static_cast<size_t>(c) * R + re];
-    ok = true;
-  } else {
-    ok = score_fly(X, c, cur, me, rate, &ucur, &scur);
+  const int per = MR + 1, nj = T - cur;
+  // the (method, ratio) grid in every tier >= cur, option w = lane + 32 q:
+  // its table loads go out first, with the current config's
+  constexpr int kQ = 3, kJ = 4;
+  bool gv[kQ];
+  long long gso[kQ];
+  double gratio[kQ], guo[kQ][kJ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int w = lane + 32 * q;
+    gv[q] = false;
+    if (w < MR) {
+      const int r = w % R;
+      gv[q] = X.tb.valid[qb + w] != 0;
+      gso[q] = X.tb.size[static_cast<size_t>(c) * R + r];
+      gratio[q] = X.S.ratio[r];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j)
+        if (j < nj) guo[q][j] = X.tb.u[(static_cast<size_t>(c) * T + cur + j) * MR + w];
+    }
   }
+  const int rr = re >= 0 ? re : 0;
+  const bool cov_v = X.tb.valid[qb + static_cast<size_t>(me) * R + rr] != 0;
+  const double ucov = X.tb.u[(static_cast<size_t>(c) * T + cur) * MR + static_cast<size_t>(me) * R + rr];
+  const long long scov = X.tb.size[static_cast<size_t>(c) * R + rr];
+  const bool covered = re >= 0 && cov_v;
+  double ucur = ucov;
+  long long scur = scov;
+  bool ok = true;
+  if (!covered) ok = score_fly(X, c, cur, me, rate, &ucur, &scur);
   if (!ok) {
     if (lane == 0) {
       X.st.copt[c] = -2;
@@ -574,45 +614,55 @@ __device__ int compute_cache(const StepCtx& X, int c, int cur, int me, int re, d
       atomicAdd(&X.st.ctl->errcount[cur], 1);
     }
     __syncwarp();
-    return -1;
+    if (member) *member = -1;
+    return Key{0.0, 0, -1};
   }
   const long long cur_bytes = csize(eorig, rate);
-  const bool keep_ok = scorable(X.P, c, me, rate);
-  const int per = MR + 1;
-  const int nopt = (T - cur) * per;
   Key best{0.0, 0, -1};
-  for (int e = lane; e < nopt; e += 32) {
-    const int j = e / per, w = e - j * per, ti = cur + j;
-    double uo;
-    long long so;
-    bool v;
-    if (w < MR) {
-      const int m = w / R, r = w - m * R;
-      v = X.tb.valid[qb + w] != 0;
-      if (v && ti == cur) v = csize(eorig, X.S.ratio[r]) < cur_bytes;
-      if (v) {
-        uo = X.tb.u[(static_cast<size_t>(c) * T + ti) * MR + w];
-        so = X.tb.size[static_cast<size_t>(c) * R + r];
-      }
-    } else {
-      v = ti != cur && !covered && keep_ok;
-      if (v) v = score_fly(X, c, ti, me, rate, &uo, &so);
+  auto consider = [&](const Key& k) {
+    if (key_better(k, best)) best = k;
+  };
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int w = lane + 32 * q;
+    if (w < MR && gv[q]) {
+      const bool shrinks = csize(eorig, gratio[q]) < cur_bytes;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j)
+        if (j < nj && (j > 0 || shrinks)) consider(Key{__dsub_rn(ucur, guo[q][j]), j == 0 ? scur - gso[q] : scur, j * per + w});
+      for (int j = kJ; j < nj; ++j)  // more than kJ tiers below
+        consider(Key{__dsub_rn(ucur, X.tb.u[(static_cast<size_t>(c) * T + cur + j) * MR + w]), scur, j * per + w});
     }
-    if (v) {
-      Key k{__dsub_rn(ucur, uo), ti == cur ? scur - so : scur, e};
-      if (key_better(k, best)) best = k;
+  }
+  for (int w = lane + 32 * kQ; w < MR; w += 32) {  // larger spaces
+    if (X.tb.valid[qb + w] == 0) continue;
+    const int r = w % R;
+    const long long so = X.tb.size[static_cast<size_t>(c) * R + r];
+    const bool shrinks = csize(eorig, X.S.ratio[r]) < cur_bytes;
+    for (int j = 0; j < nj; ++j)
+      if (j > 0 || shrinks)
+        consider(Key{__dsub_rn(ucur, X.tb.u[(static_cast<size_t>(c) * T + cur + j) * MR + w]), j == 0 ? scur - so : scur,
+                     j * per + w});
+  }
+  // keep an off-grid config and move it down a tier (option w = MR)
+  if (lane == MR % 32 && !covered && scorable(X.P, c, me, rate)) {
+    for (int j = 1; j < nj; ++j) {
+      double uo;
+      long long so;
+      if (score_fly(X, c, cur + j, me, rate, &uo, &so)) consider(Key{__dsub_rn(ucur, uo), scur, j * per + MR});
     }
   }
   best = warp_min(best);
-  const int member = best.idx >= 0 ? cur : -1;
+  const int mem = best.idx >= 0 ? cur : -1;
   if (lane == 0) {
     X.st.cdrop[c] = best.drop;
     X.st.cbytes[c] = best.bytes;
     X.st.copt[c] = best.idx;
-    X.st.mem[c] = member;
+    X.st.mem[c] = mem;
   }
   __syncwarp();
-  return member;
+  if (member) *member = mem;
+  return best;
 }
 
 __device__ __forceinline__ Key leaf_key(const DevStore& st, int i, int t) {
@@ -624,35 +674,70 @@ __device__ __forceinline__ Key leaf_key(const DevStore& st, int i, int t) {
   }
   return k;
 }
+// leaf i of tier t's tree; the three loads are issued unconditionally
+__device__ __forceinline__ WKey leaf_wkey(const DevStore& st, int i, int t) {
+  if (i >= st.n) return wkey_empty();
+  const int mem = st.mem[i];
+  const double d = st.cdrop[i];
+  const long long b = st.cbytes[i];
+  return mem == t ? WKey{drop_word(d), bytes_word(b), static_cast<unsigned>(i)} : wkey_empty();
+}
+__device__ __forceinline__ size_t node_at(const DevStore& st, int t, int l, int node) {
+  return static_cast<size_t>(t) * st.tree_stride + st.lvl_off[l] + node;
+}
+__device__ __forceinline__ WKey node_wkey(const DevStore& st, int t, int l, int node) {
+  const size_t at = node_at(st, t, l, node);
+  const ulonglong2 ab = st.tkey[at];
+  return WKey{ab.x, ab.y, static_cast<unsigned>(st.tree[at])};
+}
+__device__ __forceinline__ void node_store(const DevStore& st, int t, int l, int node, const WKey& k) {
+  const size_t at = node_at(st, t, l, node);
+  st.tree[at] = static_cast<int>(k.c);
+  st.tkey[at] = make_ulonglong2(k.a, k.b);
+}
 
-// Recompute the path from leaf c to the root of tier t's tree (whole warp).
-__device__ void tree_update(const DevStore& st, int t, int c) {
+// A leaf-to-root path of one tier's tree: the 31 siblings of every path
+// node, loaded in one round (they do not depend on the new leaf key).
+constexpr int kMaxLev = 6;  // 32^6 residents
+struct TreePath {
+  WKey sib[kMaxLev];
+};
+__device__ __forceinline__ void path_load(const DevStore& st, int t, int c, TreePath& p) {
   const int lane = threadIdx.x & 31;
-  int* tree = st.tree + static_cast<size_t>(t) * st.tree_stride;
   int node = c >> 5;
-  Key k = warp_min(leaf_key(st, (node << 5) + lane, t));
-  if (lane == 0) tree[st.lvl_off[0] + node] = k.idx;
-  __syncwarp();
-  for (int l = 1; l < st.nlev; ++l) {
-    node >>= 5;
-    const int i = (node << 5) + lane;
-    Key kk{0.0, 0, -1};
-    if (i < st.lvl_size[l - 1]) {
-      const int w = tree[st.lvl_off[l - 1] + i];
-      if (w >= 0) {
-        kk.drop = st.cdrop[w];
-        kk.bytes = st.cbytes[w];
-        kk.idx = w;
-      }
+  p.sib[0] = leaf_wkey(st, (node << 5) + lane, t);
+#pragma unroll
+  for (int l = 1; l < kMaxLev; ++l) {
+    if (l < st.nlev) {
+      node >>= 5;
+      const int i = (node << 5) + lane;
+      p.sib[l] = i < st.lvl_size[l - 1] ? node_wkey(st, t, l - 1, i) : wkey_empty();
     }
-    kk = warp_min(kk);
-    if (lane == 0) tree[st.lvl_off[l] + node] = kk.idx;
-    __syncwarp();
   }
+}
+// Recompute the path with leaf c's new key (whole warp); returns the root.
+__device__ __forceinline__ WKey path_finish(const DevStore& st, int t, int c, const TreePath& p, WKey k) {
+  const int lane = threadIdx.x & 31;
+  int child = c;
+#pragma unroll
+  for (int l = 0; l < kMaxLev; ++l) {
+    if (l < st.nlev) {
+      k = warp_min_w(lane == (child & 31) ? k : p.sib[l]);
+      child >>= 5;
+      if (lane == 0) node_store(st, t, l, child, k);
+    }
+  }
+  __syncwarp();
+  return k;
+}
+// leaf c's key in tier t's tree after compute_cache (member = its tree)
+__device__ __forceinline__ WKey member_wkey(const Key& best, int member, int t, int c) {
+  return member == t && best.idx >= 0 ? WKey{drop_word(best.drop), bytes_word(best.bytes), static_cast<unsigned>(c)}
+                                      : wkey_empty();
 }
 
 __device__ __forceinline__ int tree_root(const DevStore& st, int t) {
-  return st.tree[static_cast<size_t>(t) * st.tree_stride + st.lvl_off[st.nlev - 1]];
+  return st.tree[node_at(st, t, st.nlev - 1, 0)];
 }
 
 struct Ops {
@@ -676,6 +761,8 @@ __global__ void __launch_bounds__(32, 1) k_greedy(StepCtx X, Ops ops) {
   long long nact = ctl->n_act, seq = ctl->seq;
   const long long cap_act = ctl->cap_act, n_ops = ctl->n_ops;
   int status = ST_OK, err_ctx = -1, err_tier = -1;
+  // lane t keeps tier t's tree root; this warp is the trees' only writer
+  unsigned root = lane < T && finite ? static_cast<unsigned>(tree_root(st, lane)) : ~0u;
 
   while (true) {
     if (!in_resolve) {
@@ -719,9 +806,15 @@ __global__ void __launch_bounds__(32, 1) k_greedy(StepCtx X, Ops ops) {
       ++seq;
       ++nact;
       __syncwarp();
-      const int member = compute_cache(X, c, b.tier_index, b.method, b.ratio_index, b.ratio, eorig);
-      if (!st.TT.unlimited[b.tier_index]) tree_update(st, b.tier_index, c);
-      (void)member;
+      const bool fin = !st.TT.unlimited[b.tier_index];
+      TreePath path;
+      if (fin) path_load(st, b.tier_index, c, path);
+      int member;
+      const Key k = compute_cache(X, c, b.tier_index, b.method, b.ratio_index, b.ratio, eorig, &member);
+      if (fin) {
+        const WKey r = path_finish(st, b.tier_index, c, path, member_wkey(k, member, b.tier_index, c));
+        if (lane == b.tier_index) root = r.c;
+      }
       in_resolve = true;
     }
     // resolve_overflow: topmost over-full finite tier first (placement.cpp:54-59,211)
@@ -741,7 +834,7 @@ __global__ void __launch_bounds__(32, 1) k_greedy(StepCtx X, Ops ops) {
       err_tier = t;
       break;
     }
-    const int w = tree_root(st, t);
+    const int w = static_cast<int>(__shfl_sync(0xffffffffu, root, t));
     if (w < 0) {
       status = ST_ERR_NO_OPTION;
       err_tier = t;
@@ -791,9 +884,18 @@ __global__ void __launch_bounds__(32, 1) k_greedy(StepCtx X, Ops ops) {
     if (ti != t) ++seq;
     ++nact;
     __syncwarp();
-    compute_cache(X, w, ti, nm, nr, nratio, eorig);
-    tree_update(st, t, w);
-    if (ti != t && !st.TT.unlimited[ti]) tree_update(st, ti, w);
+    const bool fin2 = ti != t && !st.TT.unlimited[ti];
+    TreePath p1, p2;
+    path_load(st, t, w, p1);
+    if (fin2) path_load(st, ti, w, p2);
+    int member;
+    const Key k = compute_cache(X, w, ti, nm, nr, nratio, eorig, &member);
+    const WKey r1 = path_finish(st, t, w, p1, member_wkey(k, member, t, w));
+    if (lane == t) root = r1.c;
+    if (fin2) {
+      const WKey r2 = path_finish(st, ti, w, p2, member_wkey(k, member, ti, w));
+      if (lane == ti) root = r2.c;
+    }
   }
   if (lane < T) ctl->occ[lane] = occ;
   if (lane == 0) {
@@ -836,21 +938,12 @@ __global__ void __launch_bounds__(128) k_tree_level(DevStore st, int lvl, int t0
   const int lane = threadIdx.x & 31;
   const int t = t0 + blockIdx.y;
   if (node >= st.lvl_size[lvl]) return;
-  int* tree = st.tree + static_cast<size_t>(t) * st.tree_stride;
   const int i = (node << 5) + lane;
-  Key k{0.0, 0, -1};
-  if (lvl == 0) {
-    k = leaf_key(st, i, t);
-  } else if (i < st.lvl_size[lvl - 1]) {
-    const int w = tree[st.lvl_off[lvl - 1] + i];
-    if (w >= 0) {
-      k.drop = st.cdrop[w];
-      k.bytes = st.cbytes[w];
-      k.idx = w;
-    }
-  }
-  k = warp_min(k);
-  if (lane == 0) tree[st.lvl_off[lvl] + node] = k.idx;
+  WKey k = wkey_empty();
+  if (lvl == 0) k = leaf_wkey(st, i, t);
+  else if (i < st.lvl_size[lvl - 1]) k = node_wkey(st, t, lvl - 1, i);
+  k = warp_min_w(k);
+  if (lane == 0) node_store(st, t, lvl, node, k);
 }
 
 // Direct StoreState edits (placement.cpp:91-142); one thread.
@@ -1077,7 +1170,8 @@ extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_
   const size_t o_tier = carve(4 * n), o_meth = carve(4 * n), o_ridx = carve(4 * n), o_ratio = carve(8 * n),
                o_orig = carve(8 * n), o_freq = carve(8 * n), o_last = carve(8 * n), o_seq = carve(8 * n),
                o_cdrop = carve(8 * n), o_cbytes = carve(8 * n), o_copt = carve(4 * n), o_mem = carve(4 * n),
-               o_tree = carve(4 * static_cast<size_t>(off) * T.T), o_ctl = carve(sizeof(Ctl)),
+               o_tree = carve(4 * static_cast<size_t>(off) * T.T),
+               o_tkey = carve(sizeof(ulonglong2) * static_cast<size_t>(off) * T.T), o_ctl = carve(sizeof(Ctl)),
                o_saved = carve(4 * n);
   cudaError_t e = cudaMalloc(&s->buf, o);
   if (e != cudaSuccess) {
@@ -1098,6 +1192,7 @@ extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_
   d.copt = reinterpret_cast<int*>(b + o_copt);
   d.mem = reinterpret_cast<int*>(b + o_mem);
   d.tree = reinterpret_cast<int*>(b + o_tree);
+  d.tkey = reinterpret_cast<ulonglong2*>(b + o_tkey);
   d.ctl = reinterpret_cast<Ctl*>(b + o_ctl);
   d.saved = reinterpret_cast<int*>(b + o_saved);
   cudaStream_t st = h->stream;
@@ -1106,6 +1201,7 @@ extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_
   cudaMemsetAsync(d.mem, 0xff, 4 * n, st);
   cudaMemsetAsync(d.copt, 0xff, 4 * n, st);
   cudaMemsetAsync(d.tree, 0xff, 4 * static_cast<size_t>(off) * T.T, st);
+  cudaMemsetAsync(d.tkey, 0xff, sizeof(ulonglong2) * static_cast<size_t>(off) * T.T, st);
   s->cap_act = 4096;
   e = cudaMalloc(&s->act, sizeof(kvt_action) * s->cap_act);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1227,6 +1323,8 @@ extern "C" int kvt_store_clear(kvt_store* s) {
   s->h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
   KVT_CUDA_TRY(cudaMemsetAsync(s->d.tree, 0xff, 4 * static_cast<size_t>(s->d.tree_stride) * s->TT.T, s->h->stream));
+  KVT_CUDA_TRY(cudaMemsetAsync(s->d.tkey, 0xff, sizeof(ulonglong2) * static_cast<size_t>(s->d.tree_stride) * s->TT.T,
+                               s->h->stream));
   KVT_CUDA_TRY(cudaStreamSynchronize(s->h->stream));
   return KVT_OK;
 }
@@ -1521,6 +1619,7 @@ extern "C" int kvt_rearrange(kvt_store* s, const kvt_pset* p, const kvt_space* s
   k_clear<<<(s->n + 255) / 256 + 1, 256, 0, st>>>(s->d);
   s->h->launches++;
   KVT_CUDA_TRY(cudaMemsetAsync(s->d.tree, 0xff, 4 * static_cast<size_t>(s->d.tree_stride) * s->TT.T, st));
+  KVT_CUDA_TRY(cudaMemsetAsync(s->d.tkey, 0xff, sizeof(ulonglong2) * static_cast<size_t>(s->d.tree_stride) * s->TT.T, st));
   KVT_CUDA_TRY(cudaGetLastError());
   Ops ops{s->d.saved, nullptr, nullptr};
   if (n_saved == 0) return KVT_OK;
