@@ -798,7 +798,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   cluster_sync_smem();
   if (cworker) {
     int32_t m = INT_MIN;
-    for (int c = cq; c < C; c += 4) m = max(m, cl.map_shared_rank(xs.mloc, c)[crow]);
+#pragma unroll
+    for (int i = 0; i < kSnapMaxC / 4; ++i)  // the <= 4 remote reads in flight together
+      if (cq + 4 * i < C) m = max(m, cl.map_shared_rank(xs.mloc, cq + 4 * i)[crow]);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
     unsigned long long Ls = 0;
@@ -816,7 +818,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   cluster_sync_smem();
   if (cworker) {
     unsigned long long Ls = 0;
-    for (int c = cq; c < C; c += 4) Ls += cl.map_shared_rank(xs.lloc, c)[crow];
+#pragma unroll
+    for (int i = 0; i < kSnapMaxC / 4; ++i)
+      if (cq + 4 * i < C) Ls += cl.map_shared_rank(xs.lloc, cq + 4 * i)[crow];
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
     Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
     const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
@@ -826,8 +830,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
     }
   }
-  // every peer has read this CTA's mloc / lloc before the votes overwrite them
-  cluster_sync_smem();
+  // (no cluster barrier here: the votes write vote / part, never the mloc / lloc
+  // peers may still be reading; the halo barrier below keeps every CTA alive
+  // until all peers are past those reads)
+  __syncthreads();  // this CTA's block weights (lb) complete before the votes
   // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows (rq 0, 1; rq 2 idles);
   // TPC / 4 rounds of 256 pairs; rows >= R have zero weight
   for (int round = 0; round < TPC / 4; ++round) {
