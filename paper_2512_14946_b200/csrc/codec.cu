@@ -612,12 +612,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
     k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, uint8_t* __restrict__ escr,
-                float* __restrict__ scores, int T, int W, int G, int pool, int tpc) {
+                float* __restrict__ scores, int T, int W, int G, int pool, int tpc, int nslice) {
   using SnapSmem = SnapSmemT<TPC, EG>;
   using SnapScratch = SnapScratchT<TPC>;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
-  const int slice = blockIdx.y;
   const int P = T - W, R = W * G;
   const int ntiles = (P + 127) / 128;
   const int tile0 = rank * tpc, ntl = max(0, min(tpc, ntiles - tile0));
@@ -627,7 +626,6 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   extern __shared__ __align__(16) uint8_t snap_raw[];
   // 1024-align by offset (keeps the shared address space visible: LDS/STS, not generic LD/ST)
   SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + ((1024u - (smem_u32(snap_raw) & 1023u)) & 1023u));
-  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
   uint16_t* Eg = nullptr;  // EG: E[r][t] at Eg[r * TPC * 128 + t] (this SM's slot; one CTA per SM)
   if (EG) {
     uint32_t smid;
@@ -650,6 +648,11 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  // persistent clusters: this cluster's slices blockIdx.y, + gridDim.y, ...;
+  // mbarrier phases run on across slices (g = this CTA's tile count)
+  for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
+  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+  const int g0 = it * ntl;
   if (tid == 0) {
     mbar_expect_tx(&sm.qbar, kSnapQBytes);
     bulk_g2s(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar);
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       bulk_g2s(sm.stage, Ks, rows * 256, &sm.full);
     }
   }
-  mbar_wait(&sm.qbar, 0);
+  mbar_wait(&sm.qbar, it & 1);
 
   if (warp < kSnapProd) {
     // ================= producers: absmax, int8 quantisation, MMA issue
@@ -669,9 +672,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     const int ptid = tid;  // rows ptid/4 + (kSnapProd * 8) * i, 32-channel quarter ptid & 3
     const int q4 = ptid & 3, rbase = ptid >> 2;
     for (int j = 0; j < ntl; ++j) {
-      const int buf = j & 1;
+      const int g = g0 + j, buf = g & 1;
       const int rows = min(128, n_loc - j * 128);
-      mbar_wait(&sm.full, j & 1);
+      mbar_wait(&sm.full, g & 1);
       uint4 v[kRowsPT][4];
 #pragma unroll
       for (int i = 0; i < kRowsPT; ++i) {
@@ -704,7 +707,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       const float Af = bf2f(mx);
       const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
       if (ptid == 0) sm.tau[j] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;
-      if (j >= 2) mbar_wait(&sm.tfull[buf], ((j >> 1) - 1) & 1);  // MMA of tile j - 2 done reading k8[buf]
+      if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
       uint8_t* k8 = sm.k8[buf];
 #pragma unroll
       for (int i = 0; i < kRowsPT; ++i) {
@@ -733,7 +736,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       named_bar_sync(1, kSnapProd * 32);
       if (ptid == 0) {
-        if (j >= 2) mbar_wait(&sm.tempty[buf], ((j >> 1) - 1) & 1);  // consumers drained acc[buf]
+        if (g >= 2) mbar_wait(&sm.tempty[buf], ((g >> 1) - 1) & 1);  // consumers drained acc[buf]
         tc_fence_after();
         mbar_arrive(&sm.tfull[buf]);  // release: sm.tau[j] visible to the consumers
         const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
@@ -749,8 +752,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     const int r = quad * 32 + lane;
     const float sig_r = sm.sig[r];
     for (int j = 0; j < ntl; ++j) {
-      const int buf = j & 1;
-      mbar_wait(&sm.tfull[buf], (j >> 1) & 1);
+      const int g = g0 + j, buf = g & 1;
+      mbar_wait(&sm.tfull[buf], (g >> 1) & 1);
       tc_fence_after();
       uint32_t I[32];
       tmem_ld32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + cb * 32, I);
@@ -890,6 +893,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   }
   if (rank == C - 1)
     for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
+  __syncthreads();  // scratch (stage), E, mb / lb free for the next slice
+  }
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
@@ -971,8 +976,20 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  {  // persistent: as many clusters as fit at once, each loops over slices
+    static int active[2][kSnapMaxC + 1] = {};
+    int& na = active[eg][Cn];
+    if (!na) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = S;
+      na = n;
+    }
+    const char* ge = getenv("KVT_SNAP_GRID");  // experiments: force the number of clusters
+    const int ng = ge && *ge ? atoi(ge) : na;
+    cfg.gridDim = dim3(Cn, std::max(1, std::min(S, ng)));
+  }
   KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(k), static_cast<const uint8_t*>(qbuf), escr,
-                                  scores, T, W, G, c->pool, tpc));
+                                  scores, T, W, G, c->pool, tpc, S));
   LAUNCHED(h);
   return KVT_OK;
 }
