@@ -32,6 +32,15 @@ namespace cg = cooperative_groups;
 
 
 static int g_num_sms = 0;
+static int smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return v;
+}
 static int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
@@ -475,24 +484,23 @@ template <int TPC, bool EG>
 struct SnapSmemT {
   uint8_t k8[2][128 * 128];  // offset 0 of the 1024-aligned base; double-buffered
   uint8_t q8[128 * 128];
-  uint4 stage[128 * 16];     // one bf16 tile (32 KB); after the tile loop: combine scratch + votes
+  uint4 stage[128 * 16];     // one bf16 tile (32 KB), producers only
   uint8_t e[EG ? 16 : 128 * 1024];
-  int32_t mb[TPC * 4][128];   // per (block, row) shift M
+  union {
+    int32_t mb[TPC * 4][128];             // per (block, row) shift M
+    unsigned long long vote[TPC * 128];   // after the block weights: per-token votes
+  };
   uint32_t lb[TPC * 4][128];  // per (block, row) sum of E, then the block weight
+  unsigned long long lloc[128];
+  int32_t mloc[128];
+  unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
   float sig[128];
-  float tau[TPC];
+  float tau[4];  // per-tile scale, ring over the CTA's tile count
   uint32_t amax[kSnapProd];
   uint64_t full, qbar, tfull[2], tempty[2];
+  uint64_t rb[3];  // cluster rounds of the tail (row shifts, row sums, halos): one arrival per CTA
   uint32_t tmem_base;
 };
-template <int TPC>
-struct SnapScratchT {  // aliases SnapSmemT::stage after the tile loop
-  unsigned long long vote[TPC * 128];
-  unsigned long long lloc[128];
-  int32_t mloc[128], mrow[128];
-  unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
-};
-static_assert(sizeof(SnapScratchT<kSnapTpcGlobal>) <= 128 * 16 * sizeof(uint4), "scratch fits the stage");
 
 __device__ __forceinline__ uint32_t snap_e_off(int r, int byte) {  // swizzled byte offset of E[r][byte / 2]
   return static_cast<uint32_t>(r) * 1024u + ((((byte >> 4) ^ r) & 7) | ((byte >> 4) & ~7)) * 16u + (byte & 15);
@@ -612,9 +620,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
     k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, uint8_t* __restrict__ escr,
-                float* __restrict__ scores, int T, int W, int G, int pool, int tpc, int nslice) {
+                float* __restrict__ scores, int T, int W, int G, int pool, int tpc, int nslice, int slack) {
   using SnapSmem = SnapSmemT<TPC, EG>;
-  using SnapScratch = SnapScratchT<TPC>;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int P = T - W, R = W * G;
@@ -625,7 +632,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   extern __shared__ __align__(16) uint8_t snap_raw[];
   // 1024-align by offset (keeps the shared address space visible: LDS/STS, not generic LD/ST)
-  SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + ((1024u - (smem_u32(snap_raw) & 1023u)) & 1023u));
+  const uint32_t align_off = (1024u - (smem_u32(snap_raw) & 1023u)) & 1023u;
+  if (align_off > static_cast<uint32_t>(slack)) __trap();  // the launch reserved less than the misalignment
+  SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + align_off);
   uint16_t* Eg = nullptr;  // EG: E[r][t] at Eg[r * TPC * 128 + t] (this SM's slot; one CTA per SM)
   if (EG) {
     uint32_t smid;
@@ -641,260 +650,276 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     mbar_init(&sm.tfull[1], 2);
     mbar_init(&sm.tempty[0], kSnapCons);
     mbar_init(&sm.tempty[1], kSnapCons);
+    for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], C);
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_smem();  // every CTA's round barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  // persistent clusters: this cluster's slices blockIdx.y, + gridDim.y, ...;
-  // mbarrier phases run on across slices (g = this CTA's tile count)
-  for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
-  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
-  const int g0 = it * ntl;
-  if (tid == 0) {
-    mbar_expect_tx(&sm.qbar, kSnapQBytes);
-    bulk_g2s(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar);
-    bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
-    if (ntl > 0) {
-      const int rows = min(128, n_loc);
-      mbar_expect_tx(&sm.full, rows * 256);
-      bulk_g2s(sm.stage, Ks, rows * 256, &sm.full);
-    }
-  }
-  mbar_wait(&sm.qbar, it & 1);
 
+  // Persistent clusters: this cluster's slices are blockIdx.y, + gridDim.y, ...
+  // The producers run ahead into the next slice (Q8 + first tiles into TMEM)
+  // while the consumers do this slice's tail; mbarrier phases run on across
+  // slices (g = this CTA's tile count, it = its slice count).
   if (warp < kSnapProd) {
     // ================= producers: absmax, int8 quantisation, MMA issue
     constexpr uint32_t kIdesc = idesc_i8(128, 128);
     constexpr int kRowsPT = 128 * 4 / (kSnapProd * 32);  // rows per producer thread
     const int ptid = tid;  // rows ptid/4 + (kSnapProd * 8) * i, 32-channel quarter ptid & 3
     const int q4 = ptid & 3, rbase = ptid >> 2;
-    for (int j = 0; j < ntl; ++j) {
-      const int g = g0 + j, buf = g & 1;
-      const int rows = min(128, n_loc - j * 128);
-      mbar_wait(&sm.full, g & 1);
-      uint4 v[kRowsPT][4];
-#pragma unroll
-      for (int i = 0; i < kRowsPT; ++i) {
-        const int row = rbase + kSnapProd * 8 * i;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[i][u] = row < rows ? sm.stage[row * 16 + q4 * 4 + u] : make_uint4(0, 0, 0, 0);
-      }
-      uint32_t mx2 = 0;
-#pragma unroll
-      for (int i = 0; i < kRowsPT; ++i)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          mx2 = __vmaxu2(mx2, v[i][u].x & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i][u].y & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i][u].z & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i][u].w & 0x7fff7fffu);
-        }
-      const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
-      if (lane == 0) sm.amax[warp] = wmx;
-      named_bar_sync(1, kSnapProd * 32);  // stage consumed into registers, amax complete
-      if (ptid == 0 && j + 1 < ntl) {  // prefetch the next tile
-        const int nrows = min(128, n_loc - (j + 1) * 128);
+    for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
+      const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
+      const int g0 = it * ntl;
+      if (ptid == 0 && ntl > 0) {
+        // q8 / sig are free once the previous slice's last MMA has completed
+        if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) & 1], ((g0 - 1) >> 1) & 1);
+        mbar_expect_tx(&sm.qbar, kSnapQBytes);
+        bulk_g2s(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar);
+        bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
+        const int rows = min(128, n_loc);
         fence_async_smem();
-        mbar_expect_tx(&sm.full, nrows * 256);
-        bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+        mbar_expect_tx(&sm.full, rows * 256);
+        bulk_g2s(sm.stage, Ks, rows * 256, &sm.full);
       }
-      uint32_t mx = 0;
+      for (int j = 0; j < ntl; ++j) {
+        const int g = g0 + j, buf = g & 1;
+        const int rows = min(128, n_loc - j * 128);
+        mbar_wait(&sm.full, g & 1);
+        uint4 v[kRowsPT][4];
 #pragma unroll
-      for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
-      const float Af = bf2f(mx);
-      const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
-      if (ptid == 0) sm.tau[j] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;
-      if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
-      uint8_t* k8 = sm.k8[buf];
+        for (int i = 0; i < kRowsPT; ++i) {
+          const int row = rbase + kSnapProd * 8 * i;
 #pragma unroll
-      for (int i = 0; i < kRowsPT; ++i) {
-        const int row = rbase + kSnapProd * 8 * i;
-        uint32_t wq[8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t ww[4] = {v[i][u].x, v[i][u].y, v[i][u].z, v[i][u].w};
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            // rint of the exact product x * inv (fused rounding, oracle quant_i8)
-            const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
-                                         make_float2(12582912.0f, 12582912.0f));
-            const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])),
-                                         make_float2(inv, inv), make_float2(12582912.0f, 12582912.0f));
-            const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
-            const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
-            wq[2 * u + h2] = __byte_perm(lo, hi, 0x5410);
-          }
+          for (int u = 0; u < 4; ++u) v[i][u] = row < rows ? sm.stage[row * 16 + q4 * 4 + u] : make_uint4(0, 0, 0, 0);
         }
-        const int c0 = q4 * 2;  // 16-byte chunks c0, c0 + 1 of the row (SW128 K-major)
-        *reinterpret_cast<uint4*>(k8 + row * 128 + ((c0 ^ (row & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
-        *reinterpret_cast<uint4*>(k8 + row * 128 + (((c0 + 1) ^ (row & 7)) << 4)) =
-            make_uint4(wq[4], wq[5], wq[6], wq[7]);
-      }
-      fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-      named_bar_sync(1, kSnapProd * 32);
-      if (ptid == 0) {
-        if (g >= 2) mbar_wait(&sm.tempty[buf], ((g >> 1) - 1) & 1);  // consumers drained acc[buf]
-        tc_fence_after();
-        mbar_arrive(&sm.tfull[buf]);  // release: sm.tau[j] visible to the consumers
-        const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
+        uint32_t mx2 = 0;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
-        umma_commit(&sm.tfull[buf]);
+        for (int i = 0; i < kRowsPT; ++i)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            mx2 = __vmaxu2(mx2, v[i][u].x & 0x7fff7fffu);
+            mx2 = __vmaxu2(mx2, v[i][u].y & 0x7fff7fffu);
+            mx2 = __vmaxu2(mx2, v[i][u].z & 0x7fff7fffu);
+            mx2 = __vmaxu2(mx2, v[i][u].w & 0x7fff7fffu);
+          }
+        const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
+        if (lane == 0) sm.amax[warp] = wmx;
+        named_bar_sync(1, kSnapProd * 32);  // stage consumed into registers, amax complete
+        if (ptid == 0 && j + 1 < ntl) {  // prefetch the next tile
+          const int nrows = min(128, n_loc - (j + 1) * 128);
+          fence_async_smem();
+          mbar_expect_tx(&sm.full, nrows * 256);
+          bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+        }
+        uint32_t mx = 0;
+#pragma unroll
+        for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
+        const float Af = bf2f(mx);
+        const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
+        if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
+        if (ptid == 0) sm.tau[g & 3] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;  // tile g - 4 long consumed
+        uint8_t* k8 = sm.k8[buf];
+#pragma unroll
+        for (int i = 0; i < kRowsPT; ++i) {
+          const int row = rbase + kSnapProd * 8 * i;
+          uint32_t wq[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t ww[4] = {v[i][u].x, v[i][u].y, v[i][u].z, v[i][u].w};
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              // rint of the exact product x * inv (fused rounding, oracle quant_i8)
+              const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
+                                           make_float2(12582912.0f, 12582912.0f));
+              const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])),
+                                           make_float2(inv, inv), make_float2(12582912.0f, 12582912.0f));
+              const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
+              const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
+              wq[2 * u + h2] = __byte_perm(lo, hi, 0x5410);
+            }
+          }
+          const int c0 = q4 * 2;  // 16-byte chunks c0, c0 + 1 of the row (SW128 K-major)
+          *reinterpret_cast<uint4*>(k8 + row * 128 + ((c0 ^ (row & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+          *reinterpret_cast<uint4*>(k8 + row * 128 + (((c0 + 1) ^ (row & 7)) << 4)) =
+              make_uint4(wq[4], wq[5], wq[6], wq[7]);
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        named_bar_sync(1, kSnapProd * 32);
+        if (ptid == 0) {
+          if (j == 0) mbar_wait(&sm.qbar, it & 1);  // this slice's Q8 tile landed
+          if (g >= 2) mbar_wait(&sm.tempty[buf], ((g >> 1) - 1) & 1);  // consumers drained acc[buf]
+          tc_fence_after();
+          mbar_arrive(&sm.tfull[buf]);  // release: sm.tau visible to the consumers
+          const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
+          umma_commit(&sm.tfull[buf]);
+        }
       }
     }
   } else {
-    // ================= consumers: row r, tokens 128j + 32cb .. +31
+    // ================= consumers: epilogue of every tile, then the slice's tail
+    const int ctid = tid - kSnapProd * 32;  // 0 .. 511
     const int cw = warp - kSnapProd;
     const int quad = cw & 3, cb = cw >> 2;  // TMEM lane quadrant (warp % 4 == cw % 4), 32-token block
     const int r = quad * 32 + lane;
-    const float sig_r = sm.sig[r];
-    for (int j = 0; j < ntl; ++j) {
-      const int g = g0 + j, buf = g & 1;
-      mbar_wait(&sm.tfull[buf], (g >> 1) & 1);
-      tc_fence_after();
-      uint32_t I[32];
-      tmem_ld32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + cb * 32, I);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile j + 2 may overwrite it
-      const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
-      int32_t M = INT_MIN;
-      uint32_t L = 0;
-      uint32_t pk[16];
-      if (r < R && nv > 0) {
-        const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(sm.tau[j], sig_r), kSnapC0)) & ~3u);
-        L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
-      } else {
+    const int crow = (ctid >> 2) & 127, cq = ctid & 3;  // tail: 4 threads per row, blocks split 4 ways
+    constexpr int kCT = kSnapCons * 32;
+    for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
+      const int g0 = it * ntl;
+      // the producers wait for this slice's Q8 before its first MMA, so sig is
+      // in place once tile g0's accumulator is (ntl == 0: the tail reads no sig)
+      float sig_r = 0.0f;
+      for (int j = 0; j < ntl; ++j) {
+        const int g = g0 + j, buf = g & 1;
+        mbar_wait(&sm.tfull[buf], (g >> 1) & 1);
+        tc_fence_after();
+        if (j == 0) sig_r = sm.sig[r];
+        uint32_t I[32];
+        tmem_ld32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + cb * 32, I);
+        const float tau = sm.tau[g & 3];
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile g + 2 may overwrite it
+        const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
+        int32_t M = INT_MIN;
+        uint32_t L = 0;
+        uint32_t pk[16];
+        if (r < R && nv > 0) {
+          const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
+          L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = 0;
+          for (int i = 0; i < 16; ++i) pk[i] = 0;
+        }
+        if (EG) {
+          uint4* erow = reinterpret_cast<uint4*>(Eg + r * (TPC * 128) + tok0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) __stcg(erow + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
+                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+        sm.mb[j * 4 + cb][r] = M;
+        sm.lb[j * 4 + cb][r] = L;
       }
-      if (EG) {
-        uint4* erow = reinterpret_cast<uint4*>(Eg + r * (TPC * 128) + tok0);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) __stcg(erow + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
-              make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-      }
-      sm.mb[j * 4 + cb][r] = M;
-      sm.lb[j * 4 + cb][r] = L;
-    }
-  }
-  __syncthreads();  // all tiles done; stage is free
+      named_bar_sync(2, kCT);  // every tile's E, mb, lb in place
 
-  SnapScratch& xs = *reinterpret_cast<SnapScratch*>(sm.stage);
-  // ---- row shift and sum across the cluster (4 threads per row, blocks split 4 ways)
-  const int crow = (tid >> 2) & 127, cq = tid & 3;
-  const bool cworker = tid < 512;
-  if (cworker) {
-    int32_t m = INT_MIN;
-    for (int b = cq; b < nblk; b += 4) m = max(m, sm.mb[b][crow]);
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-    if (cq == 0) xs.mloc[crow] = m;
-  }
-  cluster_sync_smem();
-  if (cworker) {
-    int32_t m = INT_MIN;
+      // ---- row shift and sum across the cluster: three rounds signalled with
+      // one remote mbarrier arrive per CTA (consumers only; the producers
+      // are already on the next slice)
+      auto round_arrive = [&](int k) {
+        named_bar_sync(2, kCT);  // this CTA's round-k data written
+        if (ctid < C) {  // one arrive per peer, issued in parallel
+          fence_acq_rel_cluster();
+          mbar_arrive_remote(&sm.rb[k], static_cast<uint32_t>(ctid));
+        }
+        mbar_wait_cluster(&sm.rb[k], it & 1);  // every CTA's round-k data visible
+      };
+      {
+        int32_t m = INT_MIN;
+        for (int b = cq; b < nblk; b += 4) m = max(m, sm.mb[b][crow]);
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        if (cq == 0) sm.mloc[crow] = m;
+      }
+      round_arrive(0);
+      int32_t mrow = INT_MIN;
 #pragma unroll
-    for (int i = 0; i < kSnapMaxC / 4; ++i)  // the <= 4 remote reads in flight together
-      if (cq + 4 * i < C) m = max(m, cl.map_shared_rank(xs.mloc, cq + 4 * i)[crow]);
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-    unsigned long long Ls = 0;
-    for (int b = cq; b < nblk; b += 4) {
-      const int64_t sh = int64_t(m) - sm.mb[b][crow];
-      if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][crow]) << 16) >> sh;
-    }
-    Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
-    Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
-    if (cq == 0) {
-      xs.mrow[crow] = m;
-      xs.lloc[crow] = Ls;
-    }
-  }
-  cluster_sync_smem();
-  if (cworker) {
-    unsigned long long Ls = 0;
+      for (int i = 0; i < kSnapMaxC / 4; ++i)  // the <= 4 remote reads in flight together
+        if (cq + 4 * i < C) mrow = max(mrow, cl.map_shared_rank(sm.mloc, cq + 4 * i)[crow]);
+      mrow = max(mrow, __shfl_xor_sync(0xffffffffu, mrow, 1));
+      mrow = max(mrow, __shfl_xor_sync(0xffffffffu, mrow, 2));
+      {
+        unsigned long long Ls = 0;
+        for (int b = cq; b < nblk; b += 4) {
+          const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
+          if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][crow]) << 16) >> sh;
+        }
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+        if (cq == 0) sm.lloc[crow] = Ls;
+      }
+      round_arrive(1);
+      {
+        unsigned long long Ls = 0;
 #pragma unroll
-    for (int i = 0; i < kSnapMaxC / 4; ++i)
-      if (cq + 4 * i < C) Ls += cl.map_shared_rank(xs.lloc, cq + 4 * i)[crow];
-    Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
-    Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
-    const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
-    const int32_t m = xs.mrow[crow];
-    for (int b = cq; b < nblk; b += 4) {
-      const int64_t sh = int64_t(m) - sm.mb[b][crow];
-      sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
-    }
-  }
-  // (no cluster barrier here: the votes write vote / part, never the mloc / lloc
-  // peers may still be reading; the halo barrier below keeps every CTA alive
-  // until all peers are past those reads)
-  __syncthreads();  // this CTA's block weights (lb) complete before the votes
-  // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows (rq 0, 1; rq 2 idles);
-  // TPC / 4 rounds of 256 pairs; rows >= R have zero weight
-  for (int round = 0; round < TPC / 4; ++round) {
-    const int p = (tid % 256) + 256 * round, rq = tid / 256;
-    unsigned long long a0 = 0, a1 = 0;
-    if (rq < 2 && 2 * p < n_loc) {
-      const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
-#pragma unroll 4
-      for (int r0 = 0; r0 < 64; r0 += 4) {
-        const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
-        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = rq * 64 + r0 + q;
-          const uint32_t e2 = EG ? __ldcg(reinterpret_cast<const uint32_t*>(Eg + r * (TPC * 128)) + p)
-                                 : *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(r, 4 * p));
-          a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
-          a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+        for (int i = 0; i < kSnapMaxC / 4; ++i)
+          if (cq + 4 * i < C) Ls += cl.map_shared_rank(sm.lloc, cq + 4 * i)[crow];
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
+        Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+        const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
+        for (int b = cq; b < nblk; b += 4) {
+          const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
+          sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
         }
       }
+      named_bar_sync(2, kCT);  // block weights complete; mb dead (vote reuses it)
+      // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows (rq 0, 1);
+      // TPC / 4 rounds of 256 pairs; rows >= R have zero weight
+      for (int round = 0; round < TPC / 4; ++round) {
+        const int p = (ctid % 256) + 256 * round, rq = ctid / 256;
+        unsigned long long a0 = 0, a1 = 0;
+        if (2 * p < n_loc) {
+          const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
+#pragma unroll 4
+          for (int r0 = 0; r0 < 64; r0 += 4) {
+            const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
+            const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int rr = rq * 64 + r0 + q;
+              const uint32_t e2 = EG ? __ldcg(reinterpret_cast<const uint32_t*>(Eg + rr * (TPC * 128)) + p)
+                                     : *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(rr, 4 * p));
+              a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
+              a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+            }
+          }
+        }
+        if (rq == 1) {
+          sm.vote[2 * p] = a0;
+          sm.vote[2 * p + 1] = a1;
+        }
+        named_bar_sync(2, kCT);
+        if (rq == 0) {
+          sm.vote[2 * p] += a0;
+          sm.vote[2 * p + 1] += a1;
+        }
+      }
+      named_bar_sync(2, kCT);  // votes complete
+      // push this CTA's boundary votes into the neighbours' halos (non-last CTAs are full: n_loc = tpc * 128)
+      const int half = pool / 2;
+      if (ctid < half) {
+        if (rank > 0 && ctid < n_loc) cl.map_shared_rank(sm.rhalo, rank - 1)[ctid] = sm.vote[ctid];
+        if (rank < C - 1) cl.map_shared_rank(sm.lhalo, rank + 1)[ctid] = sm.vote[n_loc - half + ctid];
+      }
+      round_arrive(2);  // halos in place
+      // ---- pooling (max over +-pool/2 within the prefix) and scores
+      float* out = scores + static_cast<size_t>(slice) * T;
+      for (int tl = ctid; tl < n_loc; tl += kCT) {
+        unsigned long long m = 0;
+        for (int dj = -half; dj <= half; ++dj) {
+          const int tg = t_lo + tl + dj;  // global prefix token
+          if (tg < 0 || tg >= P) continue;
+          const int li = tl + dj;
+          const unsigned long long x = li < 0 ? sm.lhalo[li + half] : (li >= n_loc ? sm.rhalo[li - n_loc] : sm.vote[li]);
+          m = x > m ? x : m;
+        }
+        out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 2.8421709430404007e-14f);  // 2^-45 (exact)
+      }
+      if (rank == C - 1)
+        for (int t = P + ctid; t < T; t += kCT) out[t] = INFINITY;  // window tokens always kept
+      named_bar_sync(2, kCT);  // vote / halos / E / mb / lb free for the next slice
     }
-    unsigned long long* part = reinterpret_cast<unsigned long long*>(sm.k8);  // K8 no longer needed
-    if (rq == 1) {
-      part[2 * (p % 256)] = a0;
-      part[2 * (p % 256) + 1] = a1;
-    }
-    __syncthreads();
-    if (rq == 0) {
-      xs.vote[2 * p] = a0 + part[2 * (p % 256)];
-      xs.vote[2 * p + 1] = a1 + part[2 * (p % 256) + 1];
-    }
-    __syncthreads();
   }
-  // push this CTA's boundary votes into the neighbours' halos (non-last CTAs are full: n_loc = tpc * 128)
-  const int half = pool / 2;
-  if (tid < half) {
-    if (rank > 0 && tid < n_loc) cl.map_shared_rank(xs.rhalo, rank - 1)[tid] = xs.vote[tid];
-    if (rank < C - 1) cl.map_shared_rank(xs.lhalo, rank + 1)[tid] = xs.vote[n_loc - half + tid];
-  }
-  // halos visible; after this barrier no CTA touches another's smem, so CTAs retire independently
+  // Peers' remote arrives and DSMEM reads of this CTA's smem are all done
+  // once every CTA's consumers are past their last round.
+  tc_fence_before();
   cluster_sync_smem();
-  // ---- pooling (max over +-pool/2 within the prefix) and scores
-  float* out = scores + static_cast<size_t>(slice) * T;
-  for (int tl = tid; tl < n_loc; tl += kSnapThreads) {
-    unsigned long long m = 0;
-    for (int dj = -half; dj <= half; ++dj) {
-      const int tg = t_lo + tl + dj;  // global prefix token
-      if (tg < 0 || tg >= P) continue;
-      const int li = tl + dj;
-      const unsigned long long x = li < 0 ? xs.lhalo[li + half] : (li >= n_loc ? xs.rhalo[li - n_loc] : xs.vote[li]);
-      m = x > m ? x : m;
-    }
-    out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 2.8421709430404007e-14f);  // 2^-45 (exact)
-  }
-  if (rank == C - 1)
-    for (int t = P + tid; t < T; t += kSnapThreads) out[t] = INFINITY;  // window tokens always kept
-  __syncthreads();  // scratch (stage), E, mb / lb free for the next slice
-  }
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
@@ -925,7 +950,11 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   if (Cn > kSnapMaxC)
     return set_error(KVT_EINVAL, "snapkv: prefix (T - window) longer than 32768 tokens is not supported");
   const int tpc = (ntiles + Cn - 1) / Cn;
-  const size_t smem = (eg ? sizeof(SnapSmemT<kSnapTpcGlobal, true>) : sizeof(SnapSmemT<kSnapTpcSmem, false>)) + 1024;
+  // room for 1024-aligning the base: what is left under the 227 KB cap (the
+  // kernel traps if the base needs more; the dynamic base is 1 KiB aligned)
+  const size_t core = eg ? sizeof(SnapSmemT<kSnapTpcGlobal, true>) : sizeof(SnapSmemT<kSnapTpcSmem, false>);
+  const int slack = static_cast<int>(std::min<size_t>(1024, size_t(smem_optin()) - std::min(core, size_t(smem_optin()))));
+  const size_t smem = core + slack;
   auto kern = eg ? k_snapkv_tc<kSnapTpcGlobal, true> : k_snapkv_tc<kSnapTpcSmem, false>;
   static bool attr[2] = {false, false};
   if (!attr[eg]) {
@@ -989,7 +1018,7 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     cfg.gridDim = dim3(Cn, std::max(1, std::min(S, ng)));
   }
   KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(k), static_cast<const uint8_t*>(qbuf), escr,
-                                  scores, T, W, G, c->pool, tpc, S));
+                                  scores, T, W, G, c->pool, tpc, S, slack));
   LAUNCHED(h);
   return KVT_OK;
 }
