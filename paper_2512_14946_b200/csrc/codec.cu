@@ -814,10 +814,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       // are already on the next slice)
       auto round_arrive = [&](int k) {
         named_bar_sync(2, kCT);  // this CTA's round-k data written
-        if (ctid < C) {  // one arrive per peer, issued in parallel
-          fence_acq_rel_cluster();
+        if (ctid < C)  // one arrive per peer, issued in parallel (release.cluster: cumulative over the barrier)
           mbar_arrive_remote(&sm.rb[k], static_cast<uint32_t>(ctid));
-        }
         mbar_wait_cluster(&sm.rb[k], it & 1);  // every CTA's round-k data visible
       };
       {
