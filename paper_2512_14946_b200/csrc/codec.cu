@@ -816,7 +816,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         named_bar_sync(2, kCT);  // this CTA's round-k data written
         if (ctid < C)  // one arrive per peer, issued in parallel (release.cluster: cumulative over the barrier)
           mbar_arrive_remote(&sm.rb[k], static_cast<uint32_t>(ctid));
-        mbar_wait_cluster(&sm.rb[k], it & 1);  // every CTA's round-k data visible
+        if (cw == 0) mbar_wait_cluster(&sm.rb[k], it & 1);  // every CTA's round-k data visible ...
+        named_bar_sync(2, kCT);                             // ... to every consumer thread
       };
       {
         int32_t m = INT_MIN;
