@@ -491,14 +491,14 @@ struct SnapSmemT {
     unsigned long long vote[TPC * 128];   // after the block weights: per-token votes
   };
   uint32_t lb[TPC * 4][128];  // per (block, row) sum of E, then the block weight
-  unsigned long long lloc[128];
-  int32_t mloc[128];
+  unsigned long long lglob[128];  // row sums, summed in by every CTA (red.async.add)
+  int32_t mglob[128];             // row shifts, max-ed in by every CTA (red.async.max)
   unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
   float sig[128];
   float tau[4];  // per-tile scale, ring over the CTA's tile count
   uint32_t amax[kSnapProd];
   uint64_t full, qbar, tfull[2], tempty[2];
-  uint64_t rb[3];  // cluster rounds of the tail (row shifts, row sums, halos): one arrival per CTA
+  uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
   uint32_t tmem_base;
 };
 
@@ -617,6 +617,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
+__device__ __forceinline__ int half_of(int pool) { return pool / 2; }
+
 template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
     k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, uint8_t* __restrict__ escr,
@@ -650,8 +652,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     mbar_init(&sm.tfull[1], 2);
     mbar_init(&sm.tempty[0], kSnapCons);
     mbar_init(&sm.tempty[1], kSnapCons);
-    for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], C);
+    for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], 1);
     mbar_fence_init();
+  }
+  if (tid < 128) {
+    sm.mglob[tid] = INT_MIN;
+    sm.lglob[tid] = 0;
   }
   if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
   tc_fence_before();
@@ -809,30 +815,37 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       }
       named_bar_sync(2, kCT);  // every tile's E, mb, lb in place
 
-      // ---- row shift and sum across the cluster: three rounds signalled with
-      // one remote mbarrier arrive per CTA (consumers only; the producers
-      // are already on the next slice)
-      auto round_arrive = [&](int k) {
-        named_bar_sync(2, kCT);  // this CTA's round-k data written
-        if (ctid < C)  // one arrive per peer, issued in parallel (release.cluster: cumulative over the barrier)
-          mbar_arrive_remote(&sm.rb[k], static_cast<uint32_t>(ctid));
-        if (cw == 0) mbar_wait_cluster(&sm.rb[k], it & 1);  // every CTA's round-k data visible ...
-        named_bar_sync(2, kCT);                             // ... to every consumer thread
+      // ---- row shift and sum across the cluster. Every CTA pushes its per-row
+      // values into every CTA's mglob / lglob with red.async (max / add),
+      // which completes bytes on the receiver's round mbarrier; the receiver
+      // only waits for the expected byte count (no fence, no pull).
+      const int nb_l = rank > 0 ? 1 : 0, nb_r = rank < C - 1 ? 1 : 0;
+      if (ctid == 0) {
+        mbar_expect_tx(&sm.rb[0], static_cast<uint32_t>(C) * 128 * 4);
+        mbar_expect_tx(&sm.rb[1], static_cast<uint32_t>(C) * 128 * 8);
+        const int n_right = min(half_of(pool), max(0, min(P - (tile0 + tpc) * 128, tpc * 128)));  // right peer's tokens
+        mbar_expect_tx(&sm.rb[2], static_cast<uint32_t>((nb_l * half_of(pool) + nb_r * n_right) * 8));
+      }
+      auto round_wait = [&](int k) {
+        if (cw == 0) mbar_wait(&sm.rb[k], it & 1);  // every CTA's round-k bytes landed ...
+        named_bar_sync(2, kCT);                     // ... for every consumer thread
       };
       {
         int32_t m = INT_MIN;
         for (int b = cq; b < nblk; b += 4) m = max(m, sm.mb[b][crow]);
         m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
         m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        if (cq == 0) sm.mloc[crow] = m;
-      }
-      round_arrive(0);
-      int32_t mrow = INT_MIN;
 #pragma unroll
-      for (int i = 0; i < kSnapMaxC / 4; ++i)  // the <= 4 remote reads in flight together
-        if (cq + 4 * i < C) mrow = max(mrow, cl.map_shared_rank(sm.mloc, cq + 4 * i)[crow]);
-      mrow = max(mrow, __shfl_xor_sync(0xffffffffu, mrow, 1));
-      mrow = max(mrow, __shfl_xor_sync(0xffffffffu, mrow, 2));
+        for (int i = 0; i < kSnapMaxC / 4; ++i)
+          if (cq + 4 * i < C) {
+            const uint32_t c = static_cast<uint32_t>(cq + 4 * i);
+            red_async_max_s32(mapa_u32(&sm.mglob[crow], c), m, mapa_u32(&sm.rb[0], c));
+          }
+      }
+      round_wait(0);
+      int32_t mrow = sm.mglob[crow];
+      mrow = __shfl_sync(0xffffffffu, mrow, lane & ~3);  // all four readers saw it before the reset
+      if (cq == 0) sm.mglob[crow] = INT_MIN;            // peers' next contributions come after round 2
       {
         unsigned long long Ls = 0;
         for (int b = cq; b < nblk; b += 4) {
@@ -841,16 +854,18 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         }
         Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
         Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
-        if (cq == 0) sm.lloc[crow] = Ls;
-      }
-      round_arrive(1);
-      {
-        unsigned long long Ls = 0;
 #pragma unroll
         for (int i = 0; i < kSnapMaxC / 4; ++i)
-          if (cq + 4 * i < C) Ls += cl.map_shared_rank(sm.lloc, cq + 4 * i)[crow];
-        Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
-        Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
+          if (cq + 4 * i < C) {
+            const uint32_t c = static_cast<uint32_t>(cq + 4 * i);
+            red_async_add_u64(mapa_u32(&sm.lglob[crow], c), Ls, mapa_u32(&sm.rb[1], c));
+          }
+      }
+      round_wait(1);
+      {
+        unsigned long long Ls = sm.lglob[crow];
+        Ls = __shfl_sync(0xffffffffu, Ls, lane & ~3);
+        if (cq == 0) sm.lglob[crow] = 0;
         const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
         for (int b = cq; b < nblk; b += 4) {
           const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
@@ -890,13 +905,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         }
       }
       named_bar_sync(2, kCT);  // votes complete
-      // push this CTA's boundary votes into the neighbours' halos (non-last CTAs are full: n_loc = tpc * 128)
-      const int half = pool / 2;
+      // push this CTA's boundary votes into the neighbours' halos (st.async,
+      // complete_tx on their round-2 mbarrier; non-last CTAs are full: n_loc = tpc * 128)
+      const int half = half_of(pool);
       if (ctid < half) {
-        if (rank > 0 && ctid < n_loc) cl.map_shared_rank(sm.rhalo, rank - 1)[ctid] = sm.vote[ctid];
-        if (rank < C - 1) cl.map_shared_rank(sm.lhalo, rank + 1)[ctid] = sm.vote[n_loc - half + ctid];
+        if (rank > 0 && ctid < n_loc)
+          st_async_u64(mapa_u32(&sm.rhalo[ctid], rank - 1), sm.vote[ctid], mapa_u32(&sm.rb[2], rank - 1));
+        if (rank < C - 1)
+          st_async_u64(mapa_u32(&sm.lhalo[ctid], rank + 1), sm.vote[n_loc - half + ctid], mapa_u32(&sm.rb[2], rank + 1));
       }
-      round_arrive(2);  // halos in place
+      round_wait(2);  // halos in place
       // ---- pooling (max over +-pool/2 within the prefix) and scores
       float* out = scores + static_cast<size_t>(slice) * T;
       for (int tl = ctid; tl < n_loc; tl += kCT) {

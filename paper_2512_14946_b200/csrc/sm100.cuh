@@ -44,6 +44,42 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
       "r"(parity)
       : "memory");
 }
+// the same, polling with test_wait (no suspend): lowest wake-up latency for a
+// single waiting warp
+__device__ __forceinline__ void mbar_poll_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "POLLC_%=:\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra POLLC_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// Asynchronous remote shared-memory updates that signal the destination
+// CTA's mbarrier with their byte count (complete_tx): cluster all-reduces
+// without a release fence or a pull round trip.
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void red_async_max_s32(uint32_t raddr, int32_t v, uint32_t rbar) {
+  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.max.s32 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "r"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void red_async_add_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "l"(v), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+               "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 
 // 1-D TMA bulk copy global -> this CTA's smem, completion on mbarrier b
