@@ -880,17 +880,35 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         unsigned long long a0 = 0, a1 = 0;
         if (2 * p < n_loc) {
           const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
+          if (EG) {
 #pragma unroll 4
-          for (int r0 = 0; r0 < 64; r0 += 4) {
-            const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
-            const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+            for (int r0 = 0; r0 < 64; r0 += 4) {
+              const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
+              const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int rr = rq * 64 + r0 + q;
-              const uint32_t e2 = EG ? __ldcg(reinterpret_cast<const uint32_t*>(Eg + rr * (TPC * 128)) + p)
-                                     : *reinterpret_cast<const uint32_t*>(sm.e + snap_e_off(rr, 4 * p));
-              a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
-              a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t e2 = __ldcg(reinterpret_cast<const uint32_t*>(Eg + (rq * 64 + r0 + q) * (TPC * 128)) + p);
+                a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
+                a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+              }
+            }
+          } else {
+            // the pair's swizzled byte offset in row r depends on r & 7 only:
+            // 8 offsets, the row stride folds into the load's immediate
+            const uint8_t* eb[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) eb[q] = sm.e + rq * 64 * 1024 + snap_e_off(q, 4 * p);
+#pragma unroll
+            for (int r0 = 0; r0 < 64; r0 += 8) {
+              const uint4 wa = *reinterpret_cast<const uint4*>(wb + r0);
+              const uint4 wc = *reinterpret_cast<const uint4*>(wb + r0 + 4);
+              const uint32_t ww[8] = {wa.x, wa.y, wa.z, wa.w, wc.x, wc.y, wc.z, wc.w};
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const uint32_t e2 = *reinterpret_cast<const uint32_t*>(eb[q] + r0 * 1024);  // row rq*64 + r0 + q
+                a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
+                a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+              }
             }
           }
         }
