@@ -618,6 +618,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 }
 
 __device__ __forceinline__ int half_of(int pool) { return pool / 2; }
+// floor(2^61 / d) for a row sum d >= 2^31 (the row's top block holds an
+// E = 2^15, shifted up by 16): the quotient is < 2^30, so the correctly
+// rounded FP64 estimate is within 1 of it; one exact remainder test fixes it
+__device__ __forceinline__ unsigned long long div_2p61(unsigned long long d) {
+  const long long q0 = static_cast<long long>(__ddiv_rn(2305843009213693952.0, __ull2double_rn(d)));
+  const long long rem = static_cast<long long>(1ull << 61) - q0 * static_cast<long long>(d);
+  if (rem < 0) return static_cast<unsigned long long>(q0 - 1);
+  if (rem >= static_cast<long long>(d)) return static_cast<unsigned long long>(q0 + 1);
+  return static_cast<unsigned long long>(q0);
+}
 
 template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
@@ -866,7 +876,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         unsigned long long Ls = sm.lglob[crow];
         Ls = __shfl_sync(0xffffffffu, Ls, lane & ~3);
         if (cq == 0) sm.lglob[crow] = 0;
-        const unsigned long long wt = (crow < R && Ls) ? (1ull << 61) / Ls : 0ull;
+        const unsigned long long wt = (crow < R && Ls) ? div_2p61(Ls) : 0ull;
         for (int b = cq; b < nblk; b += 4) {
           const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
           sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
