@@ -454,15 +454,19 @@ static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKd
 // (row, 32-token block): M = ceil(max y), E = round(2^15 * 2^(y - M)) by a
 // fixed FMA polynomial, blocks are combined with exact integer shifts.
 //
-// One thread-block cluster (<= 16 CTAs) per (layer, kv-head) slice; CTA
-// `rank` owns up to 4 tiles (512 tokens). Each tile is bulk-copied (bf16) into
-// smem, quantised to int8 (SW128 K-major UMMA layout), multiplied against the
-// resident Q8 tile into TMEM, and the 16 epilogue warps (lane quadrant x
-// 32-token block) turn their 32 logits into u16 E values kept in smem. Row
-// shifts and sums are combined across the cluster through DSMEM; then every
-// thread votes one token from the stored E (no second exp), and pooling reads
-// neighbour CTAs' votes through DSMEM. The next tile's copy overlaps the MMA
-// and epilogue of the current one.
+// A thread-block cluster (<= 16 CTAs) works on one (layer, kv-head) slice
+// at a time; the clusters are persistent (as many as fit, each looping over
+// slices). CTA `rank` owns up to 4 tiles (512 tokens) of a slice. Producer
+// warps bulk-copy each tile (bf16) into smem, quantise it to int8 (SW128
+// K-major UMMA layout) and multiply it against the slice's Q8 tile into a
+// double-buffered TMEM accumulator; the 16 consumer warps (lane quadrant x
+// 32-token block) turn their 32 logits into u16 E values kept in smem. The
+// consumers then run the slice's tail while the producers already load and
+// multiply the next slice's first tiles: row shifts and row sums are
+// all-reduced by red.async (max / add) from every CTA into every CTA,
+// completing bytes on the receiver's mbarrier; every thread votes a token
+// pair from the stored E (no second exp); boundary votes go to the
+// neighbours by st.async; pooling.
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
 constexpr int kSnapProd = 8;           // producer warps: K tile absmax + int8 quantisation + MMA issue
 constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
