@@ -1434,25 +1434,32 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
 #pragma unroll
   for (int i = 0; i < kVRows; ++i)
     v[i] = j_first + i < k ? __ldcs(Vs + static_cast<uint32_t>(tok[i]) * 16u) : make_uint4(0, 0, 0, 0);
-  uint32_t mm_mine = 0;  // lane i < kVRows: (min, max) of row i as a bf16 pair
+  static_assert(kVRows == 8, "transpose-reduce below is written for 8 rows per half-warp");
+  // (min, max) of each row's 128 channels as a bf16 pair, reduced over the
+  // half-warp for all 8 rows at once: at each butterfly level a lane keeps
+  // half of its rows and trades the other half with its partner, so lanes
+  // 2i, 2i + 1 end with row i (8 shuffles for 8 rows instead of 32)
+  auto merge = [](uint32_t a, uint32_t b) { return __byte_perm(bmin2(a, b), bmax2(a, b), 0x7610); };
+  uint32_t mm[kVRows];
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
     const uint32_t m2 = bmin2(bmin2(v[i].x, v[i].y), bmin2(v[i].z, v[i].w));  // mins of even / odd channels
     const uint32_t x2 = bmax2(bmax2(v[i].x, v[i].y), bmax2(v[i].z, v[i].w));
-    // (min of the lane's 8 channels, max of them) as one bf16 pair
-    uint32_t lo = bmin2(m2, m2 >> 16), hi = bmax2(x2, x2 >> 16);
-    uint32_t mm = __byte_perm(lo, hi, 0x5410);
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) {
-      const uint32_t o = __shfl_xor_sync(0xffffffffu, mm, off);
-      mm = __byte_perm(bmin2(mm, o), bmax2(mm, o), 0x7610);
-    }
-    if (l16 == i) mm_mine = mm;
+    mm[i] = __byte_perm(bmin2(m2, m2 >> 16), bmax2(x2, x2 >> 16), 0x5410);  // this lane's 8 channels
   }
-  QParam p{};
-  if (l16 < kVRows) p = make_param(bf_lo(mm_mine), bf_hi(mm_mine), BITS);
-  const int j_mine = j_first + l16;
-  if (l16 < kVRows && j_mine < k) {
+  const bool b3 = l16 & 8, b2 = l16 & 4, b1 = l16 & 2;
+  uint32_t a4[4], a2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    a4[i] = merge(b3 ? mm[i + 4] : mm[i], __shfl_xor_sync(0xffffffffu, b3 ? mm[i] : mm[i + 4], 8));
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    a2[i] = merge(b2 ? a4[i + 2] : a4[i], __shfl_xor_sync(0xffffffffu, b2 ? a4[i] : a4[i + 2], 4));
+  uint32_t mm_mine = merge(b1 ? a2[1] : a2[0], __shfl_xor_sync(0xffffffffu, b1 ? a2[0] : a2[1], 2));
+  mm_mine = merge(mm_mine, __shfl_xor_sync(0xffffffffu, mm_mine, 1));  // row l16 / 2
+  const QParam p = make_param(bf_lo(mm_mine), bf_hi(mm_mine), BITS);
+  const int j_mine = j_first + (l16 >> 1);
+  if ((l16 & 1) == 0 && j_mine < k) {
     vs[static_cast<size_t>(slice) * k + j_mine] = p.s16;
     vz[static_cast<size_t>(slice) * k + j_mine] = p.z16;
     if (oidx) oidx[static_cast<size_t>(slice) * k + j_mine] = ix[j_mine];
@@ -1462,8 +1469,8 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
     const int j = j_first + i;
-    const float zf = __shfl_sync(0xffffffffu, p.zf, base + i), inv = __shfl_sync(0xffffffffu, p.inv, base + i);
-    const int fast = __shfl_sync(0xffffffffu, fast_mine, base + i);
+    const float zf = __shfl_sync(0xffffffffu, p.zf, base + 2 * i), inv = __shfl_sync(0xffffffffu, p.inv, base + 2 * i);
+    const int fast = __shfl_sync(0xffffffffu, fast_mine, base + 2 * i);
     uint32_t lanes[4];
     if (fast) {
       const float2 nz[4] = {make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf)};
