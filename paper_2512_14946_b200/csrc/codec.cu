@@ -1172,27 +1172,54 @@ using TopkScan = cub::BlockScan<int, kTopkThreads>;
 // shared memory, then an order-preserving block compaction.
 __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__ scores, int32_t* __restrict__ idx,
                                                        int T, int k, int keys_in_smem) {
-  extern __shared__ uint32_t skeys[];
+  extern __shared__ uint32_t skeys[];  // key t at skeys[t + t / 16]: conflict-free per-thread segments
   __shared__ int hist[256];
   __shared__ uint32_t s_prefix, s_mask;
   __shared__ int s_remaining, s_bucket, s_remaining_next;
   __shared__ typename TopkScan::TempStorage scan_tmp;
+  __shared__ uint32_t s_and[kTopkThreads / 32], s_or[kTopkThreads / 32];
   const int slice = blockIdx.x, tid = threadIdx.x;
   const float* sc = scores + static_cast<size_t>(slice) * T;
-  if (keys_in_smem)
-    for (int t = tid; t < T; t += kTopkThreads) skeys[t] = score_key(sc[t]);
+  // the bits every key shares need no radix pass (and would pile the first
+  // histogram into one bin): start at the highest bit where keys differ
+  uint32_t kand = ~0u, kor = 0u;
+#pragma unroll 4
+  for (int t = tid; t < T; t += kTopkThreads) {
+    const uint32_t key = score_key(sc[t]);
+    if (keys_in_smem) skeys[t + (t >> 4)] = key;
+    kand &= key;
+    kor |= key;
+  }
+  kand = __reduce_and_sync(0xffffffffu, kand);
+  kor = __reduce_or_sync(0xffffffffu, kor);
+  if ((tid & 31) == 0) {
+    s_and[tid >> 5] = kand;
+    s_or[tid >> 5] = kor;
+  }
+  __syncthreads();
+  kand = ~0u;
+  kor = 0u;
+#pragma unroll
+  for (int w = 0; w < kTopkThreads / 32; ++w) {
+    kand &= s_and[w];
+    kor |= s_or[w];
+  }
+  const uint32_t common = ~(kand ^ kor);  // bits equal in every key
+  const int hb = 31 - __clz(~common);      // highest differing bit (-1: all keys equal)
   if (tid == 0) {
-    s_prefix = 0;
-    s_mask = 0;
+    const uint32_t m0 = hb < 0 ? ~0u : ~((2u << hb) - 1u);  // the bits above hb: common to every key
+    s_prefix = kand & m0;
+    s_mask = m0;
     s_remaining = k;
   }
   __syncthreads();
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  for (int s8 = hb - 7; hb >= 0; s8 -= 8) {
+    const int shift = max(s8, 0);
     for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
     __syncthreads();
     const uint32_t prefix = s_prefix, mask = s_mask;
     for (int t = tid; t < T; t += kTopkThreads) {
-      const uint32_t key = keys_in_smem ? skeys[t] : score_key(sc[t]);
+      const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
     }
     __syncthreads();
@@ -1200,10 +1227,11 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
     __syncthreads();
     if (tid == 0) {
       s_remaining = s_remaining_next;
-      s_prefix = prefix | (uint32_t(s_bucket) << shift);
+      s_prefix = (prefix & ~(255u << shift)) | (uint32_t(s_bucket) << shift);  // the digit may overlap fixed bits
       s_mask = mask | (255u << shift);
     }
     __syncthreads();
+    if (shift == 0) break;
   }
   const uint32_t kth = s_prefix;
   const int ties = s_remaining;  // equal-to-kth keys to take (lowest indices)
@@ -1211,7 +1239,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   const int t0 = tid * seg, t1 = min(T, t0 + seg);
   int above = 0, eq = 0;
   for (int t = t0; t < t1; ++t) {
-    const uint32_t key = keys_in_smem ? skeys[t] : score_key(sc[t]);
+    const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
     above += key > kth;
     eq += key == kth;
   }
@@ -1223,7 +1251,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   int eq_seen = eq_before;
   int32_t* out = idx + static_cast<size_t>(slice) * k;
   for (int t = t0; t < t1; ++t) {
-    const uint32_t key = keys_in_smem ? skeys[t] : score_key(sc[t]);
+    const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
     if (key > kth) {
       out[pos++] = t;
     } else if (key == kth) {
@@ -1236,7 +1264,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
 static int launch_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const float* scores,
                        int32_t* idx) {
   const int S = s->L * s->H;
-  const size_t smem = sizeof(uint32_t) * size_t(s->T);
+  const size_t smem = sizeof(uint32_t) * (size_t(s->T) + size_t(s->T) / 16 + 1);
   const int in_smem = smem <= 160 * 1024;
   static bool attr = false;
   if (!attr) {

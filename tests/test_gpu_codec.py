@@ -158,6 +158,34 @@ def test_topk_bitexact_with_ties(gpu, orc, keep_ratio):
     assert np.array_equal(topk(gpu, s, cfg, dev(sc), True), topk(orc, s, cfg, sc, False))
 
 
+# top-k key distributions for the adaptive first radix digit: every key
+# equal, keys differing only in the last mantissa bits, +inf window scores
+# mixed in, the full signed range, and a slice too long for smem keys
+TOPK_CASES = ["equal", "ulps", "inf", "wide", "long"]
+
+
+@pytest.mark.parametrize("case", TOPK_CASES)
+@pytest.mark.parametrize("keep_ratio", [0.01, 0.37, 0.9])
+def test_topk_key_distributions(gpu, orc, case, keep_ratio):
+    T = 41000 if case == "long" else 3000
+    s = A.KvShape(1, 2, T, 128)
+    rng = np.random.default_rng(7)
+    n = s.L * s.H * s.T
+    if case == "equal":
+        sc = np.full(n, 1.25, np.float32)
+    elif case == "ulps":
+        sc = (np.float32(3.0).view(np.uint32) + rng.integers(0, 5, n).astype(np.uint32)).view(np.float32)
+    elif case == "inf":
+        sc = rng.standard_normal(n).astype(np.float32)
+        sc[rng.random(n) < 0.05] = np.inf
+    else:
+        sc = (rng.standard_normal(n) * np.float32(1e30)).astype(np.float32)
+        sc[::13] = -0.0
+        sc[::17] = 0.0
+    cfg = plan(orc.abi, "knorm", keep_ratio, s)
+    assert np.array_equal(topk(gpu, s, cfg, dev(sc), True), topk(orc, s, cfg, sc, False))
+
+
 def compress(eng, s, cfg, k, v, on_gpu):
     m = A.BlobMap()
     eng.abi.check(eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
