@@ -268,6 +268,21 @@ __device__ __forceinline__ float half_butterfly(float p) {
   return p;
 }
 
+// half_butterfly of 4 rows at once (chunk sums p[u] of rows u = 0..3): at
+// strides 8 and 4 a lane keeps half of its rows and trades the other half
+// with its partner, so every add pairs the same chunks as the per-row
+// butterfly (bit-identical); returns row (l16 >> 2) & 3's total, held by
+// lanes 4u .. 4u + 3 of the half-warp. 5 shuffles instead of 16.
+__device__ __forceinline__ float half_butterfly4(const float (&p)[4]) {
+  const int l16 = threadIdx.x & 15;
+  const bool b3 = l16 & 8, b2 = l16 & 4;
+  const float a0 = __fadd_rn(b3 ? p[2] : p[0], __shfl_xor_sync(0xffffffffu, b3 ? p[0] : p[2], 8));
+  const float a1 = __fadd_rn(b3 ? p[3] : p[1], __shfl_xor_sync(0xffffffffu, b3 ? p[1] : p[3], 8));
+  float b = __fadd_rn(b2 ? a1 : a0, __shfl_xor_sync(0xffffffffu, b2 ? a0 : a1, 4));
+  b = __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, 2));
+  return __fadd_rn(b, __shfl_xor_sync(0xffffffffu, b, 1));
+}
+
 constexpr int kUnroll = 4;
 
 // knorm: squared L2 norm of every key (larger = keep).
@@ -402,14 +417,14 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   uint32_t cnt = 0;  // <= per / 16 tokens per lane: the biased u32 sums cannot wrap for T < 2^16
   stream_rows4(Ks, n_loc, ring, full, seq, [&](const int (&t)[4], const bool (&live)[4], const uint4 (&v)[4]) {
-    float n2[4];
+    float q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) n2[u] = half_butterfly(chunk_sumsq(v[u]));
-    // one sqrt + reciprocal sequence for the half-warp's 4 rows: lane u computes row u
-    const float mine = kd_inv(l16 == 0 ? n2[0] : (l16 == 1 ? n2[1] : (l16 == 2 ? n2[2] : n2[3])));
+    for (int u = 0; u < 4; ++u) q[u] = chunk_sumsq(v[u]);
+    // lanes 4u .. 4u + 3 get row u's |k|^2: one sqrt + reciprocal per lane
+    const float mine = kd_inv(half_butterfly4(q));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const float inv = __shfl_sync(0xffffffffu, mine, (threadIdx.x & 16) + u);
+      const float inv = __shfl_sync(0xffffffffu, mine, (threadIdx.x & 16) + 4 * u);
       if (live[u]) {
         kd_fix_add(v[u], __fmul_rn(inv, kKdFx), acc);
         ++cnt;
@@ -437,9 +452,15 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
 #pragma unroll
   for (int q = 0; q < 4; ++q) sd[q] = make_float2(sdir[l16 * 8 + 2 * q], sdir[l16 * 8 + 2 * q + 1]);
   float* o = out + static_cast<size_t>(slice) * T + t_lo;
-  stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
-    const float p = half_butterfly(chunk_dot(v, sd));
-    if (live && l16 == 0) o[t] = -__fmul_rn(p, kinv[t]);
+  stream_rows4(Ks, n_loc, ring, full, seq, [&](const int (&t)[4], const bool (&live)[4], const uint4 (&v)[4]) {
+    float q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = chunk_dot(v[u], sd);
+    const float p = half_butterfly4(q);  // row (l16 >> 2)
+    const int u = l16 >> 2;
+    const int tu = u == 0 ? t[0] : (u == 1 ? t[1] : (u == 2 ? t[2] : t[3]));
+    const bool lu = u == 0 ? live[0] : (u == 1 ? live[1] : (u == 2 ? live[2] : live[3]));
+    if (lu && (l16 & 3) == 0) o[tu] = -__fmul_rn(p, kinv[tu]);
   });
   cluster_sync_smem();  // no CTA exits while a peer may still read its sfix
 }
