@@ -181,7 +181,7 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
     pk, how = peaks()
     achieved = alg / (t_ms / 1e3) / 1e9
     traffic = traffic_table().get(dom)
-    return {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+    line = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / pk["hbm_gbs"], 4),
             "traffic": traffic, "traffic_note": "ncu dram read+write bytes per launch (profiles/traffic.json)",
             "alg_bytes_per_launch": int(alg // n), "avg_launch_ms": round(t_ms / n, 4), "launches": n,
@@ -190,6 +190,18 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
             "kernels": {k_: {"ms": round(v[0], 2), "n": v[2], "GBps": round(v[1] / (v[0] / 1e3) / 1e9, 1),
                              "frac": round(v[1] / (v[0] / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
                         for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
+    if dom in ISSUE_BOUND:  # HBM fraction is reported, but it is not what bounds this kernel
+        line["bound_note"] = ISSUE_BOUND[dom]
+    return line
+
+
+# kernels whose limit is instruction issue, not HBM (ncu captures in profiles/)
+ISSUE_BOUND = {
+    "k_snapkv_tc": "issue-bound exp epilogue + cluster all-reduce tail: ncu issue active 53 %, "
+                   "214.6 M warp-instructions per launch (profiles/r1w_ncu_snapkv_raw.csv, DESIGN.md §5)",
+    "k_keydiff_cluster": "issue/latency-bound: K is read from HBM once (556 MB/launch); ncu issue active 53 % "
+                         "(profiles/r1v_ncu_keydiff_raw.csv)",
+}
 
 
 def tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, lo, hi, n_ctx=4, reps=3):
