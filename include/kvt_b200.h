@@ -202,6 +202,9 @@ typedef struct kvt_store kvt_store;     /* StoreState */
   int P##store_remove(kvt_store* s, int32_t ctx, kvt_entry* removed);              \
   int P##store_reconfigure(kvt_store* s, int32_t ctx, int32_t method, double ratio); \
   int P##store_touch(kvt_store* s, int32_t ctx, int64_t stamp);                    \
+  /* n touches in order (the serve loop's hits; placement.cpp:135-142 each) */     \
+  int P##store_touch_many(kvt_store* s, const int32_t* ctx, const int64_t* stamps, \
+                          int64_t n);                                              \
   int P##store_clear(kvt_store* s);                                                \
   int P##store_occupancy(kvt_store* s, int64_t* occ);                              \
   int P##store_snapshot(kvt_store* s, kvt_entry* entries);                         \

@@ -501,6 +501,14 @@ int orc_store_touch(kvt_store* s, int32_t c, int64_t stamp) {
   return KVT_OK;
 }
 
+/* n StoreState::touch calls in order (the serve loop's hits) */
+int orc_store_touch_many(kvt_store* s, const int32_t* ctx, const int64_t* stamps, int64_t n) {
+  int rc;
+  for (int64_t i = 0; i < n; ++i)
+    if ((rc = orc_store_touch(s, ctx[i], stamps[i]))) return rc;
+  return KVT_OK;
+}
+
 /* StoreState::clear proj/src/placement.cpp:144-148 */
 int orc_store_clear(kvt_store* s) {
   for (int32_t c = 0; c < s->n_ctx; ++c) s->e[c].tier_index = -1;

@@ -297,6 +297,11 @@ int ref_store_reconfigure(kvt_store* s, int32_t ctx, int32_t m, double ratio) {
 int ref_store_touch(kvt_store* s, int32_t ctx, int64_t stamp) {
   return guard([&] { s->st->touch(ctx_name(ctx), stamp); });
 }
+int ref_store_touch_many(kvt_store* s, const int32_t* ctx, const int64_t* stamps, int64_t n) {
+  return guard([&] {
+    for (int64_t i = 0; i < n; ++i) s->st->touch(ctx_name(ctx[i]), stamps[i]);
+  });
+}
 int ref_store_clear(kvt_store* s) {
   s->st->clear();
   return KVT_OK;
@@ -462,4 +467,76 @@ int ref_placement_utility(kvt_store* s, const kvt_pset* pc, const kvt_space* sp,
 extern "C" int ref_store_bind_space(kvt_store* s, const kvt_space* sp) {
   set_names(s, sp);
   return KVT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Serve-loop goldens: load a reference scenario file with the
+// reference's own loader, run the reference's own replay, and write the
+// expanded scenario (every input the replay used) plus its results as JSON.
+// Test infrastructure only: tests/golden/make_replay_golden.py calls it here
+// (the container with /root/reference), the fixtures travel, the GPU box
+// never runs this.
+#include <fstream>
+
+#include "kvtier/simulate.hpp"
+#include "kvtier/workload.hpp"
+#include "json.hpp"  // nlohmann/json 3.11.3, the reference build's copy (oracle/Makefile NLOHMANN)
+
+extern "C" int ref_replay_dump(const char* scenario_path, const char* out_path, const char* const* overrides,
+                               int32_t n_overrides) {
+  return guard([&] {
+    using nlohmann::json;
+    std::vector<std::string> ov;
+    for (int32_t i = 0; i < n_overrides; ++i) ov.emplace_back(overrides[i]);
+    const kvtier::LoadedScenario run = kvtier::load_scenario_file(scenario_path, ov);
+    const kvtier::Scenario& sc = run.scenario;
+    json j;
+    j["policy"] = run.policy.label();
+    j["policy_kind"] = static_cast<int>(run.policy.kind);
+    j["rule"] = run.policy.rule == kvtier::SelectionRule::Utility ? "utility" : "quality_first";
+    j["warm_start"] = sc.warm_start;
+    j["miss_store_bottom"] = sc.miss_store_bottom;
+    j["drift"] = sc.drift.enabled;
+    j["n_truth"] = sc.truth.size();
+    j["params"] = {{"alpha", sc.params.alpha}, {"prefill_a", sc.params.prefill_a},
+                   {"prefill_b", sc.params.prefill_b}, {"bytes_per_token", sc.params.bytes_per_token}};
+    for (const auto& t : sc.tiers) {
+      json jt = {{"tier_id", t.tier_id}, {"name", t.name}, {"read_bandwidth", t.read_bandwidth},
+                 {"fixed_access_latency", t.fixed_access_latency}};
+      jt["capacity_bytes"] = t.capacity_bytes ? json(*t.capacity_bytes) : json(nullptr);
+      j["tiers"].push_back(jt);
+    }
+    for (const auto& m : sc.space.methods().methods())
+      j["methods"].push_back({{"name", m.name}, {"decompression_overhead", m.decompression_overhead}});
+    j["ratios"] = sc.space.ratios();
+    for (const auto& [id, p] : sc.profiles) {
+      json jp = {{"context", id}, {"size", p.original_size_bytes}, {"frequency", p.frequency},
+                 {"grid", p.ratio_grid}};
+      for (const auto& [m, q] : p.quality_table) jp["quality"][m] = q;
+      j["profiles"].push_back(jp);
+    }
+    for (const auto& [id, curve] : sc.truth)
+      for (const auto& [m, sc_] : curve.per_method) j["truth"][id][m] = {sc_.sensitivity, sc_.shape_k};
+    j["order"] = sc.order;
+    for (const auto& r : run.trace)
+      j["trace"].push_back({{"t", r.t}, {"context", r.context}, {"n_new_tokens", r.n_new_tokens}});
+    const kvtier::ReplayResult res = kvtier::replay(run.trace, run.policy, sc);
+    json jr;
+    for (const auto& r : res.records)
+      jr["records"].push_back({{"hit", r.outcome == kvtier::Outcome::Hit}, {"tier", r.tier},
+                               {"method", r.config.method}, {"ratio", r.config.ratio}, {"ttft", r.ttft},
+                               {"quality", r.quality}});
+    for (const auto& a : res.actions)
+      jr["actions"].push_back({{"kind", kvtier::to_string(a.kind)}, {"context", a.context}, {"tier", a.tier},
+                               {"method", a.config.method}, {"ratio", a.config.ratio}});
+    jr["final_placements"] = res.final_placements;
+    const auto& m = res.metrics;
+    jr["metrics"] = {{"n_requests", m.n_requests}, {"sum_ttft", m.sum_ttft}, {"mean_ttft", m.mean_ttft},
+                     {"p50_ttft", m.p50_ttft}, {"p90_ttft", m.p90_ttft}, {"p99_ttft", m.p99_ttft},
+                     {"mean_quality", m.mean_quality}, {"miss_fraction", m.miss_fraction}};
+    for (const auto& [tier, f] : m.hit_fraction_by_tier) jr["metrics"]["hit_fraction_by_tier"][std::to_string(tier)] = f;
+    jr["reprofile_count"] = res.reprofile_count;
+    j["result"] = jr;
+    std::ofstream(out_path) << j.dump(1);
+  });
 }

@@ -125,6 +125,7 @@ PLACEMENT_SIGS = {
     "store_remove": (C.c_int, [P, i32, C.POINTER(Entry)]),
     "store_reconfigure": (C.c_int, [P, i32, i32, f64]),
     "store_touch": (C.c_int, [P, i32, i64]),
+    "store_touch_many": (C.c_int, [P, P, P, i64]),
     "store_clear": (C.c_int, [P]),
     "store_occupancy": (C.c_int, [P, P]),
     "store_snapshot": (C.c_int, [P, P]),

@@ -1312,6 +1312,41 @@ extern "C" int kvt_store_reconfigure(kvt_store* s, int32_t ctx, int32_t m, doubl
   return run_store_op(s, OP_RECONF, ctx, x, nullptr);
 }
 
+// n StoreState::touch calls in order, one thread (a later touch of the same
+// context must win last_access); stops at the first non-resident context.
+__global__ void k_touch_many(DevStore st, const int32_t* ctx, const int64_t* stamps, int64_t n) {
+  Ctl* ctl = st.ctl;
+  ctl->status = ST_OK;
+  for (int64_t i = 0; i < n; ++i) {
+    const int c = ctx[i];
+    if (c < 0 || c >= st.n || st.tier[c] < 0) {
+      ctl->status = ST_ERR_NOT_RESIDENT;
+      ctl->err_ctx = c;
+      return;
+    }
+    st.freq[c] += 1;
+    st.last[c] = stamps[i];
+  }
+}
+
+extern "C" int kvt_store_touch_many(kvt_store* s, const int32_t* ctx, const int64_t* stamps, int64_t n) {
+  if (n <= 0) return KVT_OK;
+  char* d = nullptr;
+  const size_t bc = sizeof(int32_t) * size_t(n), bs = sizeof(int64_t) * size_t(n);
+  KVT_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), bs + bc, s->h->stream));
+  KVT_CUDA_TRY(cudaMemcpyAsync(d, stamps, bs, cudaMemcpyHostToDevice, s->h->stream));
+  KVT_CUDA_TRY(cudaMemcpyAsync(d + bs, ctx, bc, cudaMemcpyHostToDevice, s->h->stream));
+  k_touch_many<<<1, 1, 0, s->h->stream>>>(s->d, reinterpret_cast<const int32_t*>(d + bs),
+                                          reinterpret_cast<const int64_t*>(d), n);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  KVT_CUDA_TRY(cudaFreeAsync(d, s->h->stream));
+  Ctl c2;
+  int rc = store_fetch_ctl(s, &c2);
+  if (rc) return rc;
+  return store_status_error(s, c2);
+}
+
 extern "C" int kvt_store_touch(kvt_store* s, int32_t ctx, int64_t stamp) {
   kvt_entry x{};
   x.last_access = stamp;
