@@ -158,6 +158,7 @@ class Replayer:
         self.records: List[RequestRecord] = []
         self.last_t: Optional[float] = None
         self.n_device_calls = 0
+        self._qcache: Dict[Tuple[int, int, float], float] = {}
         if scenario.warm_start:
             self._warm_up()
         self._refresh()
@@ -173,12 +174,44 @@ class Replayer:
             self.actions.append((KIND_NAMES[int(a["kind"])], ids[int(a["ctx"])], int(a["tier_id"]),
                                  self.names[int(a["method"])], float(a["ratio"])))
 
+    def _insert_ops(self, ctx: Sequence[int], stamps: Sequence[int]) -> List[np.ndarray]:
+        """insert_joint of every miss (frequency 1) in one call; the action
+        list split per op (each op starts with its Insert action)."""
+        if not ctx:
+            return []
+        n0 = len(self.actions)
+        acts = self.store.insert_joint(self.ps, self.sc.space, self.sc.params, np.asarray(ctx, np.int32),
+                                       frequency=np.ones(len(ctx), np.int64), stamp=np.asarray(stamps, np.int64),
+                                       rule=self.rule)
+        self.n_device_calls += 1
+        ids = self.arrays.ids
+        for a in acts:
+            self.actions.append((KIND_NAMES[int(a["kind"])], ids[int(a["ctx"])], int(a["tier_id"]),
+                                 self.names[int(a["method"])], float(a["ratio"])))
+        starts = np.nonzero(acts["kind"] == A.KVT_INSERT)[0]
+        assert len(starts) == len(ctx) and len(self.actions) - n0 == len(acts)
+        return np.split(acts, starts[1:])
+
+    def _apply(self, acts: np.ndarray):
+        """Replays one op's actions (placement.cpp:213-221, 225-250) on the mirror."""
+        tix = {t.tier_id: i for i, t in enumerate(self.tiers)}
+        for a in acts:
+            c = int(a["ctx"])
+            ti = tix[int(a["tier_id"])]
+            if int(a["kind"]) != A.KVT_RECOMPRESS and int(self.tier_index[c]) != ti:
+                self._seq += 1
+                self.seq[c] = self._seq  # arrival order within the tier
+            self.tier_index[c] = ti
+            self.method[c] = int(a["method"])
+            self.ratio[c] = float(a["ratio"])
+
     def _refresh(self):
         snap = self.store.snapshot()
         self.tier_index = snap["tier_index"].astype(np.int64)
         self.method = snap["method"].astype(np.int64)
         self.ratio = snap["ratio"].astype(np.float64)
         self.seq = snap["seq"].astype(np.int64)
+        self._seq = int(self.seq.max()) if len(self.seq) else 0
 
     def _warm_up(self):  # simulate.cpp:72-85: every context, frequency 0, one stamp each
         order = self.sc.order or sorted(self.prof, key=lambda c: c.encode())
@@ -188,61 +221,118 @@ class Replayer:
         self._insert(ctx, [0] * len(ctx), stamps)
 
     # -- serving
+    def _quality(self, c: int, m: int, ratio: float) -> float:
+        """Achieved quality of context c served at (m, ratio): the truth curve
+        when the scenario has one, else the profile (simulate.cpp:179-184)."""
+        key = (c, m, ratio)
+        q = self._qcache.get(key)
+        if q is None:
+            cid = self.arrays.ids[c]
+            truth = self.sc.truth.get(cid)
+            name = self.names[m]
+            q = synth_quality(*truth[name], ratio) if truth is not None else quality_of(self.prof[cid], name, ratio)
+            self._qcache[key] = q
+        return q
+
     def run(self, trace: Sequence[Request]) -> List[RequestRecord]:
-        """Replays `trace`: hits in host segments, misses through the device greedy."""
-        touch_c: List[int] = []
-        touch_s: List[int] = []
-        out = []
-        for r in trace:
-            if self.last_t is not None and r.t < self.last_t:
-                raise A.AbiError(A.KVT_ETRACE, f"trace timestamps are not monotone (t={r.t} after t={self.last_t})")
-            if r.n_new_tokens < 0:
-                raise A.AbiError(A.KVT_ETRACE, f"negative n_new_tokens for context {r.context}")
-            self.last_t = r.t
-            c = self.arrays.index.get(r.context)
-            if c is None:
-                raise A.AbiError(A.KVT_ETRACE, f"trace names unknown context {r.context}")
-            prof = self.prof[r.context]
-            stamp = self.stamp
-            self.stamp += 1
-            ti = int(self.tier_index[c])
-            if ti >= 0:  # hit (simulate.cpp:165-194)
-                tier = self.tiers[ti]
-                m, ratio = int(self.method[c]), float(self.ratio[c])
-                name = self.names[m]
-                load = load_time(compressed_size(prof.original_size_bytes, ratio), tier, self.ovh[m])
-                ttft = load + prefill_time(r.n_new_tokens, self.sc.params) + 0.0
-                truth = self.sc.truth.get(r.context)
-                if truth is not None:
-                    s_k = truth[name]
-                    quality = synth_quality(s_k[0], s_k[1], ratio)
-                else:
-                    quality = quality_of(prof, name, ratio)
-                rec = RequestRecord(r, True, tier.tier_id, name, ratio, ttft, quality)
-                touch_c.append(c)
-                touch_s.append(stamp)
-            else:  # miss (simulate.cpp:195-222): recompute, then the joint store
-                tokens = token_count(prof.original_size_bytes, self.sc.params) + r.n_new_tokens
-                rec = RequestRecord(r, False, -1, "", 1.0, prefill_time(tokens, self.sc.params) + 0.0, 1.0)
-                self._flush_touches(touch_c, touch_s)
-                self._insert([c], [1], [stamp])
-                self._refresh()
-            out.append(rec)
-        self._flush_touches(touch_c, touch_s)
+        """Replays `trace`. A joint-policy store never drops a context (the
+        bottom tier is unlimited), so the misses are the first requests of
+        the contexts not yet resident; the hits between two misses are served
+        as one vectorised segment from the placement mirror, with one batched
+        touch, and each miss runs insert_joint on the device store."""
+        n = len(trace)
+        if n == 0:
+            return []
+        t = np.fromiter((r.t for r in trace), np.float64, n)
+        nnew = np.fromiter((r.n_new_tokens for r in trace), np.int64, n)
+        try:
+            ctx = np.fromiter((self.arrays.index[r.context] for r in trace), np.int64, n)
+        except KeyError as e:
+            raise A.AbiError(A.KVT_ETRACE, f"trace names unknown context {e.args[0]}") from None
+        prev = np.concatenate([[self.last_t if self.last_t is not None else -np.inf], t[:-1]])
+        bad = np.nonzero(t < prev)[0]
+        if len(bad):
+            k = int(bad[0])
+            raise A.AbiError(A.KVT_ETRACE, f"trace timestamps are not monotone (t={t[k]} after t={prev[k]})")
+        neg = np.nonzero(nnew < 0)[0]
+        if len(neg):
+            raise A.AbiError(A.KVT_ETRACE, f"negative n_new_tokens for context {trace[int(neg[0])].context}")
+        self.last_t = float(t[-1])
+        stamps = self.stamp + np.arange(n, dtype=np.int64)
+        self.stamp += n
+        # misses: first request of every context that is not resident yet
+        resident = self.tier_index[ctx] >= 0
+        _, first = np.unique(ctx, return_index=True)
+        is_first = np.zeros(n, bool)
+        is_first[first] = True
+        miss_at = np.nonzero(is_first & ~resident)[0]
+
+        hit = np.ones(n, bool)
+        tier_id = np.full(n, -1, np.int64)
+        meth = np.full(n, -1, np.int64)
+        ratio = np.ones(n, np.float64)
+        ttft = np.zeros(n, np.float64)
+        qual = np.ones(n, np.float64)
+        p = self.sc.params
+        tier_lat = np.array([x.fixed_access_latency for x in self.tiers], np.float64)
+        tier_bw = np.array([x.read_bandwidth for x in self.tiers], np.float64)
+        tier_ids = np.array([x.tier_id for x in self.tiers], np.int64)
+        ovh = np.asarray(self.ovh, np.float64)
+        orig = self.arrays.orig
+
+        def serve_hits(lo, hi):
+            if hi <= lo:
+                return
+            c = ctx[lo:hi]
+            ti = self.tier_index[c]
+            m = self.method[c]
+            r = self.ratio[c]
+            # simulate.cpp:165-178: load + prefill(new tokens) + penalty (no re-profiling windows)
+            size = np.maximum(1.0, np.floor(orig[c].astype(np.float64) * r + 0.5))
+            load = tier_lat[ti] + size / tier_bw[ti] + size * ovh[m]
+            nn = nnew[lo:hi].astype(np.float64)
+            ttft[lo:hi] = (load + (p.prefill_a * nn + p.prefill_b * nn * nn)) + 0.0
+            tier_id[lo:hi] = tier_ids[ti]
+            meth[lo:hi] = m
+            ratio[lo:hi] = r
+            qual[lo:hi] = [self._quality(int(a), int(b), float(x)) for a, b, x in zip(c, m, r)]
+
+        # every miss's store in ONE device call: insert_joint runs the ops in
+        # order (each op = an insert + its overflow cascade, the same state
+        # evolution as one call per miss); touches never steer the joint
+        # policy (utility uses the profile frequency), so the hits between
+        # two misses are served from the mirror as it stood after the
+        # earlier op, replayed on the host from the action list
+        ops = self._insert_ops([int(ctx[j]) for j in miss_at], [int(stamps[j]) for j in miss_at])
+        lo = 0
+        for k, j in enumerate(miss_at):
+            j = int(j)
+            serve_hits(lo, j)
+            c = int(ctx[j])
+            # simulate.cpp:195-203: recompute the whole context, lossless; then the joint store
+            tokens = token_count(int(orig[c]), p) + int(nnew[j])
+            nt = float(tokens)
+            hit[j] = False
+            ttft[j] = (p.prefill_a * nt + p.prefill_b * nt * nt) + 0.0
+            self._apply(ops[k])
+            lo = j + 1
+        serve_hits(lo, n)
+        if len(miss_at):
+            self._refresh()  # the device store is the source of truth again
+        # the hits' touches, in order, after the inserts they follow (a context is
+        # only ever touched after its own insert, so freq / last_access end equal)
+        if hit.any():
+            cc = np.ascontiguousarray(ctx[hit], np.int32)
+            ss = np.ascontiguousarray(stamps[hit])
+            self.eng.abi.check(self.eng.abi.store_touch_many(self.store.s, A.ptr(cc), A.ptr(ss), len(cc)))
+            self.n_device_calls += 1
+        out = [RequestRecord(trace[i], bool(hit[i]), int(tier_id[i]), self.names[int(meth[i])] if hit[i] else "",
+                             float(ratio[i]), float(ttft[i]), float(qual[i])) for i in range(n)]
         self.records.extend(out)
         return out
 
     def step(self, request: Request) -> RequestRecord:
         return self.run([request])[0]
-
-    def _flush_touches(self, cs: List[int], ss: List[int]):
-        if cs:
-            c = np.asarray(cs, np.int32)
-            s = np.asarray(ss, np.int64)
-            self.eng.abi.check(self.eng.abi.store_touch_many(self.store.s, A.ptr(c), A.ptr(s), len(cs)))
-            self.n_device_calls += 1
-            cs.clear()
-            ss.clear()
 
     def finish(self) -> ReplayResult:  # simulate.cpp:229-244
         placements: Dict[str, int] = {}
