@@ -497,6 +497,15 @@ extern "C" int ref_replay_dump(const char* scenario_path, const char* out_path, 
     j["warm_start"] = sc.warm_start;
     j["miss_store_bottom"] = sc.miss_store_bottom;
     j["drift"] = sc.drift.enabled;
+    j["seed"] = sc.seed;
+    j["drift_config"] = {{"threshold", sc.drift.threshold},
+                         {"min_samples", sc.drift.min_samples},
+                         {"window_size", sc.drift.window_size},
+                         {"gpu_window", sc.drift.gpu_window},
+                         {"max_batch", sc.drift.max_batch},
+                         {"duration", sc.drift.reprofile.duration},
+                         {"penalty", sc.drift.reprofile.penalty},
+                         {"noise_amplitude", sc.drift.reprofile.noise_amplitude}};
     j["n_truth"] = sc.truth.size();
     j["params"] = {{"alpha", sc.params.alpha}, {"prefill_a", sc.params.prefill_a},
                    {"prefill_b", sc.params.prefill_b}, {"bytes_per_token", sc.params.bytes_per_token}};
@@ -536,6 +545,8 @@ extern "C" int ref_replay_dump(const char* scenario_path, const char* out_path, 
                      {"mean_quality", m.mean_quality}, {"miss_fraction", m.miss_fraction}};
     for (const auto& [tier, f] : m.hit_fraction_by_tier) jr["metrics"]["hit_fraction_by_tier"][std::to_string(tier)] = f;
     jr["reprofile_count"] = res.reprofile_count;
+    for (const auto& w : res.profiling_windows)
+      jr["profiling_windows"].push_back({{"start", w.start}, {"duration", w.duration}, {"penalty", w.penalty}});
     j["result"] = jr;
     std::ofstream(out_path) << j.dump(1);
   });

@@ -12,9 +12,13 @@ greedy) on the device, after which the host copy is refreshed from one
 snapshot. Records, actions, final placements and metrics come out in the
 reference's `ReplayResult` shape.
 
-Not here yet (SURVEY §8 f3 and the baselines): drift tracking and
-re-profiling, `miss_store_bottom`, and the LRU / fixed / impress /
-prefill policies; `Replayer` refuses scenarios that need them.
+With drift tracking on (`maybe_reprofile`,
+simulate.cpp:102-128; quality.cpp:158-220) or `miss_store_bottom`, a
+request can change the profiles and reshuffle the whole store, so the loop
+runs request by request: a re-profile rebuilds the context's quality table
+from its truth curve (std::mt19937_64 noise, bit-exact), uploads the new
+profile set and runs `rearrange` on the device. Not here: the LRU / fixed /
+impress / prefill baselines.
 """
 from __future__ import annotations
 
@@ -56,6 +60,8 @@ class ReplayResult:  # proj/include/kvtier/simulate.hpp:82-90
     metrics: Dict[str, object]
     final_placements: Dict[str, int]
     actions: List[Tuple[str, str, int, str, float]]  # (kind, context, tier id, method, ratio)
+    profiling_windows: List[Tuple[float, float, float]] = field(default_factory=list)  # (start, duration, penalty)
+    reprofile_count: int = 0
 
 
 @dataclass
@@ -72,6 +78,8 @@ class Scenario:
     miss_store_bottom: bool = False
     drift: bool = False
     rule: str = "utility"
+    seed: int = 0
+    drift_config: Dict[str, float] = field(default_factory=dict)  # DriftConfig + ReprofileConfig
 
     @staticmethod
     def from_doc(doc: dict) -> Tuple["Scenario", List[Request]]:
@@ -91,7 +99,7 @@ class Scenario:
                  for c, per in (doc.get("truth") or {}).items()}
         sc = Scenario(tiers, params, space, profiles, truth, list(doc.get("order") or []),
                       bool(doc.get("warm_start")), bool(doc.get("miss_store_bottom")), bool(doc.get("drift")),
-                      doc.get("rule", "utility"))
+                      doc.get("rule", "utility"), int(doc.get("seed", 0)), dict(doc.get("drift_config") or {}))
         trace = [Request(float(r["t"]), r["context"], int(r.get("n_new_tokens", 0))) for r in doc["trace"]]
         return sc, trace
 
@@ -135,14 +143,96 @@ def synth_quality(sensitivity: float, shape_k: float, ratio: float) -> float:  #
     return min(max(1.0 - drop, 0.0), 1.0)
 
 
+class MT19937_64:
+    """std::mt19937_64 (C++11 [rand.predef]; the reference's Rng engine,
+    proj/include/kvtier/rng.hpp), bit-exact."""
+    _MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        mt = [seed & self._MASK]
+        for i in range(1, 312):
+            mt.append((6364136223846793005 * (mt[-1] ^ (mt[-1] >> 62)) + i) & self._MASK)
+        self.mt, self.i = mt, 312
+
+    def next_u64(self) -> int:
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                x = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                xa = (x >> 1) ^ (0xB5026F5AA96619E9 if x & 1 else 0)
+                mt[k] = mt[(k + 156) % 312] ^ xa
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self._MASK
+
+    def uniform(self, lo: float, hi: float) -> float:  # rng.hpp uniform01 / uniform
+        return lo + (hi - lo) * (float(self.next_u64() >> 11) * 2.0 ** -53)
+
+
+@dataclass
+class DriftState:  # proj/include/kvtier/quality.hpp:62-72
+    window_size: int = 0
+    observed_sum: float = 0.0
+    profiled_sum: float = 0.0
+    n_observations: int = 0
+    window: List[Tuple[float, float]] = field(default_factory=list)
+
+    def _n(self) -> int:
+        return self.n_observations if self.window_size == 0 else len(self.window)
+
+    def observed_mean(self) -> float:
+        n = self._n()
+        return 0.0 if n == 0 else self.observed_sum / float(n)
+
+    def profiled_mean(self) -> float:
+        n = self._n()
+        return 0.0 if n == 0 else self.profiled_sum / float(n)
+
+    def record(self, predicted: float, observed: float):  # quality.cpp:158-180 record_observation
+        if self.window_size == 0:
+            self.profiled_sum += predicted
+            self.observed_sum += observed
+            self.n_observations += 1
+            return
+        self.window.append((predicted, observed))
+        if len(self.window) > self.window_size:
+            self.window.pop(0)
+        self.profiled_sum = 0.0
+        self.observed_sum = 0.0
+        for pr, ob in self.window:
+            self.profiled_sum += pr
+            self.observed_sum += ob
+        self.n_observations += 1
+
+
+def reprofile(old: ContextProfile, truth: Dict[str, Tuple[float, float]], noise_seed: int,
+              noise: float) -> ContextProfile:  # proj/src/quality.cpp:191-220
+    rng = MT19937_64(noise_seed)
+    table = {}
+    for m in sorted(old.quality_table, key=lambda x: x.encode()):  # std::map order
+        values = list(old.quality_table[m])
+        curve = truth.get(m)
+        for i, r in enumerate(old.ratio_grid):
+            q = synth_quality(curve[0], curve[1], r) if curve is not None else values[i]
+            if noise > 0.0:
+                q += rng.uniform(-noise, noise)
+            values[i] = min(max(q, 0.0), 1.0)
+        for i in range(1, len(values)):
+            values[i] = max(values[i], values[i - 1])
+        values[-1] = 1.0
+        table[m] = values
+    return ContextProfile(old.context, old.original_size_bytes, old.frequency, list(old.ratio_grid), table)
+
+
 class Replayer:
     """kvtier::Replayer (joint policy) on the device store."""
 
     def __init__(self, eng: Engine, scenario: Scenario):
-        if scenario.drift:
-            raise NotImplementedError("drift / re-profiling (SURVEY §8 f3) is not in the serve loop yet")
-        if scenario.miss_store_bottom:
-            raise NotImplementedError("miss_store_bottom is not in the serve loop yet")
         self.sc = scenario
         self.eng = eng
         self.tiers = sorted_tiers(scenario.tiers)  # Replayer keeps the validated order
@@ -159,6 +249,14 @@ class Replayer:
         self.last_t: Optional[float] = None
         self.n_device_calls = 0
         self._qcache: Dict[Tuple[int, int, float], float] = {}
+        dc = scenario.drift_config
+        self.window_size = int(dc.get("window_size", 0))
+        self.drift_states: Dict[int, DriftState] = {}
+        self.windows: List[Tuple[float, float, float]] = []  # (start, duration, penalty)
+        self.reprofile_count = 0
+        self.arrivals: List[float] = []
+        self._arr_lo = 0
+        self.rp_rng = MT19937_64((scenario.seed ^ 0x9E3779B97F4A7C15) & MT19937_64._MASK)
         if scenario.warm_start:
             self._warm_up()
         self._refresh()
@@ -243,6 +341,8 @@ class Replayer:
         n = len(trace)
         if n == 0:
             return []
+        if self.sc.drift or self.sc.miss_store_bottom:
+            return self._run_sequential(trace)
         t = np.fromiter((r.t for r in trace), np.float64, n)
         nnew = np.fromiter((r.n_new_tokens for r in trace), np.int64, n)
         try:
@@ -331,6 +431,120 @@ class Replayer:
         self.records.extend(out)
         return out
 
+    # -- request by request (drift tracking / re-profiling, miss_store_bottom)
+    def _gpu_free(self, now: float) -> bool:  # simulate.cpp:88-93
+        gw = float(self.sc.drift_config.get("gpu_window", 1.0))
+        while self._arr_lo < len(self.arrivals) and self.arrivals[self._arr_lo] <= now - gw:
+            self._arr_lo += 1
+        return len(self.arrivals) - self._arr_lo < int(self.sc.drift_config.get("max_batch", 8))
+
+    def _active_penalty(self, now: float) -> float:  # simulate.cpp:95-100
+        pen = 0.0
+        for start, dur, p in self.windows:
+            if now >= start and now < start + dur:
+                pen += p
+        return pen
+
+    def _upload_profiles(self):
+        self.arrays = ProfileArrays.from_profiles(list(self.prof.values()), self.sc.space)
+        self.ps = self.eng.pset(self.arrays)
+        self._qcache.clear()
+
+    def _maybe_reprofile(self, c: int, now: float):  # simulate.cpp:102-128
+        if not self.sc.drift:
+            return
+        st = self.drift_states.get(c)
+        if st is None:
+            return
+        dc = self.sc.drift_config
+        thr = float(dc.get("threshold", 0.3))
+        if not (self._gpu_free(now) and st.n_observations >= int(dc.get("min_samples", 10))
+                and (st.profiled_mean() - st.observed_mean()) > thr):  # quality.cpp:182-189 should_reprofile
+            return
+        cid = self.arrays.ids[c]
+        truth = self.sc.truth.get(cid)
+        if truth is None:
+            return
+        seed = self.rp_rng.next_u64()
+        self.prof[cid] = reprofile(self.prof[cid], truth, seed, float(dc.get("noise_amplitude", 0.0)))
+        self.windows.append((now, float(dc.get("duration", 2.0)), float(dc.get("penalty", 0.5))))
+        self.reprofile_count += 1
+        self.drift_states[c] = DriftState(self.window_size)
+        self._upload_profiles()
+        self._record_actions(self.store.rearrange(self.ps, self.sc.space, self.sc.params, rule=self.rule))
+        self.n_device_calls += 1
+        self._refresh()
+
+    def _record_actions(self, acts):
+        ids = self.arrays.ids
+        for a in acts:
+            self.actions.append((KIND_NAMES[int(a["kind"])], ids[int(a["ctx"])], int(a["tier_id"]),
+                                 self.names[int(a["method"])], float(a["ratio"])))
+
+    def _run_sequential(self, trace: Sequence[Request]) -> List[RequestRecord]:
+        p = self.sc.params
+        out: List[RequestRecord] = []
+        touch_c: List[int] = []
+        touch_s: List[int] = []
+        for r in trace:
+            if self.last_t is not None and r.t < self.last_t:
+                raise A.AbiError(A.KVT_ETRACE, f"trace timestamps are not monotone (t={r.t} after t={self.last_t})")
+            if r.n_new_tokens < 0:
+                raise A.AbiError(A.KVT_ETRACE, f"negative n_new_tokens for context {r.context}")
+            self.last_t = r.t
+            self.arrivals.append(r.t)
+            c = self.arrays.index.get(r.context)
+            if c is None:
+                raise A.AbiError(A.KVT_ETRACE, f"trace names unknown context {r.context}")
+            prof = self.prof[r.context]
+            stamp = self.stamp
+            self.stamp += 1
+            penalty = self._active_penalty(r.t)
+            ti = int(self.tier_index[c])
+            if ti >= 0:  # hit
+                tier = self.tiers[ti]
+                m, ratio = int(self.method[c]), float(self.ratio[c])
+                name = self.names[m]
+                load = load_time(compressed_size(prof.original_size_bytes, ratio), tier, self.ovh[m])
+                ttft = load + prefill_time(r.n_new_tokens, p) + penalty
+                predicted = quality_of(prof, name, ratio)
+                truth = self.sc.truth.get(r.context)
+                achieved = synth_quality(*truth[name], ratio) if truth is not None else predicted
+                rec = RequestRecord(r, True, tier.tier_id, name, ratio, ttft, achieved)
+                touch_c.append(c)
+                touch_s.append(stamp)
+                if self.sc.drift and truth is not None:  # simulate.cpp:186-193
+                    self.drift_states.setdefault(c, DriftState(self.window_size)).record(predicted, achieved)
+            else:  # miss
+                tokens = token_count(prof.original_size_bytes, p) + r.n_new_tokens
+                rec = RequestRecord(r, False, -1, "", 1.0, prefill_time(tokens, p) + penalty, 1.0)
+                self._touch(touch_c, touch_s)
+                if self.sc.miss_store_bottom:  # simulate.cpp:203-216: bottom tier at (first method, 1.0), rearrange
+                    bottom = len(self.tiers) - 1
+                    self.store.add(c, bottom, 0, 1.0, prof.original_size_bytes, 1, stamp)
+                    self.actions.append(("insert", r.context, self.tiers[bottom].tier_id, self.names[0], 1.0))
+                    self._record_actions(self.store.rearrange(self.ps, self.sc.space, self.sc.params, rule=self.rule))
+                    self.n_device_calls += 2
+                else:
+                    self._insert([c], [1], [stamp])
+                self._refresh()
+            out.append(rec)
+            if self.sc.drift:
+                self._touch(touch_c, touch_s)  # a re-profile's rearrange re-inserts with the touched stats
+                self._maybe_reprofile(c, r.t)
+        self._touch(touch_c, touch_s)
+        self.records.extend(out)
+        return out
+
+    def _touch(self, cs: List[int], ss: List[int]):
+        if cs:
+            cc = np.asarray(cs, np.int32)
+            st = np.asarray(ss, np.int64)
+            self.eng.abi.check(self.eng.abi.store_touch_many(self.store.s, A.ptr(cc), A.ptr(st), len(cs)))
+            self.n_device_calls += 1
+            cs.clear()
+            ss.clear()
+
     def step(self, request: Request) -> RequestRecord:
         return self.run([request])[0]
 
@@ -342,7 +556,8 @@ class Replayer:
                 key = "tier%d:%s@%s" % (tier.tier_id, self.names[int(self.method[c])],
                                         "%.6g" % float(self.ratio[c]))
                 placements[key] = placements.get(key, 0) + 1
-        return ReplayResult(list(self.records), aggregate(self.records), placements, list(self.actions))
+        return ReplayResult(list(self.records), aggregate(self.records), placements, list(self.actions),
+                            list(self.windows), self.reprofile_count)
 
 
 def _nearest_rank(sorted_v: List[float], pct: float) -> float:  # simulate.cpp:255-261

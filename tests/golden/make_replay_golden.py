@@ -17,14 +17,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "..", "..", "oracle", "_ref", "libkvtier_ref.so")
 SCEN = "/root/reference/proj/scenarios"
 
-# (fixture name, scenario, loader overrides): drift / re-profiling is SURVEY
-# §8 f3 (not in the native serve loop yet), so it is switched off here
+# (fixture name, scenario, loader overrides)
 CASES = [
     ("fig2_warm", "fig2", []),
     ("fig2_cold", "fig2", ["warm_start=false"]),
     ("bimodal_warm", "bimodal", []),
     ("bimodal_cold", "bimodal", ["warm_start=false"]),
     ("drift_truth_cold", "drift", ["drift.enabled=false", "warm_start=false"]),
+    ("drift_warm", "drift", []),
+    ("drift_cold", "drift", ["warm_start=false"]),
+    ("drift_window", "drift", ["drift.window_size=8", "drift.threshold=0.2"]),
+    ("drift_noise", "drift", ["drift.noise=0.05"]),
+    ("bimodal_msb", "bimodal", ["warm_start=false", "miss_store_bottom=true"]),
 ]
 
 

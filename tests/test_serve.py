@@ -1,4 +1,5 @@
-"""Serve loop against the reference's own replay.
+"""Serve loop (with f3's drift / re-profiling) against the
+reference's own replay.
 
 tests/golden/make_replay_golden.py ran the unmodified reference (scenario
 loader + kvtier::replay) on its shipped scenarios and stored the expanded
@@ -42,12 +43,25 @@ def _check(eng, doc):
     assert res.final_placements == ref["final_placements"]
     for k, v in ref["metrics"].items():
         assert res.metrics[k] == v, k
+    assert res.reprofile_count == ref["reprofile_count"]
+    assert res.profiling_windows == [(w["start"], w["duration"], w["penalty"]) for w in ref.get("profiling_windows", [])]
     return len(res.records), len(res.actions)
 
 
 def test_replay_fixtures_present():
     names = {os.path.basename(p) for p in GOLD}
-    assert {"replay_fig2_warm.json.gz", "replay_bimodal_cold.json.gz", "replay_drift_truth_cold.json.gz"} <= names
+    assert {"replay_fig2_warm.json.gz", "replay_bimodal_cold.json.gz", "replay_drift_truth_cold.json.gz",
+            "replay_drift_warm.json.gz", "replay_drift_noise.json.gz"} <= names
+    # the drift fixtures re-profile and rearrange many times
+    assert _load(os.path.join(os.path.dirname(GOLD[0]), "replay_drift_warm.json.gz"))["result"]["reprofile_count"] > 5
+
+
+def test_mt19937_64_known_answer():
+    from paper_2512_14946_b200.serve import MT19937_64
+    g = MT19937_64(5489)  # C++11 [rand.predef]: the 10000th output of a default-seeded mt19937_64
+    for _ in range(9999):
+        g.next_u64()
+    assert g.next_u64() == 9981545732273789042
 
 
 @pytest.mark.parametrize("path", GOLD, ids=[os.path.basename(p)[7:-8] for p in GOLD])
@@ -62,13 +76,9 @@ def test_gpu_serve_loop_matches_reference(gpu_abi, path):
     assert n_req > 0
 
 
-def test_serve_loop_rejects_what_it_does_not_model(oracle_abi):
+def test_serve_loop_trace_errors(oracle_abi):
     doc = _load(GOLD[0])
     sc, trace = Scenario.from_doc(doc)
-    sc.drift = True
-    with pytest.raises(NotImplementedError):
-        Replayer(Engine(oracle_abi), sc)
-    sc.drift = False
     rp = Replayer(Engine(oracle_abi), sc)
     with pytest.raises(A.AbiError):
         rp.run([Request(2.0, trace[0].context), Request(1.0, trace[0].context)])  # non-monotone trace
