@@ -327,6 +327,22 @@ int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
 /* the CPU restatement: plain memcpy (host pointers only) */
 int orc_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
 
+/* ---- oracle_mckp (proj/src/placement.cpp:300-372): the exact
+ * one-configuration-per-context optimum under the tier capacities, by
+ * branch and bound over every context's candidates in candidate_preferred
+ * order (the reference's DFS result: the maximal total utility, ties to
+ * the lexicographically first assignment). The search runs on the GPU,
+ * one subtree per thread. Fails (KVT_EVALIDATION) when the assignment space
+ * exceeds max_assignments, a context has no scorable configuration, or no
+ * assignment fits. out[n]: each context's chosen candidate. */
+int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
+                    const kvt_space* space, const kvt_params* params, double max_assignments,
+                    double* total_utility, kvt_best* out);
+/* the reference's own oracle_mckp behind the same signature (test glue, oracle/_ref) */
+int ref_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
+                    const kvt_space* space, const kvt_params* params, double max_assignments,
+                    double* total_utility, kvt_best* out);
+
 /* Device-pointer variants and timing helpers used by the bench. */
 /* Synchronise the handle's stream. */
 int kvt_sync(kvt_handle* h);

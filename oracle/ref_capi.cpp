@@ -237,6 +237,39 @@ int ref_best_config(kvt_handle*, const kvt_pset* pc, const kvt_tier* tiers, int3
   });
 }
 
+int ref_oracle_mckp(kvt_handle*, const kvt_pset* pc, const kvt_tier* tiers, int32_t n_tiers,
+                    const kvt_space* sp, const kvt_params* params, double max_assignments,
+                    double* total_utility, kvt_best* out) {
+  auto* p = const_cast<kvt_pset*>(pc);
+  return guard([&] {
+    const auto space = make_space(sp);
+    const auto& map = p->profiles(sp);
+    std::vector<kvtier::ContextProfile> profs;
+    for (const auto& [id, prof] : map) profs.push_back(prof);
+    kvtier::UtilityParams up;
+    up.alpha = params->alpha;
+    const auto res = kvtier::oracle_mckp(profs, make_tiers(tiers, n_tiers), space, up, max_assignments);
+    *total_utility = res.total_utility;
+    int32_t c = 0;
+    for (const auto& [id, prof] : map) {
+      const auto& best = res.assignment.at(id);
+      kvt_best& b = out[c++];
+      std::memset(&b, 0, sizeof b);
+      b.tier_index = best.tier_index;
+      b.tier_id = best.tier_id;
+      b.method = method_index(space, best.config.method);
+      int r = 0;
+      while (space.ratios()[r] != best.config.ratio) ++r;
+      b.ratio_index = r;
+      b.ratio = best.config.ratio;
+      b.size_bytes = best.size_bytes;
+      b.quality = best.quality;
+      b.ttft = best.ttft;
+      b.utility = best.utility;
+    }
+  });
+}
+
 int ref_store_create(kvt_handle*, const kvt_tier* tiers, int32_t n_tiers, int32_t n_ctx,
                      kvt_store** out) {
   return guard([&] {

@@ -158,6 +158,9 @@ PRODUCT_EXTRA_SIGS = {
     "tier_host_free": (C.c_int, [P]),
 }
 TIER_SIGS = {"tier_moves": (C.c_int, [P, C.POINTER(Move), i64])}
+# kvt_oracle_mckp (product) / ref_oracle_mckp (reference glue): bound when exported
+MCKP_SIGS = {"oracle_mckp": (C.c_int, [P, P, C.POINTER(Tier), i32, C.POINTER(Space), C.POINTER(Params), f64,
+                                       C.POINTER(C.c_double), P])}
 
 
 class AbiError(RuntimeError):
@@ -187,6 +190,8 @@ class Abi:
             sigs.update(PRODUCT_EXTRA_SIGS)
         if hasattr(self.lib, prefix + "tier_moves"):
             sigs.update(TIER_SIGS)
+        if hasattr(self.lib, prefix + "oracle_mckp"):
+            sigs.update(MCKP_SIGS)
         for name, (res, args) in sigs.items():
             fn = getattr(self.lib, prefix + name)
             fn.restype = res

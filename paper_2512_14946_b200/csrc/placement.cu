@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <limits>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -394,6 +395,312 @@ extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_
   if (ttft) KVT_CUDA_TRY(cudaMemcpyAsync(ttft, t.ttft, b_u, cudaMemcpyDeviceToHost, s));
   if (utility) KVT_CUDA_TRY(cudaMemcpyAsync(utility, t.u, b_u, cudaMemcpyDeviceToHost, s));
   KVT_CUDA_TRY(cudaStreamSynchronize(s));
+  return KVT_OK;
+}
+
+// ---------------------------------------------------------------- oracle_mckp
+// proj/src/placement.cpp:300-372. Every context's scorable candidates in
+// candidate_preferred order (stable over the enumeration order); a branch
+// and bound over one-candidate-per-context assignments under the finite
+// tiers' capacities. The first d contexts' choices index the GPU threads
+// (mixed radix, context 0 most significant = the DFS's lexicographic
+// order); each thread runs the reference's DFS over the rest of its
+// subtree. A thread keeps the first maximal leaf of its subtree (strictly
+// better only), so the maximal total with the smallest prefix index, then
+// the thread's pick, is the reference's result: the first optimum in DFS
+// order. Pruning: the reference's own test within a thread (bound <= its
+// best), and a strict test against the best total any thread has reached
+// (never cuts a subtree that could tie), shared as an order-preserving key.
+constexpr int kMckpMaxCtx = 24;
+constexpr long long kMckpMaxThreads = 1 << 18;
+
+__device__ __forceinline__ unsigned long long mckp_key(double v) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(v, 0.0)));
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double mckp_val(unsigned long long k) {
+  const unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__global__ void __launch_bounds__(128) k_mckp(const double* __restrict__ cu, const long long* __restrict__ csz,
+                                              const int* __restrict__ ctier, const int* __restrict__ off,
+                                              const int* __restrict__ cnt, const double* __restrict__ suffix,
+                                              DevTiers TT, int n, int d, long long nprefix,
+                                              unsigned long long* __restrict__ gbest, double* __restrict__ out_total,
+                                              int* __restrict__ out_found, int* __restrict__ out_choice) {
+  const long long pfx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (pfx >= nprefix) return;
+  int choice[kMckpMaxCtx], k[kMckpMaxCtx], best_choice[kMckpMaxCtx];
+  double tot[kMckpMaxCtx + 1];
+  long long used[KVT_MAX_TIERS];
+  for (int t = 0; t < KVT_MAX_TIERS; ++t) used[t] = 0;
+  long long rem = pfx;
+  for (int i = d - 1; i >= 0; --i) {
+    choice[i] = static_cast<int>(rem % cnt[i]);
+    rem /= cnt[i];
+  }
+  tot[0] = 0.0;
+  out_found[pfx] = 0;
+  for (int i = 0; i < d; ++i) {  // the prefix: the same capacity test and running sum as the DFS
+    const int c = off[i] + choice[i], t = ctier[c];
+    if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) return;
+    used[t] += csz[c];
+    tot[i + 1] = __dadd_rn(tot[i], cu[c]);
+  }
+  double best = 0.0;
+  bool found = false;
+  int lvl = d;
+  bool enter = true;
+  while (true) {
+    if (enter) {  // node entry (the reference's dfs(i, total) prologue)
+      const double bound = __dadd_rn(tot[lvl], suffix[lvl]);
+      if ((found && bound <= best) || bound < mckp_val(*const_cast<volatile unsigned long long*>(gbest))) {
+        enter = false;  // pruned: back to the parent
+      } else if (lvl == n) {
+        best = tot[n];
+        found = true;
+        for (int i = 0; i < n; ++i) best_choice[i] = choice[i];
+        atomicMax(gbest, mckp_key(best));
+        enter = false;
+      } else {
+        k[lvl] = 0;
+        enter = false;
+        goto try_children;
+      }
+      // go up one level, undo that level's choice, advance it
+      if (lvl == d) break;
+      --lvl;
+      {
+        const int c = off[lvl] + choice[lvl];
+        used[ctier[c]] -= csz[c];
+      }
+      ++k[lvl];
+    }
+  try_children:
+    while (k[lvl] < cnt[lvl]) {
+      const int c = off[lvl] + k[lvl], t = ctier[c];
+      if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) {
+        ++k[lvl];
+        continue;
+      }
+      used[t] += csz[c];
+      choice[lvl] = k[lvl];
+      tot[lvl + 1] = __dadd_rn(tot[lvl], cu[c]);
+      ++lvl;
+      enter = true;
+      break;
+    }
+    if (enter) continue;
+    // children exhausted
+    if (lvl == d) break;
+    --lvl;
+    {
+      const int c = off[lvl] + choice[lvl];
+      used[ctier[c]] -= csz[c];
+    }
+    ++k[lvl];
+  }
+  if (found) {
+    out_found[pfx] = 1;
+    out_total[pfx] = best;
+    for (int i = d; i < n; ++i) out_choice[pfx * n + i] = best_choice[i];
+    for (int i = 0; i < d; ++i) out_choice[pfx * n + i] = best_choice[i];
+  }
+}
+
+// the winning subtree: maximal total, then the smallest prefix index
+__global__ void __launch_bounds__(1024) k_mckp_pick(const double* __restrict__ tot, const int* __restrict__ found,
+                                                     long long nprefix, long long* __restrict__ win) {
+  __shared__ double sv[1024];
+  __shared__ long long si[1024];
+  const int tid = threadIdx.x;
+  double bv = 0.0;
+  long long bi = -1;
+  for (long long i = tid; i < nprefix; i += 1024)
+    if (found[i] && (bi < 0 || tot[i] > bv)) {
+      bv = tot[i];
+      bi = i;
+    }
+  sv[tid] = bv;
+  si[tid] = bi;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (tid < w) {
+      const double ov = sv[tid + w];
+      const long long oi = si[tid + w];
+      if (oi >= 0 && (si[tid] < 0 || ov > sv[tid] || (ov == sv[tid] && oi < si[tid]))) {
+        sv[tid] = ov;
+        si[tid] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *win = si[0];
+}
+
+extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
+                               const kvt_space* space, const kvt_params* params, double max_assignments,
+                               double* total_utility, kvt_best* out) {
+  DevSpace S;
+  DevTiers T;
+  int rc;
+  if ((rc = resolve_space(space, &S))) return rc;
+  if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
+  if (p->dev.M != S.M) return set_error(KVT_EINVAL, "profile set / space method count mismatch");
+  const int n = p->dev.n, M = S.M, R = S.R, TT = T.T, MR = M * R;
+  if (n > kMckpMaxCtx) return set_error(KVT_EVALIDATION, "instance too large for the exact solver");
+  // K1 candidate tables for every (context, tier, method, ratio)
+  std::vector<int64_t> size(size_t(n) * R);
+  std::vector<double> q(size_t(n) * MR), tt(size_t(n) * TT * MR), u(size_t(n) * TT * MR);
+  std::vector<uint8_t> valid(size_t(n) * MR);
+  if (n > 0 && (rc = kvt_score_candidates(h, p, tiers, n_tiers, space, params, size.data(), q.data(), valid.data(),
+                                          tt.data(), u.data())))
+    return rc;
+  struct Cand {
+    int t, m, r;
+  };
+  std::vector<std::vector<Cand>> cands(n);
+  double assignments = 1.0;
+  for (int c = 0; c < n; ++c) {
+    auto& v = cands[c];
+    for (int t = 0; t < TT; ++t)  // all_candidates order: tier, method, ratio (descending)
+      for (int m = 0; m < M; ++m)
+        for (int r = 0; r < R; ++r)
+          if (valid[size_t(c) * MR + size_t(m) * R + r]) v.push_back({t, m, r});
+    if (v.empty()) return set_error(KVT_EVALIDATION, "no scorable configuration for context " + std::to_string(c));
+    auto U = [&](const Cand& x) { return u[(size_t(c) * TT + x.t) * MR + size_t(x.m) * R + x.r]; };
+    auto Q = [&](const Cand& x) { return q[size_t(c) * MR + size_t(x.m) * R + x.r]; };
+    std::stable_sort(v.begin(), v.end(), [&](const Cand& a, const Cand& b) {  // candidate_preferred (utility rule)
+      if (U(a) != U(b)) return U(a) > U(b);
+      if (Q(a) != Q(b)) return Q(a) > Q(b);
+      if (T.id[a.t] != T.id[b.t]) return T.id[a.t] < T.id[b.t];
+      if (S.ratio[a.r] != S.ratio[b.r]) return S.ratio[a.r] > S.ratio[b.r];
+      return S.name_rank[a.m] < S.name_rank[b.m];
+    });
+    assignments *= static_cast<double>(v.size());
+    if (assignments > max_assignments)
+      return set_error(KVT_EVALIDATION, "instance too large for the exact solver: assignment space exceeds the limit");
+  }
+  // flattened candidates + the optimistic completion bound (right to left, like the reference)
+  std::vector<double> cu_h;
+  std::vector<long long> csz_h;
+  std::vector<int> ct_h, off_h(n + 1, 0), cnt_h(n);
+  for (int c = 0; c < n; ++c) {
+    off_h[c] = static_cast<int>(cu_h.size());
+    cnt_h[c] = static_cast<int>(cands[c].size());
+    for (const Cand& x : cands[c]) {
+      cu_h.push_back(u[(size_t(c) * TT + x.t) * MR + size_t(x.m) * R + x.r]);
+      csz_h.push_back(size[size_t(c) * R + x.r]);
+      ct_h.push_back(x.t);
+    }
+  }
+  std::vector<double> suffix(n + 1, 0.0);
+  for (int i = n; i-- > 0;) suffix[i] = suffix[i + 1] + cu_h[off_h[i]];
+  // an incumbent for the shared prune: the first fitting candidate of every
+  // context in order (a feasible total when it completes), lowered by a
+  // relative 1e-12 so that rounding in the bounds never cuts the optimum
+  double incumbent = -std::numeric_limits<double>::infinity();
+  {
+    std::vector<long long> used(TT, 0);
+    double tot = 0.0;
+    bool ok = true;
+    for (int c = 0; c < n && ok; ++c) {
+      ok = false;
+      for (int k = 0; k < cnt_h[c]; ++k) {
+        const int j = off_h[c] + k, t = ct_h[j];
+        if (!T.unlimited[t] && used[t] + csz_h[j] > T.cap[t]) continue;
+        used[t] += csz_h[j];
+        tot += cu_h[j];
+        ok = true;
+        break;
+      }
+    }
+    if (ok && n > 0) incumbent = tot - std::fabs(tot) * 1e-12 - 1e-300;
+  }
+  // subtrees: enough prefixes to fill the GPU when the space is large, few
+  // when it is small (every thread's subtree is then tiny anyway)
+  const double space_sz = assignments;
+  const long long target = space_sz > 1e6 ? kMckpMaxThreads : 4096;
+  int d = 0;
+  long long nprefix = 1;
+  while (d < n && nprefix * cnt_h[d] <= target) nprefix *= cnt_h[d++];
+  // device buffers
+  const size_t nc = std::max<size_t>(1, cu_h.size());
+  const size_t bytes = nc * (8 + 8 + 4) + size_t(n + 1) * 4 * 2 + size_t(n + 1) * 8 + 8 +
+                       size_t(nprefix) * (8 + 4 + 4 * size_t(std::max(n, 1))) + 64 * 8;
+  char* dbuf = nullptr;
+  KVT_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), bytes, h->stream));
+  size_t o = 0;
+  auto carve = [&](size_t b) {
+    char* r = dbuf + o;
+    o += (b + 63) & ~size_t(63);
+    return r;
+  };
+  auto* d_cu = reinterpret_cast<double*>(carve(nc * 8));
+  auto* d_csz = reinterpret_cast<long long*>(carve(nc * 8));
+  auto* d_ct = reinterpret_cast<int*>(carve(nc * 4));
+  auto* d_off = reinterpret_cast<int*>(carve(size_t(n + 1) * 4));
+  auto* d_cnt = reinterpret_cast<int*>(carve(size_t(n + 1) * 4));
+  auto* d_suf = reinterpret_cast<double*>(carve(size_t(n + 1) * 8));
+  auto* d_gbest = reinterpret_cast<unsigned long long*>(carve(8));
+  auto* d_tot = reinterpret_cast<double*>(carve(size_t(nprefix) * 8));
+  auto* d_found = reinterpret_cast<int*>(carve(size_t(nprefix) * 4));
+  auto* d_choice = reinterpret_cast<int*>(carve(size_t(nprefix) * 4 * size_t(std::max(n, 1))));
+  cudaStream_t st = h->stream;
+  if (!cu_h.empty()) {
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_cu, cu_h.data(), cu_h.size() * 8, cudaMemcpyHostToDevice, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_csz, csz_h.data(), csz_h.size() * 8, cudaMemcpyHostToDevice, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_ct, ct_h.data(), ct_h.size() * 4, cudaMemcpyHostToDevice, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_off, off_h.data(), size_t(n) * 4, cudaMemcpyHostToDevice, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_cnt, cnt_h.data(), size_t(n) * 4, cudaMemcpyHostToDevice, st));
+  }
+  KVT_CUDA_TRY(cudaMemcpyAsync(d_suf, suffix.data(), size_t(n + 1) * 8, cudaMemcpyHostToDevice, st));
+  {
+    unsigned long long key = 0;  // key 0 < every real total's key (no incumbent)
+    if (std::isfinite(incumbent)) {
+      uint64_t b;
+      std::memcpy(&b, &incumbent, 8);
+      key = (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+    }
+    KVT_CUDA_TRY(cudaMemcpyAsync(d_gbest, &key, 8, cudaMemcpyHostToDevice, st));
+    KVT_CUDA_TRY(cudaStreamSynchronize(st));  // key lives on this frame
+  }
+  k_mckp<<<static_cast<int>((nprefix + 127) / 128), 128, 0, st>>>(d_cu, d_csz, d_ct, d_off, d_cnt, d_suf, T, n, d,
+                                                                  nprefix, d_gbest, d_tot, d_found, d_choice);
+  h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  auto* d_win = reinterpret_cast<long long*>(d_gbest);  // gbest is dead once the search is done
+  k_mckp_pick<<<1, 1024, 0, st>>>(d_tot, d_found, nprefix, d_win);
+  h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
+  long long win = -1;
+  KVT_CUDA_TRY(cudaMemcpyAsync(&win, d_win, 8, cudaMemcpyDeviceToHost, st));
+  KVT_CUDA_TRY(cudaStreamSynchronize(st));
+  double best_total = 0.0;
+  std::vector<int> choice_h(std::max(n, 1));
+  if (win >= 0) {
+    KVT_CUDA_TRY(cudaMemcpyAsync(&best_total, d_tot + win, 8, cudaMemcpyDeviceToHost, st));
+    KVT_CUDA_TRY(cudaMemcpyAsync(choice_h.data(), d_choice + size_t(win) * n, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+  }
+  KVT_CUDA_TRY(cudaFreeAsync(dbuf, st));
+  KVT_CUDA_TRY(cudaStreamSynchronize(st));
+  if (win < 0) return set_error(KVT_EVALIDATION, "no feasible one-config-per-context assignment exists");
+  *total_utility = best_total;
+  for (int c = 0; c < n; ++c) {
+    const Cand& x = cands[c][choice_h[c]];
+    kvt_best& b = out[c];
+    std::memset(&b, 0, sizeof b);
+    b.tier_index = x.t;
+    b.tier_id = T.id[x.t];
+    b.method = x.m;
+    b.ratio_index = x.r;
+    b.ratio = S.ratio[x.r];
+    b.size_bytes = size[size_t(c) * R + x.r];
+    b.quality = q[size_t(c) * MR + size_t(x.m) * R + x.r];
+    b.ttft = tt[(size_t(c) * TT + x.t) * MR + size_t(x.m) * R + x.r];
+    b.utility = u[(size_t(c) * TT + x.t) * MR + size_t(x.m) * R + x.r];
+  }
   return KVT_OK;
 }
 

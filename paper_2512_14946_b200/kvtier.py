@@ -207,6 +207,17 @@ class Engine:
                                             C.byref(params.c), rule, A.ptr(out)))
         return out
 
+    def oracle_mckp(self, ps: "PSet", tiers, space: CandidateSpace, params: UtilityParams,
+                    max_assignments: float = 1e7):
+        """oracle_mckp (proj/src/placement.cpp:300-372): the exact
+        one-configuration-per-context optimum; (total utility, BEST_DTYPE[n])."""
+        out = np.zeros(ps.arrays.n, A.BEST_DTYPE)
+        total = C.c_double()
+        tc = _tiers_c(tiers)
+        self.abi.check(self.abi.oracle_mckp(self.h, ps.p, tc, len(tiers), C.byref(space.c), C.byref(params.c),
+                                            float(max_assignments), C.byref(total), A.ptr(out)))
+        return total.value, out
+
     def store(self, tiers, n_ctx: int, space: Optional[CandidateSpace] = None) -> "StoreState":
         return StoreState(self, tiers, n_ctx, space)
 
