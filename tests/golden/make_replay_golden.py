@@ -29,6 +29,7 @@ CASES = [
     ("drift_window", "drift", ["drift.window_size=8", "drift.threshold=0.2"]),
     ("drift_noise", "drift", ["drift.noise=0.05"]),
     ("bimodal_msb", "bimodal", ["warm_start=false", "miss_store_bottom=true"]),
+    ("bimodal_qargmax", "bimodal", ["warm_start=false", "policy=joint-qargmax"]),
 ]
 
 
