@@ -153,7 +153,7 @@ extern "C" int kvt_kv_generate(kvt_handle* h, const kvt_kv_shape* s, uint64_t se
 }
 
 // ------------------------------------------- K rows through a smem ring
-constexpr int kRingStages = 4;  // K streamed through smem in 64-token (16 KB) bulk-copy stages
+constexpr int kRingStages = 3;  // K streamed through smem in 64-token (16 KB) bulk-copy stages
 constexpr int kRingRows = 64;
 constexpr size_t kRingBytes = size_t(kRingStages) * kRingRows * 256;
 
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
 // the same rows (~18 slices x 2 MiB in flight: L2 hits) for the dot
 // products. Bit-identical to k_keydiff_sum + k_keydiff_score.
 constexpr int kKdC = 8;
-__global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
+__global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
     k_keydiff_cluster(const uint4* __restrict__ K, float* __restrict__ out, int T) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
@@ -403,7 +403,7 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
   extern __shared__ __align__(16) uint8_t kd_raw[];
   uint4* ring = reinterpret_cast<uint4*>(kd_raw);
   float* kinv = reinterpret_cast<float*>(kd_raw + kRingBytes);
-  __shared__ long long part[16][kD];
+  __shared__ int32_t part[8][kD];
   __shared__ long long sfix[kD];
   __shared__ float sdir[kD];
   __shared__ __align__(8) uint64_t full[kRingStages];
@@ -433,12 +433,16 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 2)
     }
   });
 #pragma unroll
-  for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = static_cast<int32_t>(acc[i] - cnt * 0x4B400000u);
+  for (int i = 0; i < 8; ++i) {  // the warp's two half-warps first (|sum| < 2^31: <= per / 16 rows each)
+    int32_t x = static_cast<int32_t>(acc[i] - cnt * 0x4B400000u);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    if ((tid & 16) == 0) part[tid >> 5][l16 * 8 + i] = x;
+  }
   __syncthreads();
   if (tid < kD) {
     long long sum = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sum += part[i][tid];
+    for (int i = 0; i < 8; ++i) sum += part[i][tid];
     sfix[tid] = sum;
   }
   cluster_sync_smem();
