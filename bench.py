@@ -199,8 +199,8 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
 ISSUE_BOUND = {
     "k_snapkv_tc": "issue-bound exp epilogue + cluster all-reduce tail: ncu issue active 53 %, "
                    "214.6 M warp-instructions per launch (profiles/r1w_ncu_snapkv_raw.csv, DESIGN.md §5)",
-    "k_keydiff_cluster": "issue/latency-bound: K is read from HBM once (556 MB/launch); ncu issue active 53 % "
-                         "(profiles/r1v_ncu_keydiff_raw.csv)",
+    "k_keydiff_cluster": "issue/latency-bound: K is read from HBM once (562 MB/launch with the L2 hints); "
+                         "ncu issue active 62 % (profiles/r1z_ncu_keydiff_raw.csv)",
 }
 
 

@@ -199,7 +199,7 @@ __device__ __forceinline__ void stream_rows(const uint4* __restrict__ src, int n
 // over together: f(t[], live[], v[]) can batch per-row work across them.
 template <class F>
 __device__ __forceinline__ void stream_rows4(const uint4* __restrict__ src, int n, uint4* ring, uint64_t* full,
-                                             uint32_t& seq, F&& f) {
+                                             uint32_t& seq, F&& f, uint64_t pol = 0) {
   constexpr int kU = kRingRows / 16;
   const int tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
   const int nch = (n + kRingRows - 1) / kRingRows;
@@ -207,8 +207,12 @@ __device__ __forceinline__ void stream_rows4(const uint4* __restrict__ src, int 
     const int st = (seq + c) % kRingStages;
     const int rows = min(kRingRows, n - c * kRingRows);
     mbar_expect_tx(&full[st], rows * 256);
-    bulk_g2s(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
-             rows * 256, &full[st]);
+    if (pol)
+      bulk_g2s_hint(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
+                    rows * 256, &full[st], pol);
+    else
+      bulk_g2s(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
+               rows * 256, &full[st]);
   };
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -431,7 +435,7 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
         if (l16 == 0) kinv[t[u]] = inv;
       }
     }
-  });
+  }, l2_evict_last());  // pass 2 re-reads these rows: keep them in L2
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // the warp's two half-warps first (|sum| < 2^31: <= per / 16 rows each)
     int32_t x = static_cast<int32_t>(acc[i] - cnt * 0x4B400000u);
@@ -465,7 +469,7 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
     const int tu = u == 0 ? t[0] : (u == 1 ? t[1] : (u == 2 ? t[2] : t[3]));
     const bool lu = u == 0 ? live[0] : (u == 1 ? live[1] : (u == 2 ? live[2] : live[3]));
     if (lu && (l16 & 3) == 0) o[tu] = -__fmul_rn(p, kinv[tu]);
-  });
+  }, l2_evict_first());  // last use
   cluster_sync_smem();  // no CTA exits while a peer may still read its sfix
 }
 
