@@ -725,12 +725,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         // q8 / sig are free once the previous slice's last MMA has completed
         if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) & 1], ((g0 - 1) >> 1) & 1);
         mbar_expect_tx(&sm.qbar, kSnapQBytes);
-        bulk_g2s(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar);
+        bulk_g2s_hint(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar,
+                      l2_evict_last());  // the Q8 tiles serve every chunk
         bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
         const int rows = min(128, n_loc);
         fence_async_smem();
         mbar_expect_tx(&sm.full, rows * 256);
-        bulk_g2s(sm.stage, Ks, rows * 256, &sm.full);
+        bulk_g2s_hint(sm.stage, Ks, rows * 256, &sm.full, l2_evict_first());  // K is read once
       }
       for (int j = 0; j < ntl; ++j) {
         const int g = g0 + j, buf = g & 1;
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           const int nrows = min(128, n_loc - (j + 1) * 128);
           fence_async_smem();
           mbar_expect_tx(&sm.full, nrows * 256);
-          bulk_g2s(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full);
+          bulk_g2s_hint(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full, l2_evict_first());
         }
         uint32_t mx = 0;
 #pragma unroll
