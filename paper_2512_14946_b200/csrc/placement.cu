@@ -398,13 +398,23 @@ extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_
   return KVT_OK;
 }
 
+static int num_sms_p() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return v;
+}
+
 // ---------------------------------------------------------------- oracle_mckp
 // proj/src/placement.cpp:300-372. Every context's scorable candidates in
 // candidate_preferred order (stable over the enumeration order); a branch
 // and bound over one-candidate-per-context assignments under the finite
 // tiers' capacities. The first d contexts' choices index the GPU threads
 // (mixed radix, context 0 most significant = the DFS's lexicographic
-// order); each thread runs the reference's DFS over the rest of its
+// order); persistent threads take the prefixes from a counter and run the reference's DFS on each
 // subtree. A thread keeps the first maximal leaf of its subtree (strictly
 // better only), so the maximal total with the smallest prefix index, then
 // the thread's pick, is the reference's result: the first optimum in DFS
@@ -412,7 +422,6 @@ extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_
 // best), and a strict test against the best total any thread has reached
 // (never cuts a subtree that could tie), shared as an order-preserving key.
 constexpr int kMckpMaxCtx = 24;
-constexpr long long kMckpMaxThreads = 1 << 18;
 
 __device__ __forceinline__ unsigned long long mckp_key(double v) {
   const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(v, 0.0)));
@@ -427,48 +436,82 @@ __global__ void __launch_bounds__(128) k_mckp(const double* __restrict__ cu, con
                                               const int* __restrict__ ctier, const int* __restrict__ off,
                                               const int* __restrict__ cnt, const double* __restrict__ suffix,
                                               DevTiers TT, int n, int d, long long nprefix,
-                                              unsigned long long* __restrict__ gbest, double* __restrict__ out_total,
-                                              int* __restrict__ out_found, int* __restrict__ out_choice) {
-  const long long pfx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (pfx >= nprefix) return;
+                                              unsigned long long* __restrict__ gbest,
+                                              unsigned long long* __restrict__ next, double* __restrict__ out_total,
+                                              int* __restrict__ out_found, long long* __restrict__ out_pfx,
+                                              int* __restrict__ out_choice) {
+  // persistent threads take prefixes from a counter (in increasing order per
+  // thread, so a thread's first maximal leaf is its lexicographically first)
+  const long long me = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   int choice[kMckpMaxCtx], k[kMckpMaxCtx], best_choice[kMckpMaxCtx];
   double tot[kMckpMaxCtx + 1];
   long long used[KVT_MAX_TIERS];
-  for (int t = 0; t < KVT_MAX_TIERS; ++t) used[t] = 0;
-  long long rem = pfx;
-  for (int i = d - 1; i >= 0; --i) {
-    choice[i] = static_cast<int>(rem % cnt[i]);
-    rem /= cnt[i];
-  }
-  tot[0] = 0.0;
-  out_found[pfx] = 0;
-  for (int i = 0; i < d; ++i) {  // the prefix: the same capacity test and running sum as the DFS
-    const int c = off[i] + choice[i], t = ctier[c];
-    if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) return;
-    used[t] += csz[c];
-    tot[i + 1] = __dadd_rn(tot[i], cu[c]);
-  }
   double best = 0.0;
+  long long best_pfx = -1;
   bool found = false;
-  int lvl = d;
-  bool enter = true;
   while (true) {
-    if (enter) {  // node entry (the reference's dfs(i, total) prologue)
-      const double bound = __dadd_rn(tot[lvl], suffix[lvl]);
-      if ((found && bound <= best) || bound < mckp_val(*const_cast<volatile unsigned long long*>(gbest))) {
-        enter = false;  // pruned: back to the parent
-      } else if (lvl == n) {
-        best = tot[n];
-        found = true;
-        for (int i = 0; i < n; ++i) best_choice[i] = choice[i];
-        atomicMax(gbest, mckp_key(best));
-        enter = false;
-      } else {
-        k[lvl] = 0;
-        enter = false;
-        goto try_children;
+    const long long pfx = static_cast<long long>(atomicAdd(next, 1ull));
+    if (pfx >= nprefix) break;
+    for (int t = 0; t < KVT_MAX_TIERS; ++t) used[t] = 0;
+    long long rem = pfx;
+    for (int i = d - 1; i >= 0; --i) {
+      choice[i] = static_cast<int>(rem % cnt[i]);
+      rem /= cnt[i];
+    }
+    tot[0] = 0.0;
+    bool fits = true;
+    for (int i = 0; i < d && fits; ++i) {  // the prefix: the same capacity test and running sum as the DFS
+      const int c = off[i] + choice[i], t = ctier[c];
+      if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) {
+        fits = false;
+        break;
       }
-      // go up one level, undo that level's choice, advance it
+      used[t] += csz[c];
+      tot[i + 1] = __dadd_rn(tot[i], cu[c]);
+    }
+    if (!fits) continue;
+    int lvl = d;
+    bool enter = true;
+    while (true) {
+      if (enter) {  // node entry (the reference's dfs(i, total) prologue)
+        const double bound = __dadd_rn(tot[lvl], suffix[lvl]);
+        if ((found && bound <= best) || bound < mckp_val(*const_cast<volatile unsigned long long*>(gbest))) {
+          enter = false;  // pruned: back to the parent
+        } else if (lvl == n) {
+          best = tot[n];
+          found = true;
+          best_pfx = pfx;
+          for (int i = 0; i < n; ++i) best_choice[i] = choice[i];
+          atomicMax(gbest, mckp_key(best));
+          enter = false;
+        } else {
+          k[lvl] = 0;
+          enter = false;
+          goto try_children;
+        }
+        if (lvl == d) break;
+        --lvl;
+        {
+          const int c = off[lvl] + choice[lvl];
+          used[ctier[c]] -= csz[c];
+        }
+        ++k[lvl];
+      }
+    try_children:
+      while (k[lvl] < cnt[lvl]) {
+        const int c = off[lvl] + k[lvl], t = ctier[c];
+        if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) {
+          ++k[lvl];
+          continue;
+        }
+        used[t] += csz[c];
+        choice[lvl] = k[lvl];
+        tot[lvl + 1] = __dadd_rn(tot[lvl], cu[c]);
+        ++lvl;
+        enter = true;
+        break;
+      }
+      if (enter) continue;
       if (lvl == d) break;
       --lvl;
       {
@@ -477,48 +520,26 @@ __global__ void __launch_bounds__(128) k_mckp(const double* __restrict__ cu, con
       }
       ++k[lvl];
     }
-  try_children:
-    while (k[lvl] < cnt[lvl]) {
-      const int c = off[lvl] + k[lvl], t = ctier[c];
-      if (!TT.unlimited[t] && used[t] + csz[c] > TT.cap[t]) {
-        ++k[lvl];
-        continue;
-      }
-      used[t] += csz[c];
-      choice[lvl] = k[lvl];
-      tot[lvl + 1] = __dadd_rn(tot[lvl], cu[c]);
-      ++lvl;
-      enter = true;
-      break;
-    }
-    if (enter) continue;
-    // children exhausted
-    if (lvl == d) break;
-    --lvl;
-    {
-      const int c = off[lvl] + choice[lvl];
-      used[ctier[c]] -= csz[c];
-    }
-    ++k[lvl];
   }
+  out_found[me] = found ? 1 : 0;
   if (found) {
-    out_found[pfx] = 1;
-    out_total[pfx] = best;
-    for (int i = d; i < n; ++i) out_choice[pfx * n + i] = best_choice[i];
-    for (int i = 0; i < d; ++i) out_choice[pfx * n + i] = best_choice[i];
+    out_total[me] = best;
+    out_pfx[me] = best_pfx;
+    for (int i = 0; i < n; ++i) out_choice[me * n + i] = best_choice[i];
   }
 }
 
 // the winning subtree: maximal total, then the smallest prefix index
 __global__ void __launch_bounds__(1024) k_mckp_pick(const double* __restrict__ tot, const int* __restrict__ found,
-                                                     long long nprefix, long long* __restrict__ win) {
+                                                     const long long* __restrict__ pfx, long long nprefix,
+                                                     long long* __restrict__ win) {
   __shared__ double sv[1024];
   __shared__ long long si[1024];
   const int tid = threadIdx.x;
   double bv = 0.0;
   long long bi = -1;
-  for (long long i = tid; i < nprefix; i += 1024)
-    if (found[i] && (bi < 0 || tot[i] > bv)) {
+  for (long long i = tid; i < nprefix; i += 1024)  // (here: one entry per search thread)
+    if (found[i] && (bi < 0 || tot[i] > bv || (tot[i] == bv && pfx[i] < pfx[bi]))) {
       bv = tot[i];
       bi = i;
     }
@@ -529,7 +550,7 @@ __global__ void __launch_bounds__(1024) k_mckp_pick(const double* __restrict__ t
     if (tid < w) {
       const double ov = sv[tid + w];
       const long long oi = si[tid + w];
-      if (oi >= 0 && (si[tid] < 0 || ov > sv[tid] || (ov == sv[tid] && oi < si[tid]))) {
+      if (oi >= 0 && (si[tid] < 0 || ov > sv[tid] || (ov == sv[tid] && pfx[oi] < pfx[si[tid]]))) {
         sv[tid] = ov;
         si[tid] = oi;
       }
@@ -620,15 +641,19 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
   }
   // subtrees: enough prefixes to fill the GPU when the space is large, few
   // when it is small (every thread's subtree is then tiny anyway)
+  // subtrees (prefixes of the first d contexts) handed out dynamically to
+  // persistent search threads: many more prefixes than threads when the
+  // space is large (load balance), few when it is small
   const double space_sz = assignments;
-  const long long target = space_sz > 1e6 ? kMckpMaxThreads : 4096;
+  const long long nthreads = space_sz > 1e6 ? static_cast<long long>(num_sms_p() * 4) * 128 : 4096;
+  const long long target = space_sz > 1e6 ? 64 * nthreads : 4096;
   int d = 0;
   long long nprefix = 1;
   while (d < n && nprefix * cnt_h[d] <= target) nprefix *= cnt_h[d++];
   // device buffers
   const size_t nc = std::max<size_t>(1, cu_h.size());
-  const size_t bytes = nc * (8 + 8 + 4) + size_t(n + 1) * 4 * 2 + size_t(n + 1) * 8 + 8 +
-                       size_t(nprefix) * (8 + 4 + 4 * size_t(std::max(n, 1))) + 64 * 8;
+  const size_t bytes = nc * (8 + 8 + 4) + size_t(n + 1) * 4 * 2 + size_t(n + 1) * 8 + 16 +
+                       size_t(nthreads) * (8 + 4 + 8 + 4 * size_t(std::max(n, 1))) + 64 * 10;
   char* dbuf = nullptr;
   KVT_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), bytes, h->stream));
   size_t o = 0;
@@ -644,9 +669,11 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
   auto* d_cnt = reinterpret_cast<int*>(carve(size_t(n + 1) * 4));
   auto* d_suf = reinterpret_cast<double*>(carve(size_t(n + 1) * 8));
   auto* d_gbest = reinterpret_cast<unsigned long long*>(carve(8));
-  auto* d_tot = reinterpret_cast<double*>(carve(size_t(nprefix) * 8));
-  auto* d_found = reinterpret_cast<int*>(carve(size_t(nprefix) * 4));
-  auto* d_choice = reinterpret_cast<int*>(carve(size_t(nprefix) * 4 * size_t(std::max(n, 1))));
+  auto* d_next = reinterpret_cast<unsigned long long*>(carve(8));
+  auto* d_tot = reinterpret_cast<double*>(carve(size_t(nthreads) * 8));
+  auto* d_found = reinterpret_cast<int*>(carve(size_t(nthreads) * 4));
+  auto* d_pfx = reinterpret_cast<long long*>(carve(size_t(nthreads) * 8));
+  auto* d_choice = reinterpret_cast<int*>(carve(size_t(nthreads) * 4 * size_t(std::max(n, 1))));
   cudaStream_t st = h->stream;
   if (!cu_h.empty()) {
     KVT_CUDA_TRY(cudaMemcpyAsync(d_cu, cu_h.data(), cu_h.size() * 8, cudaMemcpyHostToDevice, st));
@@ -666,12 +693,14 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
     KVT_CUDA_TRY(cudaMemcpyAsync(d_gbest, &key, 8, cudaMemcpyHostToDevice, st));
     KVT_CUDA_TRY(cudaStreamSynchronize(st));  // key lives on this frame
   }
-  k_mckp<<<static_cast<int>((nprefix + 127) / 128), 128, 0, st>>>(d_cu, d_csz, d_ct, d_off, d_cnt, d_suf, T, n, d,
-                                                                  nprefix, d_gbest, d_tot, d_found, d_choice);
+  KVT_CUDA_TRY(cudaMemsetAsync(d_next, 0, 8, st));
+  k_mckp<<<static_cast<int>((nthreads + 127) / 128), 128, 0, st>>>(d_cu, d_csz, d_ct, d_off, d_cnt, d_suf, T, n, d,
+                                                                   nprefix, d_gbest, d_next, d_tot, d_found, d_pfx,
+                                                                   d_choice);
   h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
   auto* d_win = reinterpret_cast<long long*>(d_gbest);  // gbest is dead once the search is done
-  k_mckp_pick<<<1, 1024, 0, st>>>(d_tot, d_found, nprefix, d_win);
+  k_mckp_pick<<<1, 1024, 0, st>>>(d_tot, d_found, d_pfx, nthreads, d_win);
   h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
   long long win = -1;
