@@ -388,7 +388,7 @@ def load_scenario_text(text: str, base_dir: str = "",
     sc = Scenario(tiers, params, space, [cp for cp, _ in contexts],
                   {cp.context: t for cp, t in contexts if t}, [cp.context for cp, _ in contexts],
                   bool(doc.get("warm_start", False)), bool(doc.get("miss_store_bottom", False)), drift, rule,
-                  seed, dc)
+                  seed, dc, policy)
     return sc, trace, policy
 
 

@@ -17,8 +17,9 @@ simulate.cpp:102-128; quality.cpp:158-220) or `miss_store_bottom`, a
 request can change the profiles and reshuffle the whole store, so the loop
 runs request by request: a re-profile rebuilds the context's quality table
 from its truth curve (std::mt19937_64 noise, bit-exact), uploads the new
-profile set and runs `rearrange` on the device. Not here: the LRU / fixed /
-impress / prefill baselines.
+profile set and runs `rearrange` on the device. The LRU / fixed / impress /
+prefill baselines (`Policy::parse`) run the same request-by-request loop with
+their LRU cascade (placement.cpp:374-438) on the device store.
 """
 from __future__ import annotations
 
@@ -80,6 +81,7 @@ class Scenario:
     rule: str = "utility"
     seed: int = 0
     drift_config: Dict[str, float] = field(default_factory=dict)  # DriftConfig + ReprofileConfig
+    policy: str = "joint"  # Policy::label(): joint, joint-qargmax, lru, fixed:<m>:<r>, impress:<f>[:<o>], prefill
 
     @staticmethod
     def from_doc(doc: dict) -> Tuple["Scenario", List[Request]]:
@@ -99,7 +101,8 @@ class Scenario:
                  for c, per in (doc.get("truth") or {}).items()}
         sc = Scenario(tiers, params, space, profiles, truth, list(doc.get("order") or []),
                       bool(doc.get("warm_start")), bool(doc.get("miss_store_bottom")), bool(doc.get("drift")),
-                      doc.get("rule", "utility"), int(doc.get("seed", 0)), dict(doc.get("drift_config") or {}))
+                      doc.get("rule", "utility"), int(doc.get("seed", 0)), dict(doc.get("drift_config") or {}),
+                      doc.get("policy", "joint"))
         trace = [Request(float(r["t"]), r["context"], int(r.get("n_new_tokens", 0))) for r in doc["trace"]]
         return sc, trace
 
@@ -141,6 +144,28 @@ def quality_of(prof: ContextProfile, method: str, ratio: float) -> float:  # pro
 def synth_quality(sensitivity: float, shape_k: float, ratio: float) -> float:  # proj/src/quality.cpp:115-127
     drop = sensitivity * math.pow((1.0 - ratio) / 0.1, shape_k)
     return min(max(1.0 - drop, 0.0), 1.0)
+
+
+def parse_policy(text: str):  # placement.cpp:440-495 Policy::parse -> (kind, (method, ratio), chunk overhead)
+    parts = text.split(":")
+    head = parts[0]
+    bad = A.ValidationError(A.KVT_EVALIDATION, f"unknown policy '{text}'")
+    if head in ("joint", "joint-qargmax", "lru", "prefill"):
+        if len(parts) != 1:
+            raise bad
+        return ("joint" if head.startswith("joint") else head), None, 1.3
+    if head == "fixed" and len(parts) == 3:
+        r = float(parts[2])
+        if not parts[1] or not (0.0 < r <= 1.0):
+            raise A.ValidationError(A.KVT_EVALIDATION, "fixed ratio must be in (0, 1]")
+        return "fixed", (parts[1], r), 1.3
+    if head == "impress" and len(parts) in (2, 3):
+        f = float(parts[1])
+        o = float(parts[2]) if len(parts) == 3 else 1.3
+        if not (0.0 < f <= 1.0) or not o > 0.0:
+            raise A.ValidationError(A.KVT_EVALIDATION, "impress keep fraction must be in (0, 1]")
+        return "impress", (None, f), o
+    raise bad
 
 
 class MT19937_64:
@@ -241,6 +266,9 @@ class Replayer:
         self.ps = eng.pset(self.arrays)
         self.store = eng.store(self.tiers, self.arrays.n, scenario.space)
         self.rule = A.KVT_RULE_UTILITY if scenario.rule == "utility" else A.KVT_RULE_QUALITY_FIRST
+        self.kind, self.fixed, self.chunk_overhead = parse_policy(scenario.policy)
+        if self.kind == "joint" and scenario.policy == "joint-qargmax":
+            self.rule = A.KVT_RULE_QUALITY_FIRST
         self.names = scenario.space.method_names
         self.ovh = [m.decompression_overhead for m in scenario.space.methods]
         self.stamp = 0
@@ -316,7 +344,53 @@ class Replayer:
         ctx = [self.arrays.index[c] for c in order]
         stamps = list(range(self.stamp, self.stamp + len(ctx)))
         self.stamp += len(ctx)
-        self._insert(ctx, [0] * len(ctx), stamps)
+        if self.kind == "joint":
+            self._insert(ctx, [0] * len(ctx), stamps)
+        else:
+            for c, st in zip(ctx, stamps):
+                self._policy_insert(c, 0, st)
+
+    # -- the baselines (placement.cpp:374-438, 515-547): a store at the top
+    # tier at one fixed configuration, overflow pushes the least recently
+    # used entry one tier down, unchanged (on the device store)
+    def _policy_insert(self, c: int, freq: int, stamp: int):
+        if self.kind == "joint":
+            self._insert([c], [freq], [stamp])
+            return
+        if self.kind == "prefill":
+            return
+        if self.kind == "lru":
+            m, ratio = 0, 1.0
+        elif self.kind == "fixed":
+            if self.fixed[0] not in self.names:
+                raise A.ValidationError(A.KVT_EVALIDATION, f"fixed policy method {self.fixed[0]} is not in the method set")
+            m, ratio = self.names.index(self.fixed[0]), self.fixed[1]
+        else:  # impress: (first method, keep fraction)
+            m, ratio = 0, self.fixed[1]
+        cid = self.arrays.ids[c]
+        orig = self.prof[cid].original_size_bytes
+        self.store.add(c, 0, m, ratio, orig, freq, stamp)
+        self.actions.append(("insert", cid, self.tiers[0].tier_id, self.names[m], ratio))
+        self.n_device_calls += 1
+        for ti in range(len(self.tiers)):
+            while True:
+                occ = self.store.occupancy()
+                cap = self.tiers[ti].capacity_bytes
+                if cap is None or occ[ti] <= cap:
+                    break
+                if ti + 1 >= len(self.tiers):
+                    raise A.ValidationError(A.KVT_EVALIDATION,
+                                            f"tier {self.tiers[ti].name} overflows and there is no lower tier")
+                snap = self.store.snapshot()
+                idx = np.nonzero(snap["tier_index"] == ti)[0]
+                idx = idx[np.argsort(snap["seq"][idx], kind="stable")]  # arrival order
+                v = int(idx[np.argmin(snap["last_access"][idx])])  # first minimum, like the reference
+                e = self.store.remove(v)
+                self.store.add(v, ti + 1, int(e.method), float(e.ratio), int(e.original_size_bytes),
+                               int(e.frequency), int(e.last_access))
+                self.actions.append(("evict", self.arrays.ids[v], self.tiers[ti + 1].tier_id, self.names[int(e.method)],
+                                     float(e.ratio)))
+                self.n_device_calls += 4
 
     # -- serving
     def _quality(self, c: int, m: int, ratio: float) -> float:
@@ -341,7 +415,7 @@ class Replayer:
         n = len(trace)
         if n == 0:
             return []
-        if self.sc.drift or self.sc.miss_store_bottom:
+        if self.sc.drift or self.sc.miss_store_bottom or self.kind != "joint":
             return self._run_sequential(trace)
         t = np.fromiter((r.t for r in trace), np.float64, n)
         nnew = np.fromiter((r.n_new_tokens for r in trace), np.int64, n)
@@ -451,7 +525,7 @@ class Replayer:
         self._qcache.clear()
 
     def _maybe_reprofile(self, c: int, now: float):  # simulate.cpp:102-128
-        if not self.sc.drift:
+        if not self.sc.drift or self.kind != "joint":
             return
         st = self.drift_states.get(c)
         if st is None:
@@ -506,6 +580,8 @@ class Replayer:
                 m, ratio = int(self.method[c]), float(self.ratio[c])
                 name = self.names[m]
                 load = load_time(compressed_size(prof.original_size_bytes, ratio), tier, self.ovh[m])
+                if self.kind == "impress":
+                    load *= self.chunk_overhead  # chunked reads amplify the fetch (simulate.cpp:170-172)
                 ttft = load + prefill_time(r.n_new_tokens, p) + penalty
                 predicted = quality_of(prof, name, ratio)
                 truth = self.sc.truth.get(r.context)
@@ -513,20 +589,22 @@ class Replayer:
                 rec = RequestRecord(r, True, tier.tier_id, name, ratio, ttft, achieved)
                 touch_c.append(c)
                 touch_s.append(stamp)
-                if self.sc.drift and truth is not None:  # simulate.cpp:186-193
+                if self.sc.drift and self.kind == "joint" and truth is not None:  # simulate.cpp:186-193
                     self.drift_states.setdefault(c, DriftState(self.window_size)).record(predicted, achieved)
             else:  # miss
                 tokens = token_count(prof.original_size_bytes, p) + r.n_new_tokens
                 rec = RequestRecord(r, False, -1, "", 1.0, prefill_time(tokens, p) + penalty, 1.0)
-                self._touch(touch_c, touch_s)
-                if self.sc.miss_store_bottom:  # simulate.cpp:203-216: bottom tier at (first method, 1.0), rearrange
+                self._touch(touch_c, touch_s)  # LRU reads last_access
+                if self.sc.miss_store_bottom and self.kind == "joint":  # simulate.cpp:203-216: bottom tier, rearrange
                     bottom = len(self.tiers) - 1
                     self.store.add(c, bottom, 0, 1.0, prof.original_size_bytes, 1, stamp)
                     self.actions.append(("insert", r.context, self.tiers[bottom].tier_id, self.names[0], 1.0))
                     self._record_actions(self.store.rearrange(self.ps, self.sc.space, self.sc.params, rule=self.rule))
                     self.n_device_calls += 2
-                else:
+                elif self.kind == "joint":
                     self._insert([c], [1], [stamp])
+                else:
+                    self._policy_insert(c, 1, stamp)
                 self._refresh()
             out.append(rec)
             if self.sc.drift:

@@ -30,6 +30,11 @@ CASES = [
     ("drift_noise", "drift", ["drift.noise=0.05"]),
     ("bimodal_msb", "bimodal", ["warm_start=false", "miss_store_bottom=true"]),
     ("bimodal_qargmax", "bimodal", ["warm_start=false", "policy=joint-qargmax"]),
+    ("bimodal_lru", "bimodal", ["warm_start=false", "policy=lru"]),
+    ("bimodal_fixed", "bimodal", ["policy=fixed:keydiff:0.4"]),
+    ("bimodal_impress", "bimodal", ["warm_start=false", "policy=impress:0.3"]),
+    ("fig2_prefill", "fig2", ["policy=prefill"]),
+    ("drift_lru", "drift", ["policy=lru"]),
 ]
 
 
@@ -50,7 +55,7 @@ def main():
         with gzip.open(path, "wt") as f:
             json.dump(doc, f)
         r = doc["result"]
-        print(name, len(doc["trace"]), "requests", len(r["actions"]), "actions", "miss",
+        print(name, len(doc["trace"]), "requests", len(r.get("actions", [])), "actions", "miss",
               r["metrics"]["miss_fraction"], os.path.getsize(path), "bytes")
 
 
