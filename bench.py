@@ -160,7 +160,7 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
         eng.abi.check(eng.abi.pack(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), idx, A.ptr(codec.out[0])))
         evs[3].record(stream)
         keys = [None if full else SCORER_KERNEL[cfgc.scorer], None if full else "k_topk",
-                "k_gather16" if cfgc.bits == 16 else f"k_pack_k+v<{cfgc.bits}>"]
+                "k_gather16" if cfgc.bits == 16 else f"k_pack_kv<{cfgc.bits}>"]
         recs.append((evs, keys, [ab["scores"], ab["topk"], ab["pack"]]))
     torch.cuda.synchronize()
     per = {}

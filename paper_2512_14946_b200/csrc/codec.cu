@@ -1461,14 +1461,6 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
   __syncthreads();  // smem reused by the next group
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(256, 4) k_pack_k(const uint4* __restrict__ K, const int32_t* __restrict__ idx,
-                                                uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
-                                                uint16_t* __restrict__ kz, int T, int k) {
-  __shared__ PackKSmem sm;
-  pack_k_group<BITS>(K, idx, kc, ks, kz, T, k, blockIdx.y, blockIdx.x, sm);
-}
-
 // V quantisation: per kept token over its 128 channels. A half-warp packs
 // kVRows rows: loads all of them first (kVRows 16-byte loads in flight per
 // lane), reduces each row's (min, max) as one bf16x2 butterfly, lane i
@@ -1552,27 +1544,32 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
   }
 }
 
-// grid (ceil(k / (16 * kVRows)), S): 16 half-warps x kVRows rows per block
+// K groups and V rows of a slice in one launch: grid (nk + nv, S), blocks
+// x < nk pack K group x, the rest V rows, so each slice's K and V blocks are
+// dispatched next to each other and neither half leaves a tail wave.
 template <int BITS>
-__global__ void __launch_bounds__(256, 4) k_pack_v(const uint4* __restrict__ V, const int32_t* __restrict__ idx,
-                                                int32_t* __restrict__ oidx, uint32_t* __restrict__ vc,
-                                                uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k) {
-  pack_v_rows<BITS>(V, idx, oidx, vc, vs, vz, T, k, blockIdx.y, (blockIdx.x * 16 + (threadIdx.x >> 4)) * kVRows);
+__global__ void __launch_bounds__(256, 4) k_pack_kv(const uint4* __restrict__ K, const uint4* __restrict__ V,
+                                                 const int32_t* __restrict__ idx, int32_t* __restrict__ oidx,
+                                                 uint32_t* __restrict__ kc, uint16_t* __restrict__ ks,
+                                                 uint16_t* __restrict__ kz, uint32_t* __restrict__ vc,
+                                                 uint16_t* __restrict__ vs, uint16_t* __restrict__ vz, int T, int k,
+                                                 int nk) {
+  __shared__ PackKSmem sm;
+  const int x = blockIdx.x;
+  if (x < nk) pack_k_group<BITS>(K, idx, kc, ks, kz, T, k, blockIdx.y, x, sm);
+  else pack_v_rows<BITS>(V, idx, oidx, vc, vs, vz, T, k, blockIdx.y, ((x - nk) * 16 + (threadIdx.x >> 4)) * kVRows);
 }
 
 template <int BITS>
 static void launch_pack_bits(cudaStream_t st, const kvt_blob_map& m, char* b, const uint16_t* k, const uint16_t* v,
                              const int32_t* idx, int S, int T, int kk) {
-  dim3 kgrid((kk + KVT_QGROUP - 1) / KVT_QGROUP, S);
-  k_pack_k<BITS><<<kgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), idx,
-                                        reinterpret_cast<uint32_t*>(b + m.kcode_off),
-                                        reinterpret_cast<uint16_t*>(b + m.kscale_off),
-                                        reinterpret_cast<uint16_t*>(b + m.kzero_off), T, kk);
-  dim3 vgrid((kk + 16 * kVRows - 1) / (16 * kVRows), S);
-  k_pack_v<BITS><<<vgrid, 256, 0, st>>>(reinterpret_cast<const uint4*>(v), idx, reinterpret_cast<int32_t*>(b + m.idx_off),
-                                        reinterpret_cast<uint32_t*>(b + m.vcode_off),
-                                        reinterpret_cast<uint16_t*>(b + m.vscale_off),
-                                        reinterpret_cast<uint16_t*>(b + m.vzero_off), T, kk);
+  const int nk = (kk + KVT_QGROUP - 1) / KVT_QGROUP, nv = (kk + 16 * kVRows - 1) / (16 * kVRows);
+  k_pack_kv<BITS><<<dim3(nk + nv, S), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
+      reinterpret_cast<int32_t*>(b + m.idx_off), reinterpret_cast<uint32_t*>(b + m.kcode_off),
+      reinterpret_cast<uint16_t*>(b + m.kscale_off), reinterpret_cast<uint16_t*>(b + m.kzero_off),
+      reinterpret_cast<uint32_t*>(b + m.vcode_off), reinterpret_cast<uint16_t*>(b + m.vscale_off),
+      reinterpret_cast<uint16_t*>(b + m.vzero_off), T, kk, nk);
 }
 
 static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
@@ -1594,7 +1591,7 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
   if (c->bits == 8) launch_pack_bits<8>(st, m, b, k, v, idx, S, s->T, kk);
   else if (c->bits == 4) launch_pack_bits<4>(st, m, b, k, v, idx, S, s->T, kk);
   else launch_pack_bits<2>(st, m, b, k, v, idx, S, s->T, kk);
-  h->launches += 2;
+  LAUNCHED(h);
   KVT_CUDA_TRY(cudaGetLastError());
   return KVT_OK;
 }

@@ -22,6 +22,4 @@ for r in rows[2:]:
     b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
     acc.setdefault(name, []).append(b)
 out = {k: int(sum(v) / len(v)) for k, v in acc.items()}
-if "k_pack_k<4>" in out and "k_pack_v<4>" in out:
-    out["k_pack_k+v<4>"] = out["k_pack_k<4>"] + out["k_pack_v<4>"]
 print(json.dumps(out, indent=1, sort_keys=True))
