@@ -192,6 +192,11 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
                         for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
     if dom in ISSUE_BOUND:  # HBM fraction is reported, but it is not what bounds this kernel
         line["bound_note"] = ISSUE_BOUND[dom]
+    ge = os.environ.get("KVT_SNAP_GRID")
+    if dom == "k_snapkv_tc" and ge:  # runs on a share of the SMs by design (the step's other streams get the rest)
+        sms = min(int(ge) * 16, torch.cuda.get_device_properties(0).multi_processor_count)
+        line["sms"] = sms
+        line["frac_per_sm"] = round(line["frac"] * torch.cuda.get_device_properties(0).multi_processor_count / sms, 4)
     return line
 
 
@@ -267,7 +272,7 @@ def run_b200(args):
     from paper_2512_14946_b200 import _abi as A
     from paper_2512_14946_b200 import distributed, workload
     from paper_2512_14946_b200.kvtier import Engine, ProfileArrays
-    from paper_2512_14946_b200.pipeline import Codec, KVPool, compress_placed, place
+    from paper_2512_14946_b200.pipeline import Codec, KVPool, compress_placed, place, split_plan
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -297,6 +302,7 @@ def run_b200(args):
     lanes = [Engine(pkg.product(), device=local, stream=ls.cuda_stream) for ls in lane_streams]
     codec = Codec(lanes, L, H, D)
     codec.reserve(max_T, n_out=2)
+    codec.attach_streams(lane_streams)
     ps = eng.pset(arrays)
     store = eng.store(tiers, arrays.n, space)
     order = np.arange(arrays.n, dtype=np.int32)
@@ -322,12 +328,20 @@ def run_b200(args):
     def launch_compress(snap_full):  # every placed context of this rank, async on the codec lanes
         in_b = out_b = 0
         fork()  # the lanes start after this batch's placement
-        for c in range(my_lo, my_hi):
-            if snap_full["tier_index"][c] < 0:
-                continue
-            T = int(arrays.orig[c] // bpt)
+        cs = [c for c in range(my_lo, my_hi) if snap_full["tier_index"][c] >= 0]
+        ms = [names[snap_full["method"][c]] for c in cs]
+        rs = [float(snap_full["ratio"][c]) for c in cs]
+        Ts = [int(arrays.orig[c] // bpt) for c in cs]
+        if args.lanes == "split":
+            for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, split_plan(ms, rs, Ts, len(lanes), args.snap_clusters)):
+                k, v = pool.chunk(c)
+                out_b += (codec.compress(m, r, k, v, T, c, pl) if sl is None
+                          else codec.compress_split(m, r, k, v, T, c, sl, pl))
+                in_b += int(arrays.orig[c])
+            return in_b, out_b
+        for c, m, r, T in zip(cs, ms, rs, Ts):  # round-robin, one kvt_compress per context
             k, v = pool.chunk(c)
-            out_b += codec.compress(names[snap_full["method"][c]], float(snap_full["ratio"][c]), k, v, T, c)
+            out_b += codec.compress(m, r, k, v, T, c)
             in_b += int(arrays.orig[c])
         return in_b, out_b
 
@@ -423,7 +437,11 @@ def run_b200(args):
                        "l2": "inputs larger than L2 (1 GiB chunks, pool of distinct chunks)",
                        "actions_per_step": n_act, "compressed_bytes_per_step_rank0": out_b,
                        "parallelism": f"dp{world} (contexts sharded, global greedy replicated)",
-                       "schedule": "batches software-pipelined: batch i+1's placement overlaps batch i's compression"},
+                       "schedule": "batches software-pipelined: batch i+1's placement overlaps batch i's compression"
+                                   + (f"; {args.streams} codec streams, snapkv scoring alone on stream 0 as "
+                                      f"{args.snap_clusters} 16-CTA clusters, top-k / pack / other scorers on "
+                                      "streams 1.. (pipeline.split_plan)" if args.lanes == "split" else
+                                      f"; {args.streams} codec streams, contexts round-robin")},
             "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
@@ -543,7 +561,13 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--n-ctx", type=int, default=None)
     ap.add_argument("--pool", type=int, default=8, help="distinct resident KV chunks")
-    ap.add_argument("--streams", type=int, default=2, help="codec CUDA streams (contexts round-robin)")
+    ap.add_argument("--streams", type=int, default=3, help="codec CUDA streams")
+    ap.add_argument("--lanes", choices=["split", "rr"], default="split",
+                    help="split: snapkv scoring alone on stream 0 (--snap-clusters clusters), every other codec "
+                         "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
+                         "each")
+    ap.add_argument("--snap-clusters", type=int, default=4,
+                    help="snapkv persistent 16-CTA clusters in split mode (sets KVT_SNAP_GRID)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -551,6 +575,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
+        if args.lanes == "split":  # read by kvt at every snapkv launch; the roofline leg runs the same way
+            os.environ["KVT_SNAP_GRID"] = str(args.snap_clusters)
         run_b200(args)
 
 

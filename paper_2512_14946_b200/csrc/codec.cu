@@ -1315,20 +1315,39 @@ extern "C" int kvt_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cf
 
 // -------------------------------------------------------------------- pack
 
-// bits == 16: gather kept K/V rows (half-warp per row, 16-byte lanes).
+// bits == 16: gather kept K/V rows (half-warp per kGRows rows, 16-byte
+// lanes; all 2 x kGRows loads issued before the stores, so an SM keeps
+// enough bytes in flight to run at full rate on a share of the SMs, e.g.
+// beside snapkv's clusters).
+constexpr int kGRows = 4;
 __global__ void __launch_bounds__(256) k_gather16(const uint4* __restrict__ K, const uint4* __restrict__ V,
                                                   const int32_t* __restrict__ idx, int32_t* __restrict__ oidx,
                                                   uint4* __restrict__ ko, uint4* __restrict__ vo, int T, int k) {
   const int slice = blockIdx.y, l16 = threadIdx.x & 15;
-  const int j = blockIdx.x * 16 + (threadIdx.x >> 4);
-  if (j >= k) return;
-  const int t = idx[static_cast<size_t>(slice) * k + j];
-  const size_t src = (static_cast<size_t>(slice) * T + t) * 16 + l16;
-  const size_t dst = (static_cast<size_t>(slice) * k + j) * 16 + l16;
-  const uint4 a = __ldcs(K + src), b = __ldcs(V + src);
-  __stcs(ko + dst, a);
-  __stcs(vo + dst, b);
-  if (l16 == 0) oidx[static_cast<size_t>(slice) * k + j] = t;
+  const int j0 = (blockIdx.x * 16 + (threadIdx.x >> 4)) * kGRows;
+  if (j0 >= k) return;
+  const int32_t* ix = idx + static_cast<size_t>(slice) * k;
+  int t[kGRows];
+#pragma unroll
+  for (int i = 0; i < kGRows; ++i) t[i] = j0 + i < k ? ix[j0 + i] : 0;
+  uint4 a[kGRows], b[kGRows];
+#pragma unroll
+  for (int i = 0; i < kGRows; ++i) {
+    if (j0 + i < k) {
+      const size_t src = (static_cast<size_t>(slice) * T + t[i]) * 16 + l16;
+      a[i] = __ldcs(K + src);
+      b[i] = __ldcs(V + src);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kGRows; ++i) {
+    if (j0 + i < k) {
+      const size_t dst = (static_cast<size_t>(slice) * k + j0 + i) * 16 + l16;
+      __stcs(ko + dst, a[i]);
+      __stcs(vo + dst, b[i]);
+      if (l16 == 0) oidx[static_cast<size_t>(slice) * k + j0 + i] = t[i];
+    }
+  }
 }
 
 // K quantisation: per channel over a group of <=128 kept tokens, one
@@ -1580,7 +1599,7 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
   const int S = s->L * s->H, kk = c->keep;
   cudaStream_t st = h->stream;
   if (c->bits == 16) {
-    dim3 rows_grid((kk + 15) / 16, S);
+    dim3 rows_grid((kk + 16 * kGRows - 1) / (16 * kGRows), S);
     k_gather16<<<rows_grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
                                           reinterpret_cast<int32_t*>(b + m.idx_off),
                                           reinterpret_cast<uint4*>(b + m.kcode_off),

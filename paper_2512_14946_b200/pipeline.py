@@ -9,7 +9,7 @@ kvt_* kernel in libkvt_b200.so.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -75,23 +75,94 @@ class Codec:
         wsb = self.eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg))
         m = A.BlobMap()
         self.eng.abi.check(self.eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+        self._max_T = max_T
         self._ws = [torch.empty(wsb, dtype=torch.uint8, device="cuda") for _ in self.lanes]
         self._out = [[torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda") for _ in range(n_out)]
                      for _ in self.lanes]
         self.ws, self.out = self._ws[0], self._out[0]
 
-    def compress(self, method: str, ratio: float, k, v, T: int, slot: int) -> int:
+    def compress(self, method: str, ratio: float, k, v, T: int, slot: int, lane: Optional[int] = None) -> int:
         cfg, m, _ = self.plan(method, ratio, T)
         s = A.KvShape(self.L, self.H, T, self.D)
-        li = slot % len(self.lanes)
+        li = slot % len(self.lanes) if lane is None else lane
         eng, outs = self.lanes[li], self._out[li]
         out = outs[(slot // len(self.lanes)) % len(outs)]
         eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(self._ws[li]),
                                        A.ptr(out)))
         return m.total_bytes
 
+    def attach_streams(self, streams, ring: int = 4):
+        """The lanes' torch streams (same order as the engines): enables
+        compress_split, whose scores pass through a ring of `ring` score
+        buffers handed from one stream to another by CUDA events."""
+        S = self.L * self.H
+        self._streams = list(streams)
+        self._ring = [torch.empty(S * self._max_T, dtype=torch.float32, device="cuda") for _ in range(ring)]
+        self._ready = [torch.cuda.Event() for _ in range(ring)]
+        self._free = [torch.cuda.Event() for _ in range(ring)]
+        self._idx = [torch.empty(S * self._max_T, dtype=torch.int32, device="cuda") for _ in self.lanes]
+        self._ri = 0
+
+    def compress_split(self, method: str, ratio: float, k, v, T: int, slot: int, score_lane: int,
+                       pack_lane: int) -> int:
+        """compress with the scoring pass on `score_lane` and top-k + pack on
+        `pack_lane` (token_scores -> event -> topk + pack: the same three
+        kernels kvt_compress launches, on two streams)."""
+        cfg, m, _ = self.plan(method, ratio, T)
+        if cfg.keep == T:  # no scoring pass
+            return self.compress(method, ratio, k, v, T, slot, pack_lane)
+        s = A.KvShape(self.L, self.H, T, self.D)
+        j = self._ri
+        self._ri = (j + 1) % len(self._ring)
+        se, pe = self.lanes[score_lane], self.lanes[pack_lane]
+        ss, ps = self._streams[score_lane], self._streams[pack_lane]
+        ss.wait_event(self._free[j])  # the ring slot's previous top-k has read it
+        se.abi.check(se.abi.token_scores(se.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(self._ring[j])))
+        self._ready[j].record(ss)
+        ps.wait_event(self._ready[j])
+        idx = self._idx[pack_lane]
+        pe.abi.check(pe.abi.topk(pe.h, C.byref(s), C.byref(cfg), A.ptr(self._ring[j]), A.ptr(idx)))
+        self._free[j].record(ps)
+        outs = self._out[pack_lane]
+        out = outs[(slot // len(self.lanes)) % len(outs)]
+        pe.abi.check(pe.abi.pack(pe.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(out)))
+        return m.total_bytes
+
     def launches(self) -> int:
         return sum(int(e.abi.launch_count(e.h)) for e in self.lanes)
+
+
+# Per 8,192-token chunk of the bench model, in µs (profiles/r1z: ncu and
+# bench per-kernel averages): scoring by method (snapkv on 7 clusters), and
+# K + V pack per unit of kept ratio by code width.
+_SCORE_US = {"snapkv": 494.0, "keydiff": 180.0, "knorm": 107.0}
+_PACK_US = {16: 325.0, 8: 230.0, 4: 210.0, 2: 210.0}
+
+
+def split_plan(methods: Sequence[str], ratios: Sequence[float], Ts: Sequence[int], n_lanes: int,
+               snap_clusters: int = 7) -> List[Tuple[Optional[int], int]]:
+    """(score lane, pack lane) of each context for Codec.compress_split.
+    snapkv scoring is issue-bound and runs as `snap_clusters` persistent
+    16-CTA clusters: it goes alone on lane 0 (None = no split), so one snapkv
+    launch is in flight at a time and the SMs it leaves free take the
+    memory-bound kernels (knorm / keydiff scoring, top-k, gathers, packs),
+    each context's on the least-loaded of lanes 1.. by a cost estimate."""
+    load = [0.0] * n_lanes
+    out = []
+    for m, r, T in zip(methods, ratios, Ts):
+        base, _, q = m.partition("-")
+        bits = int(q[1:]) if q else 16
+        pack = T / 8192.0 * _PACK_US.get(bits, 230.0) * r
+        score = T / 8192.0 * _SCORE_US.get(base, 0.0) if r < 1.0 else 0.0
+        li = min(range(1, n_lanes), key=load.__getitem__)
+        if base == "snapkv" and r < 1.0:
+            load[0] += score * 7.0 / snap_clusters
+            load[li] += pack
+            out.append((0, li))
+        else:
+            load[li] += pack + score
+            out.append((None, li))
+    return out
 
 
 def place(store: StoreState, ps: PSet, space: CandidateSpace, params: UtilityParams, order) -> np.ndarray:
