@@ -192,9 +192,9 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
                         for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
     if dom in ISSUE_BOUND:  # HBM fraction is reported, but it is not what bounds this kernel
         line["bound_note"] = ISSUE_BOUND[dom]
-    ge = os.environ.get("KVT_SNAP_GRID")
+    ge = os.environ.get("KVT_SNAP_SMS")
     if dom == "k_snapkv_tc" and ge:  # runs on a share of the SMs by design (the step's other streams get the rest)
-        sms = min(int(ge) * 16, torch.cuda.get_device_properties(0).multi_processor_count)
+        sms = min(int(ge), torch.cuda.get_device_properties(0).multi_processor_count)
         line["sms"] = sms
         line["frac_per_sm"] = round(line["frac"] * torch.cuda.get_device_properties(0).multi_processor_count / sms, 4)
     return line
@@ -333,7 +333,7 @@ def run_b200(args):
         rs = [float(snap_full["ratio"][c]) for c in cs]
         Ts = [int(arrays.orig[c] // bpt) for c in cs]
         if args.lanes == "split":
-            for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, split_plan(ms, rs, Ts, len(lanes), args.snap_clusters)):
+            for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, split_plan(ms, rs, Ts, len(lanes), args.snap_sms)):
                 k, v = pool.chunk(c)
                 out_b += (codec.compress(m, r, k, v, T, c, pl) if sl is None
                           else codec.compress_split(m, r, k, v, T, c, sl, pl))
@@ -439,7 +439,7 @@ def run_b200(args):
                        "parallelism": f"dp{world} (contexts sharded, global greedy replicated)",
                        "schedule": "batches software-pipelined: batch i+1's placement overlaps batch i's compression"
                                    + (f"; {args.streams} codec streams, snapkv scoring alone on stream 0 as "
-                                      f"{args.snap_clusters} 16-CTA clusters, top-k / pack / other scorers on "
+                                      f"persistent clusters on {args.snap_sms} SMs, top-k / pack / other scorers on "
                                       "streams 1.. (pipeline.split_plan)" if args.lanes == "split" else
                                       f"; {args.streams} codec streams, contexts round-robin")},
             "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
@@ -566,8 +566,8 @@ def main():
                     help="split: snapkv scoring alone on stream 0 (--snap-clusters clusters), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
-    ap.add_argument("--snap-clusters", type=int, default=4,
-                    help="snapkv persistent 16-CTA clusters in split mode (sets KVT_SNAP_GRID)")
+    ap.add_argument("--snap-sms", type=int, default=64,
+                    help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -576,7 +576,7 @@ def main():
         run_reference(args)
     else:
         if args.lanes == "split":  # read by kvt at every snapkv launch; the roofline leg runs the same way
-            os.environ["KVT_SNAP_GRID"] = str(args.snap_clusters)
+            os.environ["KVT_SNAP_SMS"] = str(args.snap_sms)
         run_b200(args)
 
 

@@ -1092,8 +1092,10 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = S;
       na = n;
     }
-    const char* ge = getenv("KVT_SNAP_GRID");  // experiments: force the number of clusters
-    const int ng = ge && *ge ? atoi(ge) : na;
+    // KVT_SNAP_SMS: an SM budget (scheduling knob for running beside other
+    // streams' kernels): as many whole clusters as fit in it
+    const char* ge = getenv("KVT_SNAP_SMS");
+    const int ng = ge && *ge ? std::min(na, atoi(ge) / Cn) : na;
     cfg.gridDim = dim3(Cn, std::max(1, std::min(S, ng)));
   }
   KVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(k), static_cast<const uint8_t*>(qbuf), escr,

@@ -78,7 +78,7 @@ def _sections(b, m, bits):
 def test_split_plan_puts_snapkv_scoring_on_lane0():
     ms = ["snapkv-q4", "knorm", "snapkv", "keydiff-q8", "snapkv-q4", "knorm-q4"]
     rs = [0.2, 0.4, 1.0, 0.3, 0.5, 0.1]
-    plan = split_plan(ms, rs, [8192] * len(ms), 3, snap_clusters=4)
+    plan = split_plan(ms, rs, [8192] * len(ms), 3, snap_sms=64)
     for (sl, pl), m, r in zip(plan, ms, rs):
         assert pl in (1, 2)
         assert sl == (0 if m.startswith("snapkv") and r < 1.0 else None)
