@@ -302,7 +302,7 @@ def run_b200(args):
     lanes = [Engine(pkg.product(), device=local, stream=ls.cuda_stream) for ls in lane_streams]
     codec = Codec(lanes, L, H, D)
     codec.reserve(max_T, n_out=2)
-    codec.attach_streams(lane_streams)
+    codec.attach_streams(lane_streams, ring=args.ring)
     ps = eng.pset(arrays)
     store = eng.store(tiers, arrays.n, space)
     order = np.arange(arrays.n, dtype=np.int32)
@@ -566,6 +566,7 @@ def main():
                     help="split: snapkv scoring alone on stream 0 (--snap-clusters clusters), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
+    ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
     ap.add_argument("--snap-sms", type=int, default=64,
                     help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
