@@ -137,6 +137,18 @@ def test_snapkv_scores_bitexact(gpu, orc, si):
     assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
 
 
+@pytest.mark.parametrize("sms", ["1", "16", "64", "100"])
+def test_snapkv_sm_budget_same_scores(gpu, sms, monkeypatch):
+    """KVT_SNAP_SMS (the bench's SM budget for snapkv's persistent clusters)
+    changes only how many clusters loop over the slices: scores identical."""
+    s = A.KvShape(2, 4, 3000, 128)  # 6-CTA clusters, 8 slices
+    kg, _ = gen(gpu, s)
+    cfg = plan(gpu.abi, "snapkv", 0.3, s)
+    want = scores(gpu, s, cfg, kg, True)
+    monkeypatch.setenv("KVT_SNAP_SMS", sms)
+    assert np.array_equal(scores(gpu, s, cfg, kg, True).view(np.uint32), want.view(np.uint32))
+
+
 def test_snapkv_rejects_too_long_prefix(gpu):
     s = A.KvShape(1, 1, 32768 + 32 + 1, 128)  # prefix of 32769 tokens
     cfg = plan(gpu.abi, "snapkv", 0.3, s)
