@@ -156,7 +156,7 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
             eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfgc), A.ptr(sc), idx))
         evs[0].record(stream)
         if not full:
-            eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(sc)))
+            eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), None, A.ptr(sc)))
         evs[1].record(stream)
         if not full:
             eng.abi.check(eng.abi.topk(eng.h, C.byref(s), C.byref(cfgc), A.ptr(sc), idx))
@@ -235,7 +235,7 @@ def tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
         s = A.KvShape(L, H, T, D)
         k, v = pool.chunk(c)
         b = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
-        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), A.ptr(codec.ws),
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), None, A.ptr(codec.ws),
                                        A.ptr(b)))
         blobs.append(b)
         placed.append((c, int(snap["tier_index"][c]), b.data_ptr(), b.numel()))
@@ -513,7 +513,7 @@ def cpu_reference_sample(W, seconds=20.0, steps=1):
         ws = np.zeros(orc.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
         blob = np.zeros(m.total_bytes, np.uint8)
         t0 = time.perf_counter()
-        orc.check(orc.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+        orc.check(orc.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
         dt = time.perf_counter() - t0
         spent += dt
         t_codec_timed += dt * (L / Ls) * count  # full chunk, every context of this group

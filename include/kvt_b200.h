@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define KVT_ABI_VERSION 1
+#define KVT_ABI_VERSION 2
 
 /* Hard limits of the device kernels (kernel-parameter structs). */
 #define KVT_MAX_TIERS 8
@@ -248,6 +248,10 @@ typedef struct {
   int32_t L, H, T, D; /* D must be 128 */
 } kvt_kv_shape;
 
+/* kvt_codec_cfg.flags */
+#define KVT_CODEC_KNORM_KEEP_LOW 1 /* knorm keeps LOW-norm keys (the cited knorm paper);
+                                      default keeps high norms, dropping low */
+
 /* One codec configuration resolved from a (method label, ratio) pair. */
 typedef struct {
   int32_t scorer;     /* kvt_scorer */
@@ -256,7 +260,9 @@ typedef struct {
   int32_t window;     /* snapkv observation window W (always kept) */
   int32_t q_heads;    /* snapkv query heads per kv head (GQA group) */
   int32_t pool;       /* snapkv max-pool kernel (odd) */
-  uint64_t q_seed;    /* snapkv synthetic query seed */
+  int32_t flags;      /* KVT_CODEC_* bits */
+  int32_t pad_;
+  uint64_t q_seed;    /* snapkv synthetic query seed (used when no Q is passed) */
 } kvt_codec_cfg;
 
 /* Layout of one compressed chunk (all offsets in bytes from blob start). */
@@ -267,6 +273,10 @@ typedef struct {
   int64_t vcode_off, vcode_bytes;   /* u32 words, [L][H][keep][D*bits/32] */
   int64_t vscale_off, vzero_off, vparam_bytes; /* fp16 [L][H][keep] each */
   int64_t total_bytes;
+  /* 1 for the identity configuration (every token kept at 16 bits): the
+   * compressed chunk IS the source KV, so the blob has no bytes, compress
+   * launches nothing and tier moves copy the source K/V directly. */
+  int64_t identity;
 } kvt_blob_map;
 
 #define KVT_QGROUP 128 /* K per-channel quant group (kept tokens) */
@@ -280,21 +290,28 @@ typedef struct {
   /* synthetic KV: counter hash of (seed, ctx, layer, head, token, dim) */          \
   int P##kv_generate(kvt_handle* h, const kvt_kv_shape* shape, uint64_t seed,        \
                      uint64_t ctx, uint16_t* k, uint16_t* v);                        \
-  /* per-(layer, head, token) float scores; larger = more important */              \
+  /* per-(layer, head, token) float scores; larger = more important. q: snapkv's  \
+   * observation-window queries, bf16 [L][H*q_heads][window][D] (the last       \
+   * `window` query positions of every query head); NULL = the     \
+   * synthetic queries of cfg->q_seed. Ignored by knorm / keydiff. */            \
   int P##token_scores(kvt_handle* h, const kvt_kv_shape* shape,                      \
-                      const kvt_codec_cfg* cfg, const uint16_t* k, float* scores);   \
+                      const kvt_codec_cfg* cfg, const uint16_t* k, const uint16_t* q, \
+                      float* scores);                                                \
   /* per (layer, head): `keep` largest scores, ties -> lower index, ascending */    \
   int P##topk(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,    \
               const float* scores, int32_t* idx);                                    \
   /* gather kept tokens, quantise, pack into blob */                                 \
   int P##pack(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,    \
               const uint16_t* k, const uint16_t* v, const int32_t* idx, void* blob); \
-  /* unpack + dequantise into bf16 [L][H][keep][D] */                                \
+  /* unpack + dequantise into bf16 [L][H][keep][D]; identity blobs have no bytes \
+   * to unpack (KVT_EINVAL: the source KV is the decompressed KV) */              \
   int P##unpack(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg,  \
                 const void* blob, uint16_t* k_out, uint16_t* v_out);                 \
-  /* scores + topk + pack in one call (workspace: scores + idx, see below) */      \
+  /* scores + topk + pack in one call (workspace: scores + idx, see below);       \
+   * q as for token_scores */                                                      \
   int P##compress(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg, \
-                  const uint16_t* k, const uint16_t* v, void* workspace, void* blob); \
+                  const uint16_t* k, const uint16_t* v, const uint16_t* q,           \
+                  void* workspace, void* blob);                                      \
   int64_t P##compress_workspace_bytes(const kvt_kv_shape* shape, const kvt_codec_cfg* cfg);
 
 KVT_DECLARE_CODEC(kvt_)

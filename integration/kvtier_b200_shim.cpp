@@ -30,6 +30,7 @@
 // Status codes map back to the reference's exceptions: KVT_EVALIDATION ->
 // kvtier::ValidationError, KVT_ETRACE -> kvtier::TraceError, anything else
 // -> std::runtime_error (proj/include/kvtier/core.hpp:18-24).
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -50,9 +51,9 @@ namespace {
 // KVT_SHIM_TRACE=1: report at exit how many reference calls the shim served
 // (the drop-in test uses it to prove the interposition took effect).
 struct CallCount {
-  long n = 0;
+  std::atomic<long> n{0};  // worker threads of `compare --jobs` call concurrently
   ~CallCount() {
-    if (std::getenv("KVT_SHIM_TRACE")) std::fprintf(stderr, "kvt_b200 shim: %ld kvtier calls served\n", n);
+    if (std::getenv("KVT_SHIM_TRACE")) std::fprintf(stderr, "kvt_b200 shim: %ld kvtier calls served\n", n.load());
   }
 } g_calls;
 
@@ -67,7 +68,7 @@ void check(int rc) {
 // One handle per thread (the reference runs independent stores on worker
 // threads under `compare --jobs`, proj/tools/kvtier_main.cpp:206-235).
 kvt_handle* handle() {
-  ++g_calls.n;
+  g_calls.n.fetch_add(1, std::memory_order_relaxed);
   struct Owner {
     kvt_handle* h = nullptr;
     ~Owner() {

@@ -10,9 +10,11 @@
  * tests/test_codec_oracle.py, not by reference vectors.
  *
  * Every rounding step is spelled out so the CUDA path can match it
- * bit-for-bit: FP64 sums in the canonical chunk-then-butterfly order,
- * fixed-point (2^-40) accumulation for keydiff's mean direction, fp32 IEEE
- * ops (no contraction: built with -ffp-contract=off) for quantisation,
+ * bit-for-bit (spec v2): fp32 dot products with explicit
+ * fmaf chains in the canonical chunk-then-butterfly order, 2^-21
+ * fixed-point int64 accumulation for keydiff's mean direction, snapkv as
+ * exact int8 x int8 logits with an integer-shift softmax, fp32 IEEE ops
+ * (no contraction: built with -ffp-contract=off) for quantisation,
  * round-half-even everywhere.
  */
 #include <math.h>
@@ -139,6 +141,10 @@ static int64_t al256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 int orc_blob_layout(const kvt_kv_shape* s, const kvt_codec_cfg* c, kvt_blob_map* o) {
   const int64_t S = (int64_t)s->L * s->H, k = c->keep, D = s->D;
   memset(o, 0, sizeof *o);
+  if (k == s->T && c->bits == 16) { /* identity: the source KV is the compressed chunk */
+    o->identity = 1;
+    return KVT_OK;
+  }
   int64_t off = 0;
   o->idx_off = off;
   o->idx_bytes = 4 * S * k;
@@ -202,7 +208,15 @@ int orc_kv_generate(kvt_handle* h, const kvt_kv_shape* s, uint64_t seed, uint64_
   return KVT_OK;
 }
 
-/* snapkv synthetic query: q[l][hq][w][d] of stream (q_seed, 0) */
+/* snapkv window query q[l][hq][w][d]: the caller's (bf16 [L][H*G][W][D]) or
+ * the synthetic stream (q_seed, 0x51) */
+static uint16_t synth_q(const kvt_kv_shape* s, const kvt_codec_cfg* c, int l, int hq, int w, int d);
+static uint16_t window_q(const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* q, int l, int hq, int w,
+                         int d) {
+  if (!q) return synth_q(s, c, l, hq, w, d);
+  const uint64_t Hq = (uint64_t)s->H * c->q_heads;
+  return q[(((uint64_t)l * Hq + (uint64_t)hq) * (uint64_t)c->window + (uint64_t)w) * D_HEAD + (uint64_t)d];
+}
 static uint16_t synth_q(const kvt_kv_shape* s, const kvt_codec_cfg* c, int l, int hq, int w, int d) {
   const uint64_t Hq = (uint64_t)s->H * c->q_heads;
   const uint64_t idx = (((uint64_t)l * Hq + (uint64_t)hq) * (uint64_t)c->window + (uint64_t)w) * D_HEAD + (uint64_t)d;
@@ -285,18 +299,21 @@ typedef struct {
   const kvt_kv_shape* s;
   const kvt_codec_cfg* c;
   const uint16_t* k;
+  const uint16_t* q; /* snapkv window queries or NULL */
   float* scores;
 } score_job_t;
 
-/* knorm: squared L2 norm of every key, larger = keep */
+/* knorm: squared L2 norm of every key, larger = keep;
+ * KVT_CODEC_KNORM_KEEP_LOW negates it (low norms kept, the cited knorm paper) */
 static void knorm_slice(void* a, int64_t sl) {
   score_job_t* J = (score_job_t*)a;
   const int T = J->s->T;
+  const float sign = (J->c->flags & KVT_CODEC_KNORM_KEEP_LOW) ? -1.0f : 1.0f;
   const uint16_t* K = J->k + (size_t)sl * T * D_HEAD;
   float x[D_HEAD];
   for (int t = 0; t < T; ++t) {
     row_f32(K + (size_t)t * D_HEAD, x);
-    J->scores[(size_t)sl * T + t] = row_dot(x, x);
+    J->scores[(size_t)sl * T + t] = sign * row_dot(x, x);
   }
 }
 
@@ -422,7 +439,7 @@ static void snapkv_slice(void* a, int64_t sl) {
   for (int g = 0; g < G; ++g)
     for (int w = 0; w < W; ++w) {
       const int r = g * W + w;
-      for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(synth_q(s, c, l, h * G + g, w, d));
+      for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(window_q(s, c, J->q, l, h * G + g, w, d));
       sig[r] = quant_i8(row, D_HEAD, q8 + (size_t)r * D_HEAD);
     }
   /* K: one int8 scale per 128-token tile of the prefix */
@@ -504,10 +521,11 @@ static void snapkv_slice(void* a, int64_t sl) {
   free(vote);
 }
 
-int orc_token_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k, float* scores) {
+int orc_token_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
+                     const uint16_t* q, float* scores) {
   (void)h;
   if (s->D != D_HEAD) return orc_fail(KVT_EINVAL, "D must be 128");
-  score_job_t J = {s, c, k, scores};
+  score_job_t J = {s, c, k, q, scores};
   const int64_t S = (int64_t)s->L * s->H;
   switch (c->scorer) {
     case KVT_SCORER_KNORM: parallel_for(S, knorm_slice, &J); break;
@@ -689,6 +707,7 @@ int orc_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const
   J.idx = idx;
   J.blob = (uint8_t*)blob;
   orc_blob_layout(s, c, &J.map);
+  if (J.map.identity) return KVT_OK; /* nothing to write: the source KV is the blob */
   memset(blob, 0, (size_t)J.map.total_bytes);
   parallel_for((int64_t)s->L * s->H, pack_slice, &J);
   return KVT_OK;
@@ -742,6 +761,8 @@ int orc_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, con
   J.ko = k_out;
   J.vo = v_out;
   orc_blob_layout(s, c, &J.map);
+  if (J.map.identity)
+    return orc_fail(KVT_EINVAL, "identity configuration: the blob aliases the source KV (kvt_blob_map.identity)");
   parallel_for((int64_t)s->L * s->H, unpack_slice, &J);
   return KVT_OK;
 }
@@ -752,12 +773,13 @@ int64_t orc_compress_workspace_bytes(const kvt_kv_shape* s, const kvt_codec_cfg*
 }
 
 int orc_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k, const uint16_t* v,
-                 void* workspace, void* blob) {
+                 const uint16_t* q, void* workspace, void* blob) {
   const int64_t S = (int64_t)s->L * s->H;
+  if (c->keep == s->T && c->bits == 16) return KVT_OK; /* identity: nothing to write */
   float* scores = (float*)workspace;
   int32_t* idx = (int32_t*)((uint8_t*)workspace + al256(4 * S * s->T));
   int rc;
-  if ((rc = orc_token_scores(h, s, c, k, scores))) return rc;
+  if ((rc = orc_token_scores(h, s, c, k, q, scores))) return rc;
   if ((rc = orc_topk(h, s, c, scores, idx))) return rc;
   return orc_pack(h, s, c, k, v, idx, blob);
 }

@@ -2,10 +2,15 @@
 // (kvtier, compiled from /root/reference/proj/src by oracle/Makefile into
 // oracle/_ref/) through the ref_* copy of the C ABI in include/kvt_b200.h,
 // so tests and bench.py's reference arm can drive it with the same arrays
-// as the CUDA path. This file only translates arrays <-> kvtier types and
-// calls the reference's public API; no algorithm lives here.
+// as the CUDA path. This file translates arrays <-> kvtier types and calls
+// the reference's public API. One exception, clearly separated at the end:
+// ref_insert_joint_cached, the single-core CPU baseline of the cached greedy
+// built on the reference's own scoring functions, so the
+// bench can separate the algorithmic speed-up from the hardware speed-up.
 #include <cstdint>
 #include <cstring>
+#include <set>
+#include <tuple>
 #include <map>
 #include <memory>
 #include <optional>
@@ -583,4 +588,121 @@ extern "C" int ref_replay_dump(const char* scenario_path, const char* out_path, 
     j["result"] = jr;
     std::ofstream(out_path) << j.dump(1);
   });
+}
+
+// ------------------------------------------------------------------------
+// CPU BASELINE (not the reference's algorithm, not the product): insert_joint
+// (proj/src/placement.cpp:225-250) with least_drop_update's rescan of every
+// resident (:174-204) replaced by a cached per-resident best update and one
+// ordered set per tier keyed (utility_drop, -bytes_freed, context) — the
+// structure SURVEY.md §0.6 validated as bit-identical, and the one the
+// device greedy (K3) implements. A resident's options depend only on its own
+// entry and profile (enumerate_updates, proj/src/utility.cpp:81-127), so only
+// the resident a step changes (or a new insert) is re-scored. Uses the
+// reference's StoreState, best_config, score_candidate and enumerate_updates.
+namespace {
+struct CachedBest {
+  bool valid = false;
+  kvtier::UpdateCandidate u;
+};
+using Key = std::tuple<double, int64_t, std::string>;  // (drop, -bytes_freed, context)
+
+bool better_option(const kvtier::UpdateCandidate& a, const kvtier::UpdateCandidate& b) {
+  if (a.utility_drop != b.utility_drop) return a.utility_drop < b.utility_drop;
+  return a.bytes_freed > b.bytes_freed;  // same resident: first enumerated wins the rest
+}
+
+CachedBest resident_best(const kvtier::StoreState& st, const kvtier::CacheEntry& e, size_t ti,
+                         const kvtier::ContextProfile& prof, const kvtier::CandidateSpace& space,
+                         const kvtier::UtilityParams& up) {
+  CachedBest b;
+  const kvtier::ConfigCandidate cur =
+      kvtier::score_candidate(prof, e.config, st.tier(ti), static_cast<int>(ti), space.methods(), up);
+  for (const auto& opt : kvtier::enumerate_updates(e, prof, st.tiers(), space, up)) {
+    kvtier::UpdateCandidate u;
+    u.context = e.context;
+    u.kind = opt.tier_index == static_cast<int>(ti) ? kvtier::PlacementAction::Kind::Recompress
+                                                    : kvtier::PlacementAction::Kind::Evict;
+    u.target = opt;
+    u.utility_drop = cur.utility - opt.utility;
+    u.bytes_freed = u.kind == kvtier::PlacementAction::Kind::Recompress ? cur.size_bytes - opt.size_bytes
+                                                                       : cur.size_bytes;
+    if (!b.valid || better_option(u, b.u)) {
+      b.u = u;
+      b.valid = true;
+    }
+  }
+  return b;
+}
+}  // namespace
+
+extern "C" int ref_insert_joint_cached(kvt_store* s, const kvt_pset* pc, const kvt_space* sp,
+                                       const kvt_params* params, int32_t rule, const int32_t* ctx,
+                                       const int64_t* frequency, const int64_t* stamp, int64_t n_ops,
+                                       int64_t* n_actions, int64_t* n_done) {
+  auto* p = const_cast<kvt_pset*>(pc);
+  set_names(s, sp);
+  s->act.clear();
+  *n_done = 0;
+  int rc = guard([&] {
+    const auto space = make_space(sp);
+    const auto& map = p->profiles(sp);
+    const auto up = mk_params(params);
+    const auto sel = rule == KVT_RULE_QUALITY_FIRST ? kvtier::SelectionRule::QualityFirst
+                                                    : kvtier::SelectionRule::Utility;
+    kvtier::StoreState& st = *s->st;
+    const size_t T = st.tier_count();
+    std::vector<std::set<Key>> sets(T);
+    std::map<std::string, CachedBest> cache;
+    auto key_of = [](const kvtier::UpdateCandidate& u) { return Key(u.utility_drop, -u.bytes_freed, u.context); };
+    auto enter = [&](const kvtier::CacheEntry& e, size_t ti) {
+      CachedBest b = resident_best(st, e, ti, map.at(e.context), space, up);
+      if (b.valid) sets[ti].insert(key_of(b.u));
+      cache[e.context] = std::move(b);
+    };
+    auto leave = [&](const std::string& c, size_t ti) {
+      auto it = cache.find(c);
+      if (it != cache.end() && it->second.valid) sets[ti].erase(key_of(it->second.u));
+    };
+    for (size_t ti = 0; ti < T; ++ti)
+      for (const auto& e : st.residents(ti)) enter(e, ti);
+    for (int64_t i = 0; i < n_ops; ++i) {
+      const std::string id = ctx_name(ctx[i]);
+      if (st.contains(id)) throw kvtier::ValidationError("context " + id + " is already resident");
+      const kvtier::ContextProfile& prof = map.at(id);
+      const kvtier::ConfigCandidate best = kvtier::best_config(prof, st.tiers(), space, up, sel);
+      kvtier::CacheEntry entry;
+      entry.context = id;
+      entry.original_size_bytes = prof.original_size_bytes;
+      entry.config = best.config;
+      entry.tier = best.tier_id;
+      entry.frequency = frequency ? frequency[i] : 0;
+      entry.last_access = stamp ? stamp[i] : 0;
+      st.add(entry);
+      std::vector<kvtier::PlacementAction> acts{{kvtier::PlacementAction::Kind::Insert, id, best.tier_id, best.config}};
+      enter(*st.find(id), st.tier_index_of(id));
+      while (auto over = st.first_over_capacity()) {
+        if (sets[*over].empty())
+          throw kvtier::ValidationError("tier " + st.tier(*over).name +
+                                        " is over capacity and no resident has a space-saving option");
+        const std::string who = std::get<2>(*sets[*over].begin());
+        const kvtier::UpdateCandidate u = cache.at(who).u;
+        leave(who, *over);
+        if (u.kind == kvtier::PlacementAction::Kind::Recompress) {
+          st.reconfigure(u.context, u.target.config);
+        } else {
+          kvtier::CacheEntry moved = st.remove(u.context);
+          moved.tier = u.target.tier_id;
+          moved.config = u.target.config;
+          st.add(std::move(moved));
+        }
+        enter(*st.find(who), st.tier_index_of(who));
+        acts.push_back({u.kind, u.context, u.target.tier_id, u.target.config});
+      }
+      append(s, space, acts);
+      *n_done = i + 1;
+    }
+  });
+  *n_actions = static_cast<int64_t>(s->act.size());
+  return rc;
 }

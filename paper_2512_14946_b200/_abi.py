@@ -71,17 +71,20 @@ class KvShape(C.Structure):
     _fields_ = [("L", C.c_int32), ("H", C.c_int32), ("T", C.c_int32), ("D", C.c_int32)]
 
 
+KVT_CODEC_KNORM_KEEP_LOW = 1
+
+
 class CodecCfg(C.Structure):
     _fields_ = [("scorer", C.c_int32), ("bits", C.c_int32), ("keep", C.c_int32),
                 ("window", C.c_int32), ("q_heads", C.c_int32), ("pool", C.c_int32),
-                ("q_seed", C.c_uint64)]
+                ("flags", C.c_int32), ("pad_", C.c_int32), ("q_seed", C.c_uint64)]
 
 
 class BlobMap(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "idx_off", "idx_bytes", "kcode_off", "kcode_bytes", "kscale_off", "kzero_off",
         "kparam_bytes", "vcode_off", "vcode_bytes", "vscale_off", "vzero_off", "vparam_bytes",
-        "total_bytes")]
+        "total_bytes", "identity")]
 
 
 class Move(C.Structure):
@@ -142,11 +145,11 @@ CODEC_SIGS = {
     "codec_plan": (C.c_int, [C.c_char_p, f64, C.POINTER(KvShape), C.POINTER(CodecCfg)]),
     "blob_layout": (C.c_int, [C.POINTER(KvShape), C.POINTER(CodecCfg), C.POINTER(BlobMap)]),
     "kv_generate": (C.c_int, [P, C.POINTER(KvShape), u64, u64, P, P]),
-    "token_scores": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P]),
+    "token_scores": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, P]),
     "topk": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P]),
     "pack": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, P, P]),
     "unpack": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, P]),
-    "compress": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, P, P]),
+    "compress": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, P, P, P]),
     "compress_workspace_bytes": (i64, [C.POINTER(KvShape), C.POINTER(CodecCfg)]),
 }
 
@@ -158,6 +161,8 @@ PRODUCT_EXTRA_SIGS = {
     "tier_host_free": (C.c_int, [P]),
 }
 TIER_SIGS = {"tier_moves": (C.c_int, [P, C.POINTER(Move), i64])}
+# ref_insert_joint_cached: the CPU cached-greedy baseline (oracle/ref_capi.cpp), same signature
+CACHED_SIGS = {"insert_joint_cached": PLACEMENT_SIGS["insert_joint"]}
 # kvt_oracle_mckp (product) / ref_oracle_mckp (reference glue): bound when exported
 MCKP_SIGS = {"oracle_mckp": (C.c_int, [P, P, C.POINTER(Tier), i32, C.POINTER(Space), C.POINTER(Params), f64,
                                        C.POINTER(C.c_double), P])}
@@ -192,6 +197,8 @@ class Abi:
             sigs.update(TIER_SIGS)
         if hasattr(self.lib, prefix + "oracle_mckp"):
             sigs.update(MCKP_SIGS)
+        if hasattr(self.lib, prefix + "insert_joint_cached"):
+            sigs.update(CACHED_SIGS)
         for name, (res, args) in sigs.items():
             fn = getattr(self.lib, prefix + name)
             fn.restype = res

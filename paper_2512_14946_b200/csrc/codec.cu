@@ -1,8 +1,8 @@
 // KV codec on sm_100a: synthetic KV, token scores (knorm / keydiff /
 // snapkv), per-(layer, head) top-k, gather + quantise + pack, unpack +
-// dequantise. Builder-defined spec; bit-exact to
-// oracle/orc_codec.c for everything but snapkv's softmax (fp32 here,
-// tolerance-checked).
+// dequantise. Builder-defined spec; every output (scores,
+// kept indices, codes, fp16 params, dequantised KV) is bit-exact to
+// oracle/orc_codec.c, snapkv's integer softmax included.
 //
 // Memory-bound design: one bf16 row (128 channels = 256 B) is owned by a
 // half-warp, one 16-byte vector load per lane; reductions over the row are
@@ -31,25 +31,13 @@ namespace cg = cooperative_groups;
 
 
 
-static int g_num_sms = 0;
-static int smem_optin() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
-  return v;
+static int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);  // the handle's device (every entry point holds a DeviceGuard)
+  return dev;
 }
-static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!g_num_sms) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
+static int smem_optin() { return device_smem_optin(cur_dev()); }
+static int num_sms() { return device_sms(cur_dev()); }
 
 #define LAUNCHED(h)                      \
   do {                                   \
@@ -142,6 +130,7 @@ __global__ void __launch_bounds__(256) k_kv_generate(uint4* __restrict__ K, uint
 
 extern "C" int kvt_kv_generate(kvt_handle* h, const kvt_kv_shape* s, uint64_t seed, uint64_t ctx, uint16_t* k,
                                uint16_t* v) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, nullptr))) return rc;
   const uint64_t n8 = uint64_t(s->L) * s->H * s->T * s->D / 8;
@@ -157,46 +146,11 @@ constexpr int kRingStages = 3;  // K streamed through smem in 64-token (16 KB) b
 constexpr int kRingRows = 64;
 constexpr size_t kRingBytes = size_t(kRingStages) * kRingRows * 256;
 
-// Streams rows [0, n) of `src` (256 B each) through the smem ring; calls
-// f(t, row) once per row from the half-warp that owns it (16 lanes, one
-// uint4 each). `seq` counts ring chunks across calls (mbarrier parity).
+// Streams rows [0, n) of `src` (256 B each) through the smem ring, handing
+// each half-warp its kRingRows / 16 rows of a ring chunk together: f(t[],
+// live[], v[]) (16 lanes, one uint4 of each row per lane) can batch per-row
+// work across them. `seq` counts ring chunks across calls (mbarrier parity).
 // Block-uniform; warp-uniform trip counts (f may use half-warp shuffles).
-template <class F>
-__device__ __forceinline__ void stream_rows(const uint4* __restrict__ src, int n, uint4* ring, uint64_t* full,
-                                            uint32_t& seq, F&& f) {
-  const int tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
-  const int nch = (n + kRingRows - 1) / kRingRows;
-  auto issue = [&](int c) {
-    const int st = (seq + c) % kRingStages;
-    const int rows = min(kRingRows, n - c * kRingRows);
-    mbar_expect_tx(&full[st], rows * 256);
-    bulk_g2s(ring + static_cast<size_t>(st) * kRingRows * 16, src + static_cast<size_t>(c) * kRingRows * 16,
-             rows * 256, &full[st]);
-  };
-  if (tid == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem use before async writes
-    for (int c = 0; c < min(nch, kRingStages); ++c) issue(c);
-  }
-  for (int c = 0; c < nch; ++c) {
-    const uint32_t g = seq + c;
-    const int st = g % kRingStages;
-    mbar_wait(&full[st], (g / kRingStages) & 1);
-    const int rows = min(kRingRows, n - c * kRingRows);
-    const uint4* base = ring + static_cast<size_t>(st) * kRingRows * 16;
-#pragma unroll
-    for (int u = 0; u < kRingRows / 16; ++u) {
-      const int r = (hw & ~1) * (kRingRows / 16) + 2 * u + (hw & 1);  // both half-warps of a warp iterate together
-      const uint4 v = r < rows ? base[r * 16 + l16] : make_uint4(0, 0, 0, 0);
-      f(c * kRingRows + r, r < rows, v);
-    }
-    __syncthreads();  // stage consumed by every thread
-    if (tid == 0 && c + kRingStages < nch) issue(c + kRingStages);
-  }
-  seq += nch;
-}
-
-// stream_rows with the half-warp's kRingRows / 16 rows of a ring chunk handed
-// over together: f(t[], live[], v[]) can batch per-row work across them.
 template <class F>
 __device__ __forceinline__ void stream_rows4(const uint4* __restrict__ src, int n, uint4* ring, uint64_t* full,
                                              uint32_t& seq, F&& f, uint64_t pol = 0) {
@@ -290,7 +244,9 @@ __device__ __forceinline__ float half_butterfly4(const float (&p)[4]) {
 constexpr int kUnroll = 4;
 
 // knorm: squared L2 norm of every key (larger = keep).
-__global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, float* __restrict__ out, long long ntok) {
+// KVT_CODEC_KNORM_KEEP_LOW: the negated norm (low norms rank first).
+__global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, float* __restrict__ out, long long ntok,
+                                               float sign) {
   const int l16 = threadIdx.x & 15;
   const long long hw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
   const long long nhw = (gridDim.x * (long long)blockDim.x) >> 4;
@@ -307,7 +263,7 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
     for (int u = 0; u < kUnroll; ++u) {
       const long long t = t0 + u * nhw;
       const float n2 = half_butterfly(chunk_sumsq(v[u]));
-      if (t < ntok && l16 == 0) out[t] = n2;
+      if (t < ntok && l16 == 0) out[t] = sign * n2;
     }
   }
 }
@@ -614,10 +570,13 @@ __device__ __forceinline__ float quant_row_i8(const float (&x)[8], uint8_t* tile
   return a > 0.0f ? __fdiv_rn(a, 127.0f) : 0.0f;
 }
 
-// Synthetic window queries of every slice -> int8 Q8 tile (SW128 layout, rows
-// >= R zero) + per-row scale, one 256-thread block per slice. Independent of
-// the KV chunk; the main kernel bulk-copies it.
-__global__ void __launch_bounds__(256) k_snap_q(uint8_t* __restrict__ qbuf, int H, int W, int G, uint64_t q_seed) {
+// Window queries of every slice -> int8 Q8 tile (SW128 layout, rows >= R
+// zero) + per-row scale, one 256-thread block per slice; the main kernel
+// bulk-copies it. q: the caller's bf16 [L][H*G][W][128] observation-window
+// queries, or null for the synthetic queries of q_seed (then independent of
+// the KV chunk and cached per shape).
+__global__ void __launch_bounds__(256) k_snap_q(uint8_t* __restrict__ qbuf, const uint16_t* __restrict__ q, int H,
+                                                int W, int G, uint64_t q_seed) {
   __shared__ __align__(1024) uint8_t q8[128 * 128];
   __shared__ float sig[128];
   const int slice = blockIdx.x, l = slice / H, h = slice % H, R = W * G;
@@ -632,7 +591,7 @@ __global__ void __launch_bounds__(256) k_snap_q(uint8_t* __restrict__ qbuf, int 
       if (r < R) {
         const int g = r / W, w = r - g * W;
         const uint64_t idx = ((uint64_t(l) * Hq + uint64_t(h * G + g)) * uint64_t(W) + uint64_t(w)) * kD + d;
-        v = bf2f(synth_bf16(q_seed, 0x51ull, idx, d % 16 == 3));
+        v = q ? bf2f(q[idx]) : bf2f(synth_bf16(q_seed, 0x51ull, idx, d % 16 == 3));
       }
       x[e] = v;
     }
@@ -1010,7 +969,7 @@ static int64_t ws_snapq(const kvt_kv_shape* s) { return al256(int64_t(kSnapQByte
 
 // qbuf: ws_snapq(s) bytes of device workspace for the Q8 tiles
 static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                         float* scores, uint8_t* qbuf) {
+                         const uint16_t* q, float* scores, uint8_t* qbuf) {
   const int S = s->L * s->H, T = s->T, W = c->window, G = c->q_heads;
   if (W * G > 128 || W > T || W < 0 || G < 1) return set_error(KVT_EINVAL, "snapkv window x q_heads must be <= 128");
   if (c->pool < 1 || (c->pool & 1) == 0 || c->pool > 15)
@@ -1035,12 +994,10 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   const int slack = static_cast<int>(std::min<size_t>(1024, size_t(smem_optin()) - std::min(core, size_t(smem_optin()))));
   const size_t smem = core + slack;
   auto kern = eg ? k_snapkv_tc<kSnapTpcGlobal, true> : k_snapkv_tc<kSnapTpcSmem, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[eg]) {
-    KVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    KVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr[eg] = true;
-  }
+  KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(kern), h->device, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem)));
+  KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(kern), h->device,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   uint8_t* escr = nullptr;
   if (eg) {  // E scratch slots (one per SM) live with the handle
     const size_t need = size_t(kSnapESlots) * kSnapESlotBytes;
@@ -1053,25 +1010,30 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     }
     escr = static_cast<uint8_t*>(h->snape);
   }
-  (void)qbuf;  // Q8 tiles live in the handle's cache (same for every chunk of this shape)
-  const unsigned long long key[5] = {static_cast<unsigned long long>(s->L), static_cast<unsigned long long>(s->H),
-                                     static_cast<unsigned long long>(W), static_cast<unsigned long long>(G),
-                                     static_cast<unsigned long long>(c->q_seed)};
-  const size_t qbytes = size_t(kSnapQBytes) * S;
-  if (!h->snapq || h->snapq_bytes < qbytes || std::memcmp(key, h->snapq_key, sizeof key) != 0) {
-    if (h->snapq_bytes < qbytes) {
-      if (h->snapq) KVT_CUDA_TRY(cudaFree(h->snapq));
-      h->snapq = nullptr;
-      h->snapq_bytes = 0;
-      KVT_CUDA_TRY(cudaMalloc(&h->snapq, qbytes));
-      h->snapq_bytes = qbytes;
-    }
-    k_snap_q<<<S, 256, 0, h->stream>>>(static_cast<uint8_t*>(h->snapq), s->H, W, G, static_cast<uint64_t>(c->q_seed));
+  if (q) {  // caller's queries: this chunk's Q8 tiles into the workspace
+    k_snap_q<<<S, 256, 0, h->stream>>>(qbuf, q, s->H, W, G, 0);
     LAUNCHED(h);
-    KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));  // once per shape: safe for later launches on any stream
-    std::memcpy(h->snapq_key, key, sizeof key);
+  } else {  // synthetic queries: Q8 tiles cached in the handle (same for every chunk of this shape)
+    const unsigned long long key[5] = {static_cast<unsigned long long>(s->L), static_cast<unsigned long long>(s->H),
+                                       static_cast<unsigned long long>(W), static_cast<unsigned long long>(G),
+                                       static_cast<unsigned long long>(c->q_seed)};
+    const size_t qbytes = size_t(kSnapQBytes) * S;
+    if (!h->snapq || h->snapq_bytes < qbytes || std::memcmp(key, h->snapq_key, sizeof key) != 0) {
+      if (h->snapq_bytes < qbytes) {
+        if (h->snapq) KVT_CUDA_TRY(cudaFree(h->snapq));
+        h->snapq = nullptr;
+        h->snapq_bytes = 0;
+        KVT_CUDA_TRY(cudaMalloc(&h->snapq, qbytes));
+        h->snapq_bytes = qbytes;
+      }
+      k_snap_q<<<S, 256, 0, h->stream>>>(static_cast<uint8_t*>(h->snapq), nullptr, s->H, W, G,
+                                         static_cast<uint64_t>(c->q_seed));
+      LAUNCHED(h);
+      KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));  // once per shape: safe for later launches on any stream
+      std::memcpy(h->snapq_key, key, sizeof key);
+    }
+    qbuf = static_cast<uint8_t*>(h->snapq);
   }
-  qbuf = static_cast<uint8_t*>(h->snapq);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(Cn, S);
   cfg.blockDim = dim3(kSnapThreads);
@@ -1085,13 +1047,16 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   cfg.attrs = at;
   cfg.numAttrs = 1;
   {  // persistent: as many clusters as fit at once, each loops over slices
-    static int active[2][kSnapMaxC + 1] = {};
-    int& na = active[eg][Cn];
-    if (!na) {
+    struct Q {
+      decltype(kern) k;
+      cudaLaunchConfig_t* cfg;
+    } q{kern, &cfg};
+    const int na = cached_per_device(reinterpret_cast<const void*>(kern), h->device, Cn, [](void* a) {
+      Q* q = static_cast<Q*>(a);
       int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = S;
-      na = n;
-    }
+      return cudaOccupancyMaxActiveClusters(&n, q->k, q->cfg) == cudaSuccess ? n : -1;
+    }, &q);
+    if (na < 1) return set_error(KVT_ECUDA, "snapkv: cudaOccupancyMaxActiveClusters found no resident cluster");
     // KVT_SNAP_SMS: an SM budget (scheduling knob for running beside other
     // streams' kernels): as many whole clusters as fit in it
     const char* ge = getenv("KVT_SNAP_SMS");
@@ -1105,21 +1070,19 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
 }
 
 static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                         float* scores, uint8_t* snapq, unsigned long long* fixed) {
+                         const uint16_t* q, float* scores, uint8_t* snapq, unsigned long long* fixed) {
   const int S = s->L * s->H, T = s->T;
   cudaStream_t st = h->stream;
   if (c->scorer == KVT_SCORER_KNORM) {
     const long long ntok = static_cast<long long>(S) * T;
     const long long want = (ntok * 16 + 255) / 256;
     const int blocks = static_cast<int>(std::min<long long>(want, num_sms() * 16LL));
-    k_knorm<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), scores, ntok);
+    k_knorm<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), scores, ntok,
+                                     (c->flags & KVT_CODEC_KNORM_KEEP_LOW) ? -1.0f : 1.0f);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_KEYDIFF && kd_cluster_smem(T) <= 100 * 1024 && T <= kKdC * 16000) {
-    static bool attr = false;
-    if (!attr) {
-      KVT_CUDA_TRY(cudaFuncSetAttribute(k_keydiff_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-      attr = true;
-    }
+    KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(k_keydiff_cluster), h->device,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     k_keydiff_cluster<<<dim3(kKdC, S), 256, kd_cluster_smem(T), st>>>(reinterpret_cast<const uint4*>(k), scores, T);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_KEYDIFF) {
@@ -1131,7 +1094,7 @@ static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
                                           reinterpret_cast<const long long*>(fixed), scores, T);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_SNAPKV) {
-    return launch_snapkv(h, s, c, k, scores, snapq);
+    return launch_snapkv(h, s, c, k, q, scores, snapq);
   } else {
     return set_error(KVT_EINVAL, "unknown scorer");
   }
@@ -1149,12 +1112,13 @@ static int ensure_scratch(kvt_handle* h, size_t bytes) {
 }
 
 extern "C" int kvt_token_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                                float* scores) {
+                                const uint16_t* q, float* scores) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, c))) return rc;
   if ((rc = ensure_scratch(h, ws_snapq(s) + ws_fixed(s)))) return rc;
   char* b = static_cast<char*>(h->scratch);
-  return launch_scores(h, s, c, k, scores, reinterpret_cast<uint8_t*>(b),
+  return launch_scores(h, s, c, k, q, scores, reinterpret_cast<uint8_t*>(b),
                        reinterpret_cast<unsigned long long*>(b + ws_snapq(s)));
 }
 
@@ -1298,11 +1262,8 @@ static int launch_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
   const int S = s->L * s->H;
   const size_t smem = sizeof(uint32_t) * (size_t(s->T) + size_t(s->T) / 16 + 1);
   const int in_smem = smem <= 160 * 1024;
-  static bool attr = false;
-  if (!attr) {
-    KVT_CUDA_TRY(cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr = true;
-  }
+  KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(k_topk), h->device, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024));
   k_topk<<<S, kTopkThreads, in_smem ? smem : 0, h->stream>>>(scores, idx, s->T, c->keep, in_smem);
   LAUNCHED(h);
   return KVT_OK;
@@ -1310,6 +1271,7 @@ static int launch_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
 
 extern "C" int kvt_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const float* scores,
                         int32_t* idx) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, c))) return rc;
   return launch_topk(h, s, c, scores, idx);
@@ -1600,6 +1562,7 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
   char* b = static_cast<char*>(blob);
   const int S = s->L * s->H, kk = c->keep;
   cudaStream_t st = h->stream;
+  if (m.identity) return KVT_OK;  // nothing to write: the source KV is the blob
   if (c->bits == 16) {
     dim3 rows_grid((kk + 16 * kGRows - 1) / (16 * kGRows), S);
     k_gather16<<<rows_grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
@@ -1619,6 +1582,7 @@ static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg
 
 extern "C" int kvt_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
                         const uint16_t* v, const int32_t* idx, void* blob) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, c))) return rc;
   return launch_pack(h, s, c, k, v, idx, blob);
@@ -1662,10 +1626,13 @@ __global__ void __launch_bounds__(256) k_unpack(const uint8_t* __restrict__ blob
 
 extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const void* blob,
                           uint16_t* k_out, uint16_t* v_out) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, c))) return rc;
   kvt_blob_map m;
   blob_map(*s, *c, &m);
+  if (m.identity)
+    return set_error(KVT_EINVAL, "identity configuration: the blob aliases the source KV (kvt_blob_map.identity)");
   const int S = s->L * s->H, kk = c->keep;
   const char* b = static_cast<const char*>(blob);
   if (c->bits == 16) {
@@ -1681,234 +1648,6 @@ extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_
 }
 
 
-// ------------------------------------------------------- fused compress
-//
-// One thread-block cluster of kFuseC CTAs per (layer, kv-head) slice does
-// scores -> top-k -> gather + quantise + pack in a single launch. Each CTA
-// owns a contiguous token range of the slice. Cross-CTA steps go through
-// distributed shared memory: keydiff's mean direction (exact int64 fixed
-// point, so the sum order does not matter), the four radix-select
-// histograms and the (above, equal) counts that place each CTA's kept
-// indices. Only kFuseC x (#clusters in flight) slices are live at a time
-// (~40 x 2 MiB of K at T = 8192), so the re-reads of K (keydiff's second
-// pass, the kept rows in the pack) are L2 hits: HBM sees K once, the kept V
-// rows once and the blob once. Bit-identical to the unfused kernels.
-constexpr int kFuseC = 8;
-constexpr int kFuseThreads = 256;
-
-constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-constexpr size_t kFuseUnion = cmax(kRingBytes, cmax(sizeof(PackKSmem), 16 * kD * sizeof(long long)));
-constexpr size_t kFuseMaxSmem = 200 * 1024;
-using FuseScan = cub::BlockScan<int, kFuseThreads>;
-
-static size_t fuse_smem_bytes(int T) {
-  const size_t per = (T + kFuseC - 1) / kFuseC;
-  return kFuseUnion + 2 * al256(4 * per);
-}
-
-__global__ void __cluster_dims__(kFuseC, 1, 1) __launch_bounds__(kFuseThreads, 2)
-    k_compress_fused(const uint4* __restrict__ K, const uint4* __restrict__ V, int T, int k, int bits, int scorer,
-                     kvt_blob_map m, char* __restrict__ blob) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = static_cast<int>(cl.block_rank());
-  const int slice = blockIdx.y, tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
-  const int per = (T + kFuseC - 1) / kFuseC;
-  const int t_lo = min(T, rank * per), t_hi = min(T, t_lo + per), n_loc = t_hi - t_lo;
-  extern __shared__ __align__(16) uint8_t fsm[];
-  PackKSmem& pk = *reinterpret_cast<PackKSmem*>(fsm);
-  long long(*part)[kD] = reinterpret_cast<long long(*)[kD]>(fsm);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(fsm + kFuseUnion);
-  float* kinv = reinterpret_cast<float*>(fsm + kFuseUnion + ((4 * per + 255) & ~255));  // keydiff: per-token 1/|k|
-  __shared__ int hist[2][256];
-  __shared__ int tot[256];
-  __shared__ long long sfix[kD];
-  __shared__ float sdir[kD];
-  __shared__ int cnt[2];
-  __shared__ int s_rem, s_bucket;
-  __shared__ typename FuseScan::TempStorage scan_tmp;
-  const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
-  uint4* ring = reinterpret_cast<uint4*>(fsm);  // aliases part / pk: used in different phases
-  __shared__ __align__(8) uint64_t full[kRingStages];
-  uint32_t seq = 0;
-  if (tid == 0) {
-    for (int i = 0; i < kRingStages; ++i) mbar_init(&full[i], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  int32_t* bidx = reinterpret_cast<int32_t*>(blob + m.idx_off);
-  if (k == T) {  // every token kept: the indices are 0..T-1 whatever the scores
-    for (int t = tid; t < n_loc; t += kFuseThreads) bidx[static_cast<size_t>(slice) * k + t_lo + t] = t_lo + t;
-    cl.sync();
-  } else {
-  // ---- phase 1: token scores of [t_lo, t_hi) as orderable keys
-  if (scorer == KVT_SCORER_KNORM) {
-    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
-      const float n2 = half_butterfly(chunk_sumsq(v));
-      if (live && l16 == 0) keys[t] = score_key(n2);
-    });
-  } else {  // keydiff: exact fixed-point sum of unit keys over the whole slice, then cosine
-    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t cnt_t = 0;  // <= per / 16 tokens per lane: biased u32 sums cannot wrap
-    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {
-      const float inv = kd_inv(half_butterfly(chunk_sumsq(v)));
-      if (live) {
-        kd_fix_add(v, __fmul_rn(inv, kKdFx), acc);
-        ++cnt_t;
-        if (l16 == 0) kinv[t] = inv;
-      }
-    });
-#pragma unroll
-    for (int i = 0; i < 8; ++i) part[hw][l16 * 8 + i] = static_cast<int32_t>(acc[i] - cnt_t * 0x4B400000u);
-    __syncthreads();
-    if (tid < kD) {
-      long long sum = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) sum += part[i][tid];
-      sfix[tid] = sum;
-    }
-    cluster_sync_smem();
-    if (tid < kD) {
-      long long sum = 0;
-      for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(sfix, c)[tid];
-      sdir[tid] = __fmul_rn(__ll2float_rn(sum), 1.0f / kKdFx);
-    }
-    __syncthreads();
-    float2 sd[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sd[q] = make_float2(sdir[l16 * 8 + 2 * q], sdir[l16 * 8 + 2 * q + 1]);
-    stream_rows(Ks, n_loc, ring, full, seq, [&](int t, bool live, const uint4& v) {  // second pass: L2 hits
-      const float p = half_butterfly(chunk_dot(v, sd));
-      if (live && l16 == 0) keys[t] = score_key(-__fmul_rn(p, kinv[t]));
-    });
-  }
-  __syncthreads();
-
-  // ---- phase 2: cluster-wide MSB-first radix select of the k-th key
-  uint32_t prefix = 0, mask = 0;
-  int rem = k;
-  for (int shift = 24, rd = 0; shift >= 0; shift -= 8, ++rd) {
-    int* h = hist[rd & 1];
-    h[tid] = 0;  // kFuseThreads == 256 bins
-    __syncthreads();
-    for (int t = tid; t < n_loc; t += kFuseThreads) {
-      const uint32_t key = keys[t];
-      if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255], 1);
-    }
-    cluster_sync_smem();
-    {
-      int sum = 0;
-      for (int c = 0; c < kFuseC; ++c) sum += cl.map_shared_rank(h, c)[tid];
-      tot[tid] = sum;
-    }
-    __syncthreads();
-    if (tid < 32) select_bucket(tot, rem, &s_bucket, &s_rem);
-    __syncthreads();
-    prefix |= uint32_t(s_bucket) << shift;
-    mask |= 255u << shift;
-    rem = s_rem;
-  }
-  const uint32_t kth = prefix;
-  const int ties = rem;
-
-  // ---- order-preserving compaction of the kept indices (ascending)
-  const int seg = (n_loc + kFuseThreads - 1) / kFuseThreads;
-  const int s0 = min(n_loc, tid * seg), s1 = min(n_loc, s0 + seg);
-  int above = 0, eq = 0;
-  for (int t = s0; t < s1; ++t) {
-    const uint32_t key = keys[t];
-    above += key > kth;
-    eq += key == kth;
-  }
-  int above_before, eq_before, above_all, eq_all;
-  FuseScan(scan_tmp).ExclusiveSum(above, above_before, above_all);
-  __syncthreads();
-  FuseScan(scan_tmp).ExclusiveSum(eq, eq_before, eq_all);
-  if (tid == 0) {
-    cnt[0] = above_all;
-    cnt[1] = eq_all;
-  }
-  cluster_sync_smem();
-  int a_base = 0, e_base = 0;
-  for (int c = 0; c < rank; ++c) {
-    const int* rc = cl.map_shared_rank(cnt, c);
-    a_base += rc[0];
-    e_base += rc[1];
-  }
-  {
-    int eq_seen = e_base + eq_before;
-    int pos = a_base + above_before + min(eq_seen, ties);
-    int32_t* out = bidx + static_cast<size_t>(slice) * k;
-    for (int t = s0; t < s1; ++t) {
-      const uint32_t key = keys[t];
-      if (key > kth) {
-        out[pos++] = t_lo + t;
-      } else if (key == kth) {
-        if (eq_seen < ties) out[pos++] = t_lo + t;
-        ++eq_seen;
-      }
-    }
-  }
-  cl.sync();  // every CTA's indices are visible; no DSMEM access after this point
-  }
-
-  // ---- phase 3: gather + quantise + pack (rows re-read from L2)
-  if (bits == 16) {
-    uint4* ko = reinterpret_cast<uint4*>(blob + m.kcode_off);
-    uint4* vo = reinterpret_cast<uint4*>(blob + m.vcode_off);
-    for (int jb = rank * 16; jb < k; jb += kFuseC * 16) {
-      const int j = jb + hw;
-      if (j < k) {
-        const int t = bidx[static_cast<size_t>(slice) * k + j];
-        const size_t src = (static_cast<size_t>(slice) * T + t) * 16 + l16;
-        const size_t dst = (static_cast<size_t>(slice) * k + j) * 16 + l16;
-        const uint4 a = __ldcs(K + src), b = __ldcs(V + src);
-        __stcs(ko + dst, a);
-        __stcs(vo + dst, b);
-      }
-    }
-  } else {
-    auto pack = [&](auto bits_c) {
-      constexpr int B = decltype(bits_c)::value;
-      const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
-      for (int g = rank; g < ng; g += kFuseC)
-        pack_k_group<B>(K, bidx, reinterpret_cast<uint32_t*>(blob + m.kcode_off),
-                        reinterpret_cast<uint16_t*>(blob + m.kscale_off), reinterpret_cast<uint16_t*>(blob + m.kzero_off),
-                        T, k, slice, g, pk);
-      // warp-uniform trip count: both half-warps of a warp run every iteration
-      for (int wb = (rank * 16 + (hw & ~1)) * kVRows; wb < k; wb += kFuseC * 16 * kVRows)
-        pack_v_rows<B>(V, bidx, nullptr, reinterpret_cast<uint32_t*>(blob + m.vcode_off),
-                       reinterpret_cast<uint16_t*>(blob + m.vscale_off), reinterpret_cast<uint16_t*>(blob + m.vzero_off),
-                       T, k, slice, wb + (hw & 1) * kVRows);
-    };
-    if (bits == 8) pack(std::integral_constant<int, 8>{});
-    else if (bits == 4) pack(std::integral_constant<int, 4>{});
-    else pack(std::integral_constant<int, 2>{});
-  }
-}
-
-static bool fused_ok(const kvt_kv_shape* s, const kvt_codec_cfg* c) {
-  return (c->scorer != KVT_SCORER_SNAPKV || c->keep == s->T) && fuse_smem_bytes(s->T) <= kFuseMaxSmem;
-}
-
-static int launch_fused(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                        const uint16_t* v, void* blob) {
-  kvt_blob_map m;
-  blob_map(*s, *c, &m);
-  const size_t smem = fuse_smem_bytes(s->T);
-  static bool attr = false;
-  if (!attr) {
-    KVT_CUDA_TRY(cudaFuncSetAttribute(k_compress_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kFuseMaxSmem)));
-    attr = true;
-  }
-  dim3 grid(kFuseC, s->L * s->H);
-  k_compress_fused<<<grid, kFuseThreads, smem, h->stream>>>(reinterpret_cast<const uint4*>(k),
-                                                             reinterpret_cast<const uint4*>(v), s->T, c->keep, c->bits,
-                                                             c->scorer, m, static_cast<char*>(blob));
-  LAUNCHED(h);
-  return KVT_OK;
-}
-
 // ---------------------------------------------------------------- compress
 
 __global__ void __launch_bounds__(256) k_iota(int32_t* __restrict__ idx, int T, long long n) {
@@ -1916,7 +1655,8 @@ __global__ void __launch_bounds__(256) k_iota(int32_t* __restrict__ idx, int T, 
 }
 
 extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                            const uint16_t* v, void* workspace, void* blob) {
+                            const uint16_t* v, const uint16_t* q, void* workspace, void* blob) {
+  KVT_ON_DEVICE(h);
   int rc;
   if ((rc = check_shape(s, c))) return rc;
   char* w = static_cast<char*>(workspace);
@@ -1924,6 +1664,7 @@ extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_code
   uint8_t* snapq = reinterpret_cast<uint8_t*>(w + ws_scores(s));
   auto* fixed = reinterpret_cast<unsigned long long*>(w + ws_scores(s) + ws_snapq(s));
   int32_t* idx = reinterpret_cast<int32_t*>(w + ws_scores(s) + ws_snapq(s) + ws_fixed(s));
+  if (c->keep == s->T && c->bits == 16) return KVT_OK;  // identity: the source KV is the blob (kvt_blob_map)
   if (c->keep == s->T) {  // every token kept: indices 0..T-1 whatever the scores; no scoring pass
     const long long n = static_cast<long long>(s->L) * s->H * s->T;
     k_iota<<<static_cast<int>(std::min<long long>((n + 255) / 256, num_sms() * 8LL)), 256, 0, h->stream>>>(idx, s->T,
@@ -1931,10 +1672,7 @@ extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_code
     LAUNCHED(h);
     return launch_pack(h, s, c, k, v, idx, blob);
   }
-  // one-launch cluster path (experimental: slower than the three kernels
-  // below at 2 CTAs/SM; profiles/README.md r1e)
-  if (fused_ok(s, c) && getenv("KVT_FUSED")) return launch_fused(h, s, c, k, v, blob);
-  if ((rc = launch_scores(h, s, c, k, scores, snapq, fixed))) return rc;
+  if ((rc = launch_scores(h, s, c, k, q, scores, snapq, fixed))) return rc;
   if ((rc = launch_topk(h, s, c, scores, idx))) return rc;
   return launch_pack(h, s, c, k, v, idx, blob);
 }

@@ -24,6 +24,10 @@ inline int64_t al256(int64_t x) { return (x + 255) & ~int64_t(255); }
 inline void blob_map(const kvt_kv_shape& s, const kvt_codec_cfg& c, kvt_blob_map* o) {
   const int64_t S = int64_t(s.L) * s.H, k = c.keep, D = s.D;
   std::memset(o, 0, sizeof(*o));
+  if (c.keep == s.T && c.bits == 16) {  // identity: the source KV is the compressed chunk
+    o->identity = 1;
+    return;
+  }
   int64_t off = 0;
   o->idx_off = off;
   o->idx_bytes = 4 * S * k;

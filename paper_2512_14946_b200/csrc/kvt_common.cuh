@@ -107,6 +107,7 @@ __device__ inline bool quality_of(const DevProfiles& p, int c, int m, double rat
 
 // Handle: device, stream, scratch, and a launch counter (bench evidence).
 struct kvt_handle {
+  ~kvt_handle();
   int device = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
@@ -119,6 +120,10 @@ struct kvt_handle {
   unsigned long long snapq_key[5] = {0, 0, 0, 0, 0};
   void* snape = nullptr;  // snapkv E scratch slots for prefixes beyond 8192 tokens
   size_t snape_bytes = 0;
+  // tier-move executor: two copy streams per direction (d2h x2, h2d x2),
+  // created on first use, destroyed with the handle
+  cudaStream_t move_s[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t move_start = nullptr, move_done[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace kvt {
@@ -128,6 +133,38 @@ struct Error {
 };
 
 int set_error(int code, const std::string& msg);
+
+// Per-device facts and one-time kernel attributes. The ABI lets one process
+// drive several devices (kvt_create(device, ...)) from several threads (the
+// reference's `compare --jobs`), so nothing here is a plain static: every
+// cache is keyed by device ordinal and guarded by a mutex.
+int device_sms(int dev);
+int device_smem_optin(int dev);
+// cudaFuncSetAttribute(fn, a, value) on device `dev` (current device must be
+// dev, see DeviceGuard), issued once per (fn, a, dev, value)
+cudaError_t func_attr(const void* fn, int dev, cudaFuncAttribute a, int value);
+// value cached per (fn, dev, key); compute() runs once (occupancy queries)
+int cached_per_device(const void* fn, int dev, long long key, int (*compute)(void*), void* arg);
+
+// Makes h->device current for the duration of an ABI call and restores the
+// caller's device afterwards (no cudaSetDevice side effect leaks out).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+#define KVT_ON_DEVICE(hp)                                                      \
+  if (!(hp)) return ::kvt::set_error(KVT_EINVAL, "null handle");               \
+  ::kvt::DeviceGuard kvt_dg__((hp)->device)
 
 #define KVT_CUDA_TRY(expr)                                                     \
   do {                                                                         \

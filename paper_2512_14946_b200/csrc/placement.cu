@@ -19,12 +19,14 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <memory>
 #include <limits>
+#include <map>
 #include <mutex>
-#include <unordered_map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -39,6 +41,50 @@ static thread_local std::string g_err;
 int set_error(int code, const std::string& msg) {
   g_err = msg;
   return code;
+}
+
+namespace {
+std::mutex g_dev_mu;
+std::map<int, std::pair<int, int>> g_dev_info;  // device -> (SMs, smem opt-in)
+std::map<std::tuple<const void*, int, int>, int> g_attr;  // (fn, device, attribute) -> value set
+std::map<std::tuple<const void*, int, long long>, int> g_cached;
+
+const std::pair<int, int>& dev_info(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_dev_info.find(dev);
+  if (it == g_dev_info.end()) {
+    int sms = 0, optin = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    it = g_dev_info.emplace(dev, std::make_pair(sms > 0 ? sms : 148, optin > 0 ? optin : 232448)).first;
+  }
+  return it->second;
+}
+}  // namespace
+
+int device_sms(int dev) { return dev_info(dev).first; }
+int device_smem_optin(int dev) { return dev_info(dev).second; }
+
+cudaError_t func_attr(const void* fn, int dev, cudaFuncAttribute a, int value) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  const auto key = std::make_tuple(fn, dev, static_cast<int>(a));
+  auto it = g_attr.find(key);
+  if (it != g_attr.end() && it->second == value) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, a, value);
+  if (e == cudaSuccess) g_attr[key] = value;
+  return e;
+}
+
+int cached_per_device(const void* fn, int dev, long long key, int (*compute)(void*), void* arg) {
+  const auto k = std::make_tuple(fn, dev, key);
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_cached.find(k);
+    if (it != g_cached.end()) return it->second;
+  }
+  const int v = compute(arg);  // outside the lock: may call into the driver
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  return g_cached.emplace(k, v).first->second;
 }
 
 }  // namespace kvt
@@ -66,7 +112,8 @@ extern "C" int kvt_create(int device, void* stream, kvt_handle** out) {
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0)
     return set_error(KVT_ECUDA, std::string("no CUDA device visible: ") + cudaGetErrorString(e));
-  KVT_CUDA_TRY(cudaSetDevice(device));
+  if (device < 0 || device >= n) return set_error(KVT_EINVAL, "device ordinal out of range");
+  DeviceGuard dg(device);
   cudaDeviceProp prop;
   KVT_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10)
@@ -78,16 +125,25 @@ extern "C" int kvt_create(int device, void* stream, kvt_handle** out) {
   return KVT_OK;
 }
 
+kvt_handle::~kvt_handle() {
+  DeviceGuard dg(device);
+  if (scratch) cudaFree(scratch);
+  if (snapq) cudaFree(snapq);
+  if (snape) cudaFree(snape);
+  for (int i = 0; i < 4; ++i) {
+    if (move_s[i]) cudaStreamSynchronize(move_s[i]), cudaStreamDestroy(move_s[i]);
+    if (move_done[i]) cudaEventDestroy(move_done[i]);
+  }
+  if (move_start) cudaEventDestroy(move_start);
+}
+
 extern "C" int kvt_destroy(kvt_handle* h) {
-  if (!h) return KVT_OK;
-  if (h->scratch) cudaFree(h->scratch);
-  if (h->snapq) cudaFree(h->snapq);
-  if (h->snape) cudaFree(h->snape);
-  delete h;
+  delete h;  // frees scratch, snapkv caches and the tier-move streams / events
   return KVT_OK;
 }
 
 extern "C" int kvt_sync(kvt_handle* h) {
+  KVT_ON_DEVICE(h);
   KVT_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return KVT_OK;
 }
@@ -182,9 +238,10 @@ struct kvt_pset {
   uint64_t id = 0;
 };
 
-static uint64_t g_pset_counter = 0;
+static std::atomic<uint64_t> g_pset_counter{0};
 
 extern "C" int kvt_pset_create(kvt_handle* h, const kvt_profiles* pr, kvt_pset** out) {
+  KVT_ON_DEVICE(h);
   if (!h || !pr || !out) return set_error(KVT_EINVAL, "null argument");
   if (pr->n_ctx < 0 || pr->n_methods <= 0 || pr->n_methods > KVT_MAX_METHODS)
     return set_error(KVT_EINVAL, "bad profile set dimensions");
@@ -239,6 +296,7 @@ extern "C" int kvt_pset_create(kvt_handle* h, const kvt_profiles* pr, kvt_pset**
 }
 
 extern "C" int kvt_pset_destroy(kvt_pset* p) {
+  KVT_ON_DEVICE((p ? p->h : nullptr));
   if (!p) return KVT_OK;
   cudaFree(p->buf);
   delete p;
@@ -373,6 +431,7 @@ static int launch_score(kvt_handle* h, const DevProfiles& P, const DevSpace& S, 
 extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
                                     const kvt_space* space, const kvt_params* params, int64_t* size,
                                     double* quality, uint8_t* valid, double* ttft, double* utility) {
+  KVT_ON_DEVICE(h);
   DevSpace S;
   DevTiers T;
   int rc;
@@ -399,13 +458,9 @@ extern "C" int kvt_score_candidates(kvt_handle* h, const kvt_pset* p, const kvt_
 }
 
 static int num_sms_p() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return v;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return device_sms(dev);
 }
 
 // ---------------------------------------------------------------- oracle_mckp
@@ -563,6 +618,7 @@ __global__ void __launch_bounds__(1024) k_mckp_pick(const double* __restrict__ t
 extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
                                const kvt_space* space, const kvt_params* params, double max_assignments,
                                double* total_utility, kvt_best* out) {
+  KVT_ON_DEVICE(h);
   DevSpace S;
   DevTiers T;
   int rc;
@@ -735,6 +791,7 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
 
 extern "C" int kvt_best_config(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
                                const kvt_space* space, const kvt_params* params, int32_t rule, kvt_best* out) {
+  KVT_ON_DEVICE(h);
   DevSpace S;
   DevTiers T;
   int rc;
@@ -1472,6 +1529,7 @@ static int store_fetch_ctl(kvt_store* s, Ctl* c) {
 
 extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_tiers, int32_t n_ctx,
                                 kvt_store** out) {
+  KVT_ON_DEVICE(h);
   DevTiers T;
   int rc;
   if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
@@ -1552,6 +1610,7 @@ extern "C" int kvt_store_create(kvt_handle* h, const kvt_tier* tiers, int32_t n_
 }
 
 extern "C" int kvt_store_destroy(kvt_store* s) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   if (!s) return KVT_OK;
   cudaFree(s->buf);
   cudaFree(s->tbuf);
@@ -1564,6 +1623,7 @@ extern "C" int kvt_store_destroy(kvt_store* s) {
 }
 
 extern "C" int kvt_store_bind_space(kvt_store* s, const kvt_space* space) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   DevSpace S;
   int rc;
   if ((rc = resolve_space(space, &S))) return rc;
@@ -1620,6 +1680,7 @@ static int run_store_op(kvt_store* s, int op, int c, const kvt_entry& e, kvt_ent
 }
 
 extern "C" int kvt_store_add(kvt_store* s, int32_t ctx, const kvt_entry* e) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   if (e->tier_index < 0 || e->tier_index >= s->TT.T)
     return set_error(KVT_EVALIDATION, "unknown tier index " + std::to_string(e->tier_index));
   if (e->original_size_bytes <= 0) return set_error(KVT_EVALIDATION, "original size must be > 0");
@@ -1633,12 +1694,14 @@ extern "C" int kvt_store_add(kvt_store* s, int32_t ctx, const kvt_entry* e) {
 }
 
 extern "C" int kvt_store_remove(kvt_store* s, int32_t ctx, kvt_entry* removed) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   kvt_entry x{};
   kvt_entry tmp{};
   return run_store_op(s, OP_REMOVE, ctx, x, removed ? removed : &tmp);
 }
 
 extern "C" int kvt_store_reconfigure(kvt_store* s, int32_t ctx, int32_t m, double ratio) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   if (!(ratio > 0.0) || ratio > 1.0 || !std::isfinite(ratio))
     return set_error(KVT_EVALIDATION, "compression ratio must be in (0, 1]");
   kvt_entry x{};
@@ -1666,6 +1729,7 @@ __global__ void k_touch_many(DevStore st, const int32_t* ctx, const int64_t* sta
 }
 
 extern "C" int kvt_store_touch_many(kvt_store* s, const int32_t* ctx, const int64_t* stamps, int64_t n) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   if (n <= 0) return KVT_OK;
   char* d = nullptr;
   const size_t bc = sizeof(int32_t) * size_t(n), bs = sizeof(int64_t) * size_t(n);
@@ -1684,12 +1748,14 @@ extern "C" int kvt_store_touch_many(kvt_store* s, const int32_t* ctx, const int6
 }
 
 extern "C" int kvt_store_touch(kvt_store* s, int32_t ctx, int64_t stamp) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   kvt_entry x{};
   x.last_access = stamp;
   return run_store_op(s, OP_TOUCH, ctx, x, nullptr);
 }
 
 extern "C" int kvt_store_clear(kvt_store* s) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   k_clear<<<(s->n + 255) / 256 + 1, 256, 0, s->h->stream>>>(s->d);
   s->h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
@@ -1701,6 +1767,7 @@ extern "C" int kvt_store_clear(kvt_store* s) {
 }
 
 extern "C" int kvt_store_occupancy(kvt_store* s, int64_t* occ) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   Ctl c;
   int rc = store_fetch_ctl(s, &c);
   if (rc) return rc;
@@ -1709,6 +1776,7 @@ extern "C" int kvt_store_occupancy(kvt_store* s, int64_t* occ) {
 }
 
 extern "C" int kvt_store_snapshot(kvt_store* s, kvt_entry* out) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   const size_t n = s->n;
   std::vector<int> tier(n), meth(n);
   std::vector<double> ratio(n);
@@ -1740,6 +1808,7 @@ extern "C" int kvt_store_snapshot(kvt_store* s, kvt_entry* out) {
 }
 
 extern "C" int kvt_store_actions(kvt_store* s, kvt_action* out, int64_t n) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   Ctl c;
   int rc = store_fetch_ctl(s, &c);
   if (rc) return rc;
@@ -1890,6 +1959,7 @@ static int stage_ops(kvt_store* s, const int32_t* ctx, const int64_t* freq, cons
 extern "C" int kvt_insert_joint(kvt_store* s, const kvt_pset* p, const kvt_space* space, const kvt_params* params,
                                 int32_t rule, const int32_t* ctx, const int64_t* frequency, const int64_t* stamp,
                                 int64_t n_ops, int64_t* n_actions, int64_t* n_done) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   *n_actions = 0;
   *n_done = 0;
   StepCtx X;
@@ -1903,6 +1973,7 @@ extern "C" int kvt_insert_joint(kvt_store* s, const kvt_pset* p, const kvt_space
 
 extern "C" int kvt_resolve_overflow(kvt_store* s, const kvt_pset* p, const kvt_space* space,
                                     const kvt_params* params, int64_t* n_actions) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   StepCtx X;
   int rc;
   *n_actions = 0;
@@ -1913,6 +1984,7 @@ extern "C" int kvt_resolve_overflow(kvt_store* s, const kvt_pset* p, const kvt_s
 
 extern "C" int kvt_least_drop_update(kvt_store* s, const kvt_pset* p, const kvt_space* space,
                                      const kvt_params* params, int32_t tier_index, kvt_update* out) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   StepCtx X;
   int rc;
   if (tier_index < 0 || tier_index >= s->TT.T) return set_error(KVT_EINVAL, "tier index out of range");
@@ -1961,6 +2033,7 @@ static int sort_pairs(kvt_store* s, unsigned long long* k_in, unsigned long long
 
 extern "C" int kvt_rearrange(kvt_store* s, const kvt_pset* p, const kvt_space* space, const kvt_params* params,
                              int32_t rule, int64_t* n_actions) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   StepCtx X;
   int rc;
   *n_actions = 0;
@@ -1999,6 +2072,7 @@ extern "C" int kvt_rearrange(kvt_store* s, const kvt_pset* p, const kvt_space* s
 
 extern "C" int kvt_placement_utility(kvt_store* s, const kvt_pset* p, const kvt_space* space,
                                      const kvt_params* params, double* out) {
+  KVT_ON_DEVICE((s ? s->h : nullptr));
   StepCtx X;
   int rc;
   if ((rc = prepare(s, p, space, params, KVT_RULE_UTILITY, &X))) return rc;
@@ -2048,24 +2122,14 @@ extern "C" int kvt_placement_utility(kvt_store* s, const kvt_pset* p, const kvt_
 // handle's stream (input ready) and joined back into it (completion).
 namespace {
 constexpr int64_t kMovePiece = 8LL << 20;
-struct MoveStreams {
-  cudaStream_t s[4] = {nullptr, nullptr, nullptr, nullptr};  // d2h x2, h2d x2
-  cudaEvent_t start = nullptr, done[4] = {nullptr, nullptr, nullptr, nullptr};
-};
-std::mutex g_move_mu;
-std::unordered_map<kvt_handle*, MoveStreams> g_moves;
 
-int move_streams(kvt_handle* h, MoveStreams** out) {
-  std::lock_guard<std::mutex> lk(g_move_mu);
-  MoveStreams& m = g_moves[h];
-  if (!m.s[0]) {
-    for (int i = 0; i < 4; ++i) {
-      KVT_CUDA_TRY(cudaStreamCreateWithFlags(&m.s[i], cudaStreamNonBlocking));
-      KVT_CUDA_TRY(cudaEventCreateWithFlags(&m.done[i], cudaEventDisableTiming));
-    }
-    KVT_CUDA_TRY(cudaEventCreateWithFlags(&m.start, cudaEventDisableTiming));
+int move_streams(kvt_handle* h) {  // the handle's copy streams, created on first use
+  if (h->move_s[0]) return KVT_OK;
+  for (int i = 0; i < 4; ++i) {
+    KVT_CUDA_TRY(cudaStreamCreateWithFlags(&h->move_s[i], cudaStreamNonBlocking));
+    KVT_CUDA_TRY(cudaEventCreateWithFlags(&h->move_done[i], cudaEventDisableTiming));
   }
-  *out = &m;
+  KVT_CUDA_TRY(cudaEventCreateWithFlags(&h->move_start, cudaEventDisableTiming));
   return KVT_OK;
 }
 }  // namespace
@@ -2085,10 +2149,10 @@ extern "C" int kvt_tier_host_free(void* p) {
 extern "C" int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n) {
   if (!h || (n > 0 && !moves)) return set_error(KVT_EINVAL, "null argument");
   if (n <= 0) return KVT_OK;
-  MoveStreams* ms;
+  DeviceGuard dg(h->device);
   int rc;
-  if ((rc = move_streams(h, &ms))) return rc;
-  KVT_CUDA_TRY(cudaEventRecord(ms->start, h->stream));
+  if ((rc = move_streams(h))) return rc;
+  KVT_CUDA_TRY(cudaEventRecord(h->move_start, h->stream));
   bool used[4] = {false, false, false, false};
   int next[2] = {0, 0};  // round-robin per direction class (0: to host, 1: to device)
   for (int64_t i = 0; i < n; ++i) {
@@ -2102,18 +2166,18 @@ extern "C" int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n) {
       const int si = cls * 2 + next[cls];
       next[cls] ^= 1;
       if (!used[si]) {
-        KVT_CUDA_TRY(cudaStreamWaitEvent(ms->s[si], ms->start, 0));
+        KVT_CUDA_TRY(cudaStreamWaitEvent(h->move_s[si], h->move_start, 0));
         used[si] = true;
       }
       const size_t len = static_cast<size_t>(std::min(kMovePiece, mv.bytes - off));
       KVT_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(mv.dst) + off, static_cast<const char*>(mv.src) + off, len,
-                                   kinds[mv.kind], ms->s[si]));
+                                   kinds[mv.kind], h->move_s[si]));
     }
   }
   for (int i = 0; i < 4; ++i)
     if (used[i]) {
-      KVT_CUDA_TRY(cudaEventRecord(ms->done[i], ms->s[i]));
-      KVT_CUDA_TRY(cudaStreamWaitEvent(h->stream, ms->done[i], 0));
+      KVT_CUDA_TRY(cudaEventRecord(h->move_done[i], h->move_s[i]));
+      KVT_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->move_done[i], 0));
     }
   return KVT_OK;
 }

@@ -39,6 +39,18 @@ def context_ids(n_local: int, world: int) -> list:
     return [f"r{r:03d}-{i:07d}" for r in range(world) for i in range(n_local)]
 
 
+def merge_rank_profiles(parts) -> ProfileArrays:
+    """The global ProfileArrays of per-rank profile sets (equal context count,
+    one shared ratio grid): what `gather_profiles` returns on every rank,
+    built here from the parts directly (fixtures, single-process checks)."""
+    world, n = len(parts), parts[0].n
+    G = len(parts[0].grid) // n
+    qual = np.concatenate([p.qual.reshape(n, p.M, G) for p in parts])
+    return ProfileArrays.uniform_grid(context_ids(n, world), np.concatenate([p.orig for p in parts]),
+                                      np.concatenate([p.freq for p in parts]), parts[0].grid[:G], qual,
+                                      np.concatenate([p.has for p in parts]))
+
+
 def gather_profiles(mine: ProfileArrays, group=None, device=None) -> ProfileArrays:
     """All-gather every rank's profile rows into the global ProfileArrays
     (uniform ratio grid, equal context count per rank). `device` is where

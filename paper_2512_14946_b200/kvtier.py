@@ -329,14 +329,18 @@ class StoreState:  # proj/include/kvtier/placement.hpp:29-70
         return acts
 
     def insert_joint(self, ps: PSet, space: CandidateSpace, params: UtilityParams, ctx,
-                     frequency=None, stamp=None, rule: int = A.KVT_RULE_UTILITY) -> np.ndarray:
+                     frequency=None, stamp=None, rule: int = A.KVT_RULE_UTILITY, cached: bool = False) -> np.ndarray:
+        """insert_joint of every context of `ctx`, in order. cached=True runs
+        the CPU cached-greedy baseline (ref_insert_joint_cached; reference
+        library only)."""
+        fn = self.abi.insert_joint_cached if cached else self.abi.insert_joint
         ctx = np.atleast_1d(np.asarray(ctx, np.int32))
         nops = len(ctx)
         freq = np.zeros(nops, np.int64) if frequency is None else np.atleast_1d(np.asarray(frequency, np.int64))
         stp = np.zeros(nops, np.int64) if stamp is None else np.atleast_1d(np.asarray(stamp, np.int64))
         n, done = C.c_int64(), C.c_int64()
-        rc = self.abi.insert_joint(self.s, ps.p, C.byref(space.c), C.byref(params.c), rule,
-                                   A.ptr(ctx), A.ptr(freq), A.ptr(stp), nops, C.byref(n), C.byref(done))
+        rc = fn(self.s, ps.p, C.byref(space.c), C.byref(params.c), rule,
+                A.ptr(ctx), A.ptr(freq), A.ptr(stp), nops, C.byref(n), C.byref(done))
         self.last_done = done.value
         acts = self._actions(n.value)
         self.abi.check(rc)

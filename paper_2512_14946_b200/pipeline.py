@@ -71,7 +71,9 @@ class Codec:
     def reserve(self, max_T: int, n_out: int = 2):
         """Workspace + output ring (per lane) for chunks up to max_T tokens."""
         s = A.KvShape(self.L, self.H, max_T, self.D)
-        cfg = A.CodecCfg(0, 16, max_T, 32, 4, 7, 0)
+        # the largest blob: bf16 rows, every token but one kept (keeping all
+        # T at 16 bits is the identity configuration, which has no blob)
+        cfg = A.CodecCfg(scorer=0, bits=16, keep=max(1, max_T - 1), window=32, q_heads=4, pool=7)
         wsb = self.eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg))
         m = A.BlobMap()
         self.eng.abi.check(self.eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
@@ -87,9 +89,14 @@ class Codec:
         li = slot % len(self.lanes) if lane is None else lane
         eng, outs = self.lanes[li], self._out[li]
         out = outs[(slot // len(self.lanes)) % len(outs)]
-        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(self._ws[li]),
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(self._ws[li]),
                                        A.ptr(out)))
-        return m.total_bytes
+        return self.retained_bytes(m, T)
+
+    def retained_bytes(self, m: A.BlobMap, T: int) -> int:
+        """Bytes the compressed chunk occupies: the blob, or for the identity
+        configuration the source K and V it aliases."""
+        return 4 * self.L * self.H * T * self.D if m.identity else int(m.total_bytes)
 
     def attach_streams(self, streams, ring: int = 4):
         """The lanes' torch streams (same order as the engines): enables
@@ -117,7 +124,7 @@ class Codec:
         se, pe = self.lanes[score_lane], self.lanes[pack_lane]
         ss, ps = self._streams[score_lane], self._streams[pack_lane]
         ss.wait_event(self._free[j])  # the ring slot's previous top-k has read it
-        se.abi.check(se.abi.token_scores(se.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(self._ring[j])))
+        se.abi.check(se.abi.token_scores(se.h, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(self._ring[j])))
         self._ready[j].record(ss)
         ps.wait_event(self._ready[j])
         idx = self._idx[pack_lane]
@@ -126,7 +133,7 @@ class Codec:
         outs = self._out[pack_lane]
         out = outs[(slot // len(self.lanes)) % len(outs)]
         pe.abi.check(pe.abi.pack(pe.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(out)))
-        return m.total_bytes
+        return self.retained_bytes(m, T)
 
     def launches(self) -> int:
         return sum(int(e.abi.launch_count(e.h)) for e in self.lanes)
@@ -154,7 +161,7 @@ def split_plan(methods: Sequence[str], ratios: Sequence[float], Ts: Sequence[int
         bits = int(q[1:]) if q else 16
         pack = T / 8192.0 * _PACK_US.get(bits, 230.0) * r
         score = T / 8192.0 * _SCORE_US.get(base, 0.0) if r < 1.0 else 0.0
-        li = min(range(1, n_lanes), key=load.__getitem__)
+        li = min(range(1, n_lanes), key=load.__getitem__) if n_lanes > 1 else 0
         if base == "snapkv" and r < 1.0:
             load[0] += score * 112.0 / snap_sms
             load[li] += pack

@@ -22,6 +22,7 @@ LLAMA70B = dict(L=80, H=8, D=128)  # 327,680 B/token
 QUANT_TOKEN_DROP_METHODS = ["keydiff", "knorm", "snapkv", "keydiff-q8", "knorm-q8", "snapkv-q8",
                             "keydiff-q4", "knorm-q4", "snapkv-q4"]
 MIXED_BITS_METHODS = ["keydiff-q8", "knorm-q4", "snapkv-q2", "knorm-q2", "keydiff-q4", "snapkv-q8"]
+C5_METHODS = ["keydiff", "knorm-q4", "snapkv-q8"]
 DEFAULT_GRID = [0.05, 0.1, 0.2, 0.4, 0.6, 0.8, 0.9, 1.0]
 
 
@@ -97,8 +98,9 @@ CONFIGS = {
     # configs[3]: Llama-3.1-70B-shaped KV, 10K contexts (sharded)
     "c4": dict(model="llama-3.1-70b", n_ctx=10000, tokens=8192, methods=["keydiff", "knorm", "snapkv"],
                gpu_frac=0.10, varied=False),
-    # configs[4]: 1M chunk-config candidates (13,889 x 72)
-    "c5": dict(model="llama-3.1-8b", n_ctx=13889, tokens=8192, methods=["keydiff", "knorm", "snapkv"],
+    # configs[4]: 1M chunk-config candidates (13,889 x 72); one token-drop, one
+    # q4 and one q8 method so the pass exercises quantise/pack as well
+    "c5": dict(model="llama-3.1-8b", n_ctx=13889, tokens=8192, methods=C5_METHODS,
                gpu_frac=0.10, varied=True),
 }
 

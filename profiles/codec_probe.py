@@ -72,13 +72,13 @@ def main():
         for r in range(args.reps + 1):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             ev[0].record()
-            ab.check(ab.token_scores(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(sc)))
+            ab.check(ab.token_scores(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(sc)))
             ev[1].record()
             ab.check(ab.topk(eng.h, C.byref(s), C.byref(cfg), A.ptr(sc), A.ptr(idx)))
             ev[2].record()
             ab.check(ab.pack(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(blob)))
             ev[3].record()
-            ab.check(ab.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+            ab.check(ab.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
             ev[4].record()
             torch.cuda.synchronize()
             if r == 0:

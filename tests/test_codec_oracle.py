@@ -102,7 +102,7 @@ def _kv(L, H, T, seed=3, ctx=1):
 
 def _scores(lib, s, cfg, k):
     out = np.zeros((s.L, s.H, s.T), np.float32)
-    lib.check(lib.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+    lib.check(lib.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(out)))
     return out
 
 
@@ -137,6 +137,48 @@ def test_snapkv_scores_match_numpy(lib):
     q = R.gen_q(1, 2, cfg.q_heads, cfg.window, 128, cfg.q_seed)
     want = R.snapkv_scores(k, q, cfg.window, cfg.q_heads, cfg.pool)
     assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
+
+
+def test_snapkv_caller_queries_match_numpy(lib):
+    """Caller-supplied observation-window queries, bf16
+    [L][H*G][W][128], replace the synthetic ones: oracle == numpy."""
+    s = shape(2, 2, 300)
+    k, _ = _kv(2, 2, 300)
+    cfg = plan(lib, "snapkv", 0.5, s)
+    rng = np.random.default_rng(4)
+    qf = rng.standard_normal((2, 2 * cfg.q_heads, cfg.window, 128)).astype(np.float32) * np.float32(9.0)
+    q = (qf.view(np.uint32) >> 16).astype(np.uint16)
+    out = np.zeros((2, 2, 300), np.float32)
+    lib.check(lib.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(q), A.ptr(out)))
+    want = R.snapkv_scores(k, q, cfg.window, cfg.q_heads, cfg.pool)
+    assert np.array_equal(out.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
+    assert not np.array_equal(out, _scores(lib, s, cfg, k))
+
+
+def test_knorm_keep_low_flag(lib):
+    s = shape(1, 2, 100)
+    k, _ = _kv(1, 2, 100)
+    cfg = plan(lib, "knorm", 0.5, s)
+    cfg.flags = A.KVT_CODEC_KNORM_KEEP_LOW
+    assert np.array_equal(_scores(lib, s, cfg, k), -R.knorm_scores(k))
+
+
+def test_identity_configuration_has_no_blob(lib):
+    """ratio 1.0 at 16 bits keeps every token verbatim: the compressed chunk
+    is the source KV (kvt_blob_map.identity), so compress writes nothing and
+    unpack refuses. A full keep at fewer bits still quantises."""
+    s = shape(1, 2, 64)
+    k, v = _kv(1, 2, 64)
+    cfg = plan(lib, "knorm", 1.0, s)
+    m = A.BlobMap()
+    lib.check(lib.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    assert cfg.keep == 64 and cfg.bits == 16 and m.identity == 1 and m.total_bytes == 0
+    lib.check(lib.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, None, None))
+    with pytest.raises(A.AbiError):
+        lib.check(lib.unpack(None, C.byref(s), C.byref(cfg), None, None, None))
+    q8 = plan(lib, "knorm-q8", 0.515625, s)  # eff(8) = 8/16 + 1/64: every token at 8 bits
+    lib.check(lib.blob_layout(C.byref(s), C.byref(q8), C.byref(m)))
+    assert q8.keep == 64 and q8.bits == 8 and m.identity == 0 and m.total_bytes > 0
 
 
 def test_topk_rule_ties_and_order(lib):
@@ -202,7 +244,7 @@ def test_pack_unpack_roundtrip(lib, method, ratio):
     lib.check(lib.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
     ws = np.zeros(lib.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
     blob = np.zeros(m.total_bytes, np.uint8)
-    lib.check(lib.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+    lib.check(lib.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
     idx = blob[m.idx_off:m.idx_off + m.idx_bytes].view(np.int32).reshape(2, 2, cfg.keep)
     assert (np.diff(idx, axis=-1) > 0).all() and idx.min() >= 0 and idx.max() < 300
     ko = np.zeros((2, 2, cfg.keep, 128), np.uint16)

@@ -69,11 +69,11 @@ def test_kv_generate_bitexact(gpu, orc, si):
 def scores(eng, s, cfg, k, on_gpu):
     if on_gpu:
         out = torch.empty(s.L * s.H * s.T, dtype=torch.float32, device="cuda")
-        eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+        eng.abi.check(eng.abi.token_scores(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(out)))
         eng.abi.check(eng.abi.sync(eng.h))
         return out.cpu().numpy()
     out = np.zeros(s.L * s.H * s.T, np.float32)
-    eng.abi.check(eng.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+    eng.abi.check(eng.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(out)))
     return out
 
 
@@ -137,6 +137,66 @@ def test_snapkv_scores_bitexact(gpu, orc, si):
     assert np.array_equal(sg.view(np.uint32), so.view(np.uint32))
 
 
+def window_queries(s, cfg, seed, spread=1.0):
+    """Caller-supplied observation-window queries, bf16 [L][H*G][W][128]:
+    random normal rows with a few large channels (real queries are peaky)."""
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((s.L, s.H * cfg.q_heads, cfg.window, 128)).astype(np.float32) * np.float32(spread)
+    q[..., 3] *= np.float32(8.0)
+    q[..., 77] *= np.float32(-5.0)
+    return (q.view(np.uint32) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("si", [0, 1, 4, 5, 7, 9])
+@pytest.mark.parametrize("spread", [1.0, 30.0])
+def test_snapkv_caller_queries_bitexact(gpu, orc, si, spread):
+    """snapkv over the caller's observation-window queries
+    instead of the synthetic ones: token_scores and compress equal the oracle."""
+    s = SNAP_SHAPES[si]
+    kg, vg = gen(gpu, s)
+    ko, vo = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, "snapkv-q4", 0.2, s)
+    q = window_queries(s, cfg, si, spread)
+    qg = dev(q.view(np.int16))
+    out = torch.empty(s.L * s.H * s.T, dtype=torch.float32, device="cuda")
+    gpu.abi.check(gpu.abi.token_scores(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), A.ptr(qg), A.ptr(out)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    want = np.zeros(s.L * s.H * s.T, np.float32)
+    orc.abi.check(orc.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(ko), A.ptr(q), A.ptr(want)))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    synth = scores(orc, s, cfg, ko, False)
+    if s.T > cfg.window + 1:
+        assert not np.array_equal(synth, want)  # the queries matter
+    # compress with the caller's queries: same blob as the oracle's
+    m = A.BlobMap()
+    orc.abi.check(orc.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    ws = torch.empty(gpu.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg)), dtype=torch.uint8, device="cuda")
+    bg = torch.zeros(m.total_bytes, dtype=torch.uint8, device="cuda")
+    gpu.abi.check(gpu.abi.compress(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), A.ptr(vg), A.ptr(qg), A.ptr(ws),
+                                   A.ptr(bg)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    wso = np.zeros(orc.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
+    bo = np.zeros(m.total_bytes, np.uint8)
+    orc.abi.check(orc.abi.compress(None, C.byref(s), C.byref(cfg), A.ptr(ko), A.ptr(vo), A.ptr(q), A.ptr(wso),
+                                   A.ptr(bo)))
+    assert np.array_equal(bg.cpu().numpy(), bo)
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+def test_knorm_keep_low_flag(gpu, orc, si):
+    """KVT_CODEC_KNORM_KEEP_LOW (the cited knorm paper keeps low-norm keys;
+    PAPER.md:637 drops them): scores are the negated norms, bit-exact."""
+    s = SHAPES[si]
+    kg, _ = gen(gpu, s)
+    ko, _ = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, "knorm", 0.3, s)
+    hi = scores(gpu, s, cfg, kg, True)
+    cfg.flags = A.KVT_CODEC_KNORM_KEEP_LOW
+    lo_g, lo_o = scores(gpu, s, cfg, kg, True), scores(orc, s, cfg, ko, False)
+    assert np.array_equal(lo_g.view(np.uint32), lo_o.view(np.uint32))
+    assert np.array_equal(lo_g, -hi)
+
+
 @pytest.mark.parametrize("sms", ["1", "16", "64", "100"])
 def test_snapkv_sm_budget_same_scores(gpu, sms, monkeypatch):
     """KVT_SNAP_SMS (the bench's SM budget for snapkv's persistent clusters)
@@ -155,7 +215,7 @@ def test_snapkv_rejects_too_long_prefix(gpu):
     k = torch.zeros(s.L * s.H * s.T * s.D, dtype=torch.int16, device="cuda")
     out = torch.empty(s.L * s.H * s.T, dtype=torch.float32, device="cuda")
     with pytest.raises(A.AbiError):
-        gpu.abi.check(gpu.abi.token_scores(gpu.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(out)))
+        gpu.abi.check(gpu.abi.token_scores(gpu.h, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(out)))
 
 
 @pytest.mark.parametrize("keep_ratio", [0.001, 0.2, 0.5, 1.0])
@@ -205,12 +265,12 @@ def compress(eng, s, cfg, k, v, on_gpu):
     if on_gpu:
         ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
         blob = torch.zeros(m.total_bytes, dtype=torch.uint8, device="cuda")
-        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
         eng.abi.check(eng.abi.sync(eng.h))
     else:
         ws = np.zeros(wsb, np.uint8)
         blob = np.zeros(m.total_bytes, np.uint8)
-        eng.abi.check(eng.abi.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(blob)))
+        eng.abi.check(eng.abi.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
     return blob, m
 
 
@@ -225,25 +285,30 @@ def blob_sections(b, m, bits):
     return out
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "unfused"])
 @pytest.mark.parametrize("si", range(len(PACK_SHAPES)))
 @pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.3), ("keydiff-q4", 0.2), ("knorm-q2", 0.1),
                                           ("keydiff", 0.4), ("knorm-q4", 0.02), ("knorm-q8", 0.5),
                                           ("keydiff-q8", 1.0), ("knorm", 1.0), ("snapkv", 1.0),
                                           ("snapkv-q4", 0.2), ("snapkv-q8", 0.4)])
-def test_compress_unpack_bitexact(gpu, orc, si, method, ratio, fused, monkeypatch):
-    """compress = scores + top-k + pack; `fused` is the one-launch cluster
-    kernel (knorm/keydiff), `unfused` the three-phase kernels."""
-    if fused:
-        monkeypatch.setenv("KVT_FUSED", "1")
-    else:
-        monkeypatch.delenv("KVT_FUSED", raising=False)
+def test_compress_unpack_bitexact(gpu, orc, si, method, ratio):
+    """compress = scores + top-k + pack, then unpack: blobs and dequantised
+    KV equal the oracle's. Identity configurations (every token at 16 bits)
+    have no blob: nothing is launched and unpack refuses (the source is the
+    decompressed KV)."""
     s = PACK_SHAPES[si]
     kg, vg = gen(gpu, s)
     ko, vo = gen(orc, s, on_gpu=False)
     cfg = plan(orc.abi, method, ratio, s)
+    l0 = gpu.abi.launch_count(gpu.h)
     bg, m = compress(gpu, s, cfg, kg, vg, True)
     bo, _ = compress(orc, s, cfg, ko, vo, False)
+    if m.identity:
+        assert cfg.keep == s.T and cfg.bits == 16 and m.total_bytes == 0
+        assert gpu.abi.launch_count(gpu.h) == l0
+        for e, b in ((gpu, bg), (orc, bo)):
+            with pytest.raises(A.AbiError):
+                e.abi.check(e.abi.unpack(e.h if e is gpu else None, C.byref(s), C.byref(cfg), A.ptr(b), None, None))
+        return
     sg, so = blob_sections(bg, m, cfg.bits), blob_sections(bo, m, cfg.bits)
     for name in so:
         assert np.array_equal(sg[name], so[name]), name

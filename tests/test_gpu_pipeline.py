@@ -42,7 +42,7 @@ def test_compress_split_matches_compress(gpu_abi):
         cfg, m, wsb = codec.plan(method, ratio, T)
         ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
         blob = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
-        ref_eng.abi.check(ref_eng.abi.compress(ref_eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws),
+        ref_eng.abi.check(ref_eng.abi.compress(ref_eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws),
                                                A.ptr(blob)))
         ref_eng.abi.check(ref_eng.abi.sync(ref_eng.h))
         want.append(blob.cpu())

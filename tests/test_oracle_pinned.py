@@ -193,3 +193,30 @@ def test_oracle_matches_reference_random(oracle_abi, ref_abi, seed):
         ro = run_inserts(eo, arrays, tiers, space, params, order, rule, then_rearrange=True)
         rr = run_inserts(er, arrays, tiers, space, params, order, rule, then_rearrange=True)
         compare_runs(ro, rr, f"seed{seed}/rule{rule}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_cached_greedy_baseline_equals_reference(ref_abi, seed):
+    """ref_insert_joint_cached (the single-core CPU baseline of the cached
+    per-resident best update, on the reference's own scoring
+    functions) reproduces the reference's insert_joint exactly: actions,
+    store, placement utility, errors."""
+    from cases import random_instance
+    from parity import compare_runs
+    eng = Engine(ref_abi)
+    arrays, tiers, space, params = random_instance(seed + 900, n_ctx=[40, 80, 150, 300, 30, 60][seed],
+                                                   n_methods=1 + seed % 3, n_tiers=2 + seed % 2)
+    order = np.random.default_rng(seed).permutation(arrays.n)
+    runs = []
+    for cached in (False, True):
+        ps = eng.pset(arrays)
+        st = eng.store(tiers, arrays.n, space)
+        err = None
+        try:
+            acts = st.insert_joint(ps, space, params, order, cached=cached)
+        except A.ValidationError as e:
+            acts, err = None, str(e)
+        runs.append(dict(actions=acts, occupancy=st.occupancy(), residents=st.residents(), snapshot=st.snapshot(),
+                         utility=None if err else st.placement_utility(ps, space, params), error=err))
+    compare_runs(runs[1], runs[0], f"seed{seed}")
+    assert runs[1]["error"] == runs[0]["error"]

@@ -43,7 +43,7 @@ def test_gpu_blob_round_trip_through_host_tier(gpu_abi):
         eng.abi.check(eng.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
         ws = torch.empty(eng.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg)), dtype=torch.uint8, device="cuda")
         b = torch.zeros(m.total_bytes, dtype=torch.uint8, device="cuda")
-        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(ws), A.ptr(b)))
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(b)))
         blobs.append((b, ws))
     arena = HostArena(eng.abi, sum(b.numel() for b, _ in blobs) + 4096)
     ex = TierExecutor(eng, arena)
