@@ -10,10 +10,18 @@ KV bytes of the batch / device time of the step, summed over ranks.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
   python bench.py --impl reference   # CPU reference arm (oracle/_ref + codec port)
 
-N > 1 (torchrun): each rank owns n_ctx contexts (weak scaling). The
-placement is global: profiles are all-gathered over NCCL and every rank runs
-the identical deterministic greedy over all contexts, then compresses only
-its own contexts.
+N > 1: one process per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run). Each rank owns n_ctx contexts (weak
+scaling). The placement is global: every step, each rank's profile record is
+all-gathered over NCCL (inside the timed region) and merged into the global
+profile set on the device (kvt_pset_merge); every rank runs the identical
+deterministic greedy over all contexts, then compresses only its own.
+
+Lines: `value` (inputs resident in HBM), `e2e` (profile rows H2D from pinned
+host memory + action list and placement D2H every step, through the C ABI),
+`e2e_tiered` (e2e plus the tier moves the placement implies: every context
+placed below the GPU tier leaves HBM over PCIe), `roofline`, `tier_move`
+(PCIe and SSD rates, verified), `cpu_baseline`.
 """
 from __future__ import annotations
 
@@ -140,11 +148,15 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
     # a host stall between an event and its launch must not count as kernel time
     with torch.cuda.stream(stream):
         torch.cuda._sleep(100_000_000)
+    n_identity = 0
     for c in range(lo, hi):
         if snap["tier_index"][c] < 0:
             continue
         T = int(arrays.orig[c] // bpt)
         cfgc, m, wsb = codec.plan(names[snap["method"][c]], float(snap["ratio"][c]), T)
+        if m.identity:  # the compressed chunk is the source KV: no kernel, no bytes
+            n_identity += 1
+            continue
         s = A.KvShape(L, H, T, D)
         k, v = pool.chunk(c)
         sc = codec.ws  # scores at offset 0
@@ -169,6 +181,7 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
     torch.cuda.synchronize()
     per = {}
     phase = {"scores": 0.0, "topk": 0.0, "pack": 0.0}
+    step_bytes = sum(ab for evs, keys, abs_ in recs for key, ab in zip(keys, abs_) if key is not None)
     for evs, keys, abs_ in recs:
         for i, (key, ph) in enumerate(zip(keys, ("scores", "topk", "pack"))):
             if key is None:
@@ -196,12 +209,62 @@ def kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
                         for k_, v in sorted(per.items(), key=lambda kv: -kv[1][0])}}
     if dom in ISSUE_BOUND:  # HBM fraction is reported, but it is not what bounds this kernel
         line["bound_note"] = ISSUE_BOUND[dom]
+    line["identity_contexts"] = n_identity
+    line["alg_bytes_per_step_rank"] = int(step_bytes)
+    line["unpack"] = unpack_rate(eng, stream, codec, pool, snap, arrays, names, L, H, D, bpt, lo, hi)
     ge = os.environ.get("KVT_SNAP_SMS")
     if dom == "k_snapkv_tc" and ge:  # runs on a share of the SMs by design (the step's other streams get the rest)
         sms = min(int(ge), torch.cuda.get_device_properties(0).multi_processor_count)
         line["sms"] = sms
         line["frac_per_sm"] = round(line["frac"] * torch.cuda.get_device_properties(0).multi_processor_count / sms, 4)
     return line
+
+
+def unpack_rate(eng, stream, codec, pool, snap, arrays, names, L, H, D, bpt, lo, hi, per_bits=3):
+    """k_unpack (unpack + dequantise, the decompression half of north-star
+    item 1): a few placed quantised contexts per bit width, compressed then
+    unpacked into bf16 [L][H][keep][D], CUDA events on the launching stream.
+    Algorithmic bytes per launch = blob + 2 x 2 B x L H keep D."""
+    import torch
+
+    from paper_2512_14946_b200 import _abi as A
+    pk, _ = peaks()
+    seen, out = {}, {}
+    for c in range(lo, hi):
+        if snap["tier_index"][c] < 0:
+            continue
+        T = int(arrays.orig[c] // bpt)
+        meth, ratio = names[snap["method"][c]], float(snap["ratio"][c])
+        cfgc, m, _ = codec.plan(meth, ratio, T)
+        if m.identity or cfgc.bits == 16 or seen.get(cfgc.bits, 0) >= per_bits:
+            continue
+        seen[cfgc.bits] = seen.get(cfgc.bits, 0) + 1
+        k, v = pool.chunk(c)
+        s_ = A.KvShape(L, H, T, D)
+        blob = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s_), C.byref(cfgc), A.ptr(k), A.ptr(v), None,
+                                       A.ptr(codec.ws), A.ptr(blob)))
+        n = L * H * cfgc.keep * D
+        ko = torch.empty(n, dtype=torch.int16, device="cuda")
+        vo = torch.empty_like(ko)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.abi.check(eng.abi.unpack(eng.h, C.byref(s_), C.byref(cfgc), A.ptr(blob), A.ptr(ko), A.ptr(vo)))  # warm
+        e0.record(stream)
+        eng.abi.check(eng.abi.unpack(eng.h, C.byref(s_), C.byref(cfgc), A.ptr(blob), A.ptr(ko), A.ptr(vo)))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        alg = m.total_bytes + 2 * 2 * n
+        r = out.setdefault(f"q{cfgc.bits}", {"ms": 0.0, "bytes": 0, "n": 0})
+        r["ms"] += ms
+        r["bytes"] += alg
+        r["n"] += 1
+    for r in out.values():
+        gbs = r["bytes"] / (r["ms"] / 1e3) / 1e9
+        r.update(GBps=round(gbs, 1), frac=round(gbs / pk["hbm_gbs"], 4), avg_launch_ms=round(r["ms"] / r["n"], 4),
+                 ms=round(r["ms"], 3))
+    return {"kernel": "k_unpack", "by_bits": out,
+            "note": "alg bytes = blob + 4 B x L H keep D (bf16 K and V out); placed contexts of this batch"}
 
 
 # kernels whose limit is instruction issue, not HBM (ncu captures in profiles/)
@@ -213,42 +276,60 @@ ISSUE_BOUND = {
 }
 
 
-def tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, lo, hi, n_ctx=4, reps=3):
-    """SURVEY §8 f1 evidence: pinned cudaMemcpyAsync GB/s of the tier-move
-    executor (kvt_tier_moves) moving the compressed blobs of contexts the
-    greedy placed below the GPU tier to the pinned CPU-tier arena (D2H) and
-    back (H2D), CUDA events on the handle stream. PCIe-bound; reported beside
-    the HBM-bound codec, not folded into `value`."""
+def tier_move_rates(eng, stream, codec, pool, snap, arrays, space, L, H, D, bpt, lo, hi, n_ctx=4, reps=3,
+                    ssd_bytes=4 << 30):
+    """SURVEY §8 f1 evidence. PCIe: pinned cudaMemcpyAsync GB/s of
+    kvt_tier_moves moving the compressed bytes of contexts the greedy placed
+    below the GPU tier to the pinned CPU-tier arena (D2H) and back into fresh
+    device buffers (H2D), CUDA events on the handle stream; both directions
+    are verified byte for byte before timing. SSD: up to `ssd_bytes` of
+    SSD-tier contexts staged through pinned DRAM and written to a file with
+    kvt_tier_file_write (O_DIRECT, threads), read back and verified."""
+    import tempfile
+
     import torch
 
     from paper_2512_14946_b200 import _abi as A
-    from paper_2512_14946_b200.tiers import HostArena, TierExecutor, host_moves_bytes
+    from paper_2512_14946_b200.tiers import HostArena, SsdTier, TierExecutor, context_sources, host_moves_bytes
 
-    snap = store.snapshot()
     names = space.method_names
-    blobs, placed = [], []
-    for c in range(lo, hi):
-        if snap["tier_index"][c] <= 0 or len(blobs) >= n_ctx:
-            continue
+
+    def compressed(c):
         T = int(arrays.orig[c] // bpt)
         cfgc, m, _ = codec.plan(names[snap["method"][c]], float(snap["ratio"][c]), T)
-        s = A.KvShape(L, H, T, D)
+        s_ = A.KvShape(L, H, T, D)
         k, v = pool.chunk(c)
-        b = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
-        eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfgc), A.ptr(k), A.ptr(v), None, A.ptr(codec.ws),
-                                       A.ptr(b)))
-        blobs.append(b)
-        placed.append((c, int(snap["tier_index"][c]), b.data_ptr(), b.numel()))
-    if not blobs:
+        b = torch.empty(max(1, m.total_bytes), dtype=torch.uint8, device="cuda")
+        eng.abi.check(eng.abi.compress(eng.h, C.byref(s_), C.byref(cfgc), A.ptr(k), A.ptr(v), None,
+                                       A.ptr(codec.ws), A.ptr(b)))
+        return [(p_, n_) for p_, n_ in context_sources(b.data_ptr(), m, k.data_ptr(), v.data_ptr(), k.numel() * 2)], b
+
+    # ---- PCIe leg: CPU-tier (and SSD-tier) contexts, device <-> pinned host
+    srcs, keep = [], []
+    for c in range(lo, hi):
+        if snap["tier_index"][c] > 0 and len(keep) < n_ctx:
+            r_, b = compressed(c)
+            srcs += r_
+            keep.append(b)
+    if not srcs:
         return None
-    arena = HostArena(eng.abi, sum(b.numel() for b in blobs) + (1 << 20))
+    total = sum(n_ for _, n_ in srcs)
+    arena = HostArena(eng.abi, total + (1 << 20))
     ex = TierExecutor(eng, arena)
-    down = ex.moves_for(placed)
-    up = ex.reverse(down)
-    nbytes = host_moves_bytes(down)
+    down = ex.moves_for([(i, 1, p_, n_) for i, (p_, n_) in enumerate(srcs)])
+    fresh = [torch.empty(n_, dtype=torch.uint8, device="cuda") for _, n_ in srcs]
+    up = [A.Move(mv.dst, t.data_ptr(), mv.bytes, A.KVT_MOVE_H2D, 0) for mv, t in zip(down, fresh)]
+    ex.run(down)
+    eng.abi.check(eng.abi.sync(eng.h))
+    ok = True
+    for (p_, n_), mv in zip(srcs, down):  # host copy == device bytes, right after the D2H
+        ok &= bool(np.array_equal(arena.view(mv.dst, mv.bytes), _device_bytes(p_, n_)))
+    ex.run(up)
+    eng.abi.check(eng.abi.sync(eng.h))
+    for (p_, n_), t in zip(srcs, fresh):  # H2D into fresh buffers == the original device bytes
+        ok &= bool(np.array_equal(t.cpu().numpy(), _device_bytes(p_, n_)))
     rates = {}
     for name, mv in (("d2h", down), ("h2d", up)):
-        ex.run(mv)  # warm-up
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(stream)
@@ -256,16 +337,113 @@ def tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt
             ex.run(mv)
         e1.record(stream)
         torch.cuda.synchronize()
-        rates[name] = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
-    ok = True  # the host copies equal the device blobs (after the last D2H + H2D round trip)
-    for b, mv in zip(blobs, down):
-        host = np.ctypeslib.as_array((C.c_uint8 * mv.bytes).from_address(mv.dst))
-        ok &= bool(np.array_equal(host, b.cpu().numpy()))
+        rates[name] = host_moves_bytes(mv) * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    out = {"d2h_gbs": round(rates["d2h"], 1), "h2d_gbs": round(rates["h2d"], 1), "bytes": int(total),
+           "contexts": len(keep), "verified": bool(ok),
+           "note": "kvt_tier_moves: compressed bytes of below-GPU-tier contexts (source K/V for identity "
+                   "configurations), device -> pinned host, then host -> fresh device buffers; 8 MiB pieces "
+                   "over 2 copy streams per direction; each direction verified byte for byte before timing"}
     arena.close()
-    return {"d2h_gbs": round(rates["d2h"], 1), "h2d_gbs": round(rates["h2d"], 1), "bytes": nbytes,
-            "contexts": len(blobs), "verified": bool(ok),
-            "note": "kvt_tier_moves: compressed blobs of CPU/SSD-tier contexts, device <-> pinned host, "
-                    "8 MiB pieces over 2 copy streams per direction"}
+
+    # ---- SSD leg: SSD-tier contexts, staged through pinned DRAM, into a file
+    ssd_src = []
+    for c in range(lo, hi):
+        if snap["tier_index"][c] == 2 and sum(n_ for _, n_ in ssd_src) < ssd_bytes:
+            r_, b = compressed(c)
+            ssd_src += r_
+            keep.append(b)
+    if ssd_src:
+        nb = sum(n_ for _, n_ in ssd_src)
+        d = os.environ.get("KVT_SSD_DIR") or tempfile.gettempdir()
+        st_ = os.statvfs(d)
+        if st_.f_bavail * st_.f_frsize < 2 * nb + (1 << 30):
+            out["ssd"] = {"skipped": f"not enough free space in {d}"}
+            return out
+        stage = HostArena(eng.abi, nb + 64 * 4096)
+        back = HostArena(eng.abi, nb + 64 * 4096)
+        ex2 = TierExecutor(eng, stage)
+        mv = ex2.moves_for([(i, 2, p_, n_) for i, (p_, n_) in enumerate(ssd_src)])
+        ex2.run(mv)
+        eng.abi.check(eng.abi.sync(eng.h))
+        ssd = SsdTier(eng.abi, os.path.join(d, f"kvt_ssd_tier_{os.getpid()}.bin"), nb + 64 * 4096, threads=8)
+        offs = [ssd.alloc(m_.bytes) for m_ in mv]
+        t0 = time.perf_counter()
+        ssd.write([(m_.dst, m_.bytes, o) for m_, o in zip(mv, offs)])
+        t_w = time.perf_counter() - t0
+        dst = [back.slot(i, m_.bytes) for i, m_ in enumerate(mv)]
+        t0 = time.perf_counter()
+        ssd.read([(a, m_.bytes, o) for a, m_, o in zip(dst, mv, offs)])
+        t_r = time.perf_counter() - t0
+        ok2 = all(np.array_equal(back.view(a, m_.bytes), _device_bytes(p_, n_))
+                  for a, m_, (p_, n_) in zip(dst, mv, ssd_src))
+        out["ssd"] = {"write_gbs": round(nb / t_w / 1e9, 2), "read_gbs": round(nb / t_r / 1e9, 2), "bytes": int(nb),
+                      "o_direct": ssd.direct, "dir": d, "verified": bool(ok2), "threads": 8,
+                      "note": "SSD-tier contexts: HBM -> pinned DRAM (kvt_tier_moves) -> file (kvt_tier_file_write, "
+                              "fdatasync), read back (kvt_tier_file_read) and compared with the device bytes; "
+                              "the read may be served from the page cache when O_DIRECT is unavailable"}
+        ssd.close()
+        stage.close()
+        back.close()
+    return out
+
+
+def _device_bytes(ptr, n):
+    """Copy n device bytes at `ptr` to a host numpy array (cudaMemcpy via torch)."""
+    return _alias(ptr, n).cpu().numpy()
+
+
+def _alias(ptr, n):
+    """A torch uint8 CUDA tensor viewing n bytes at device address `ptr`."""
+    import torch
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_Cai(), device="cuda")
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def config_dict(args, W, n_total, world):
+    """The workload description, identical in both arms (same_config)."""
+    cfg, space = W["cfg"], W["space"]
+    return {"workload": f"{args.config}: {cfg['model']} KV, {W['arrays'].n} contexts/GPU x {cfg['tokens']} tokens, "
+                        f"{len(space.methods)} methods x {len(space.ratios)} ratios x 3 tiers",
+            "contexts_total": int(n_total), "contexts_per_gpu": int(W["arrays"].n), "methods": space.method_names,
+            "tiers": "gpu {:.0%} of bytes @8e12 B/s, cpu 30% @5e10, ssd unlimited @6e9 + 1e-4 s".format(
+                cfg["gpu_frac"]),
+            "seed": "7 + rank", "n_gpus": world}
+
+
+def nccl_summary(path_glob):
+    """What NCCL_DEBUG=INFO logged on this rank: communicator size, NVLS."""
+    import glob
+    out = {"ranks": None, "nvls": False, "lines": 0}
+    for fn in glob.glob(path_glob):
+        try:
+            txt = open(fn, errors="replace").read()
+        except OSError:
+            continue
+        out["lines"] += txt.count("\n")
+        for ln in txt.splitlines():
+            if "Init COMPLETE" in ln and "nranks" in ln:
+                try:
+                    out["ranks"] = int(ln.split("nranks")[1].split()[0])
+                except Exception:
+                    pass
+            if "NVLS" in ln and ("enabled" in ln.lower() or "nvls multicast support is available" in ln.lower()):
+                out["nvls"] = True
+    return out
 
 
 def run_b200(args):
@@ -275,14 +453,27 @@ def run_b200(args):
     import paper_2512_14946_b200 as pkg
     from paper_2512_14946_b200 import _abi as A
     from paper_2512_14946_b200 import distributed, workload
-    from paper_2512_14946_b200.kvtier import Engine, ProfileArrays
-    from paper_2512_14946_b200.pipeline import Codec, KVPool, compress_placed, place, split_plan
+    from paper_2512_14946_b200.kvtier import Engine
+    from paper_2512_14946_b200.pipeline import Codec, KVPool, place, split_plan
+    from paper_2512_14946_b200.tiers import StagingRing, context_sources
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}; measuring {world} ranks", file=sys.stderr)
+    if args.ranks_share_gpu:  # test mode: every rank on cuda:0, the exchange over gloo on host buffers
+        local = 0
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench: rank {rank} needs cuda:{local}, {torch.cuda.device_count()} device(s) visible")
     torch.cuda.set_device(local)
-    if world > 1:
+    nccl_log = None
+    if world > 1 and args.ranks_share_gpu:
+        dist.init_process_group("gloo")
+    elif world > 1:
+        nccl_log = f"/tmp/kvt_bench_nccl.{os.getpid()}.log"
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)  # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     W = workload.build(args.config, n_ctx=args.n_ctx, seed=7 + rank)
@@ -291,29 +482,37 @@ def run_b200(args):
     bpt = W["bytes_per_token"]
     n_local = mine.n
 
-    # global profile set: all-gather every rank's profile rows (NCCL), then
-    # the replicated deterministic greedy over all contexts (distributed.py)
-    arrays = distributed.gather_profiles(mine, device=f"cuda:{local}") if world > 1 else mine
-    tiers = workload.three_tiers(int(arrays.orig.sum()), cfg["gpu_frac"], 0.30)
-    my_lo, my_hi = distributed.shard(arrays.n, world, rank)
-
     stream = torch.cuda.Stream()
     eng = Engine(pkg.product(), device=local, stream=stream.cuda_stream)
-    max_T = int(arrays.orig.max() // bpt)
+    # this rank's profile record: pinned on the host (the e2e leg copies it in
+    # every step) and resident on the device (the value leg); all-gathered over
+    # NCCL and merged on the device into the global profile set
+    with torch.cuda.stream(stream):
+        rp = (distributed.RankPlacement(eng, mine, device="cpu", merge_on=f"cuda:{local}") if args.ranks_share_gpu
+              else distributed.RankPlacement(eng, mine, device=f"cuda:{local}", pin=True))
+    tot = torch.tensor([int(mine.orig.sum())], dtype=torch.int64, device="cpu" if args.ranks_share_gpu else "cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    total_bytes = int(tot.item())  # every rank's contexts
+    tiers = workload.three_tiers(total_bytes, cfg["gpu_frac"], 0.30)
+    n_total = world * n_local
+    my_lo, my_hi = distributed.shard(n_total, world, rank)
+    assert my_hi - my_lo == n_local
+
+    max_T = int(mine.orig.max() // bpt)
     pool = KVPool(eng, L, H, max_T, D, n_chunks=args.pool)
-    # codec lanes: contexts round-robin over `--streams` CUDA streams (one kvt handle each)
     lane_streams = [torch.cuda.Stream() for _ in range(args.streams)]
     lanes = [Engine(pkg.product(), device=local, stream=ls.cuda_stream) for ls in lane_streams]
     codec = Codec(lanes, L, H, D)
     codec.reserve(max_T, n_out=2)
     codec.attach_streams(lane_streams, ring=args.ring)
-    ps = eng.pset(arrays)
-    store = eng.store(tiers, arrays.n, space)
-    order = np.arange(arrays.n, dtype=np.int32)
-
-    class Mine:  # the contexts this rank compresses
-        n = n_local
-        orig = arrays.orig[my_lo:my_hi]
+    with torch.cuda.stream(stream):
+        ps_static = rp.exchange()  # the global set once (value leg at N = 1 reuses it)
+    store = eng.store(tiers, n_total, space)
+    order = np.arange(n_total, dtype=np.int32)
+    names = space.method_names
+    kv_bytes = L * H * max_T * D * 2
+    staging = None  # pinned landing slots of the tiered leg
 
     def fork():  # codec lanes start after everything queued on the main stream
         for ls in lane_streams:
@@ -323,45 +522,55 @@ def run_b200(args):
         for ls in lane_streams:
             stream.wait_stream(ls)
 
-    names = space.method_names
-
-    def placed(pset):  # placement of one batch; the host waits for the main stream only
-        acts = place(store, pset, space, params, order)
+    def placed(upload, exchange):
+        """One batch's placement on the main stream: [H2D of this rank's
+        record] -> [NCCL all-gather + device merge] -> greedy -> action list
+        and placement D2H (the host needs them to launch its compressions)."""
+        with torch.cuda.stream(stream):
+            if upload:
+                rp.upload()
+            ps = rp.exchange() if exchange else ps_static
+        acts = place(store, ps, space, params, order)
         return acts, store.snapshot()
 
-    def launch_compress(snap_full):  # every placed context of this rank, async on the codec lanes
-        in_b = out_b = 0
-        fork()  # the lanes start after this batch's placement
+    def launch_compress(snap_full, tiered):
+        in_b = out_b = moved = 0
+        fork()
         cs = [c for c in range(my_lo, my_hi) if snap_full["tier_index"][c] >= 0]
         ms = [names[snap_full["method"][c]] for c in cs]
         rs = [float(snap_full["ratio"][c]) for c in cs]
-        Ts = [int(arrays.orig[c] // bpt) for c in cs]
-        if args.lanes == "split":
-            for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, split_plan(ms, rs, Ts, len(lanes), args.snap_sms)):
-                k, v = pool.chunk(c)
+        Ts = [int(mine.orig[c - my_lo] // bpt) for c in cs]
+        plan = (split_plan(ms, rs, Ts, len(lanes), args.snap_sms) if args.lanes == "split"
+                else [(None, None)] * len(cs))
+        for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, plan):
+            k, v = pool.chunk(c)
+            if args.lanes == "split":
                 out_b += (codec.compress(m, r, k, v, T, c, pl) if sl is None
                           else codec.compress_split(m, r, k, v, T, c, sl, pl))
-                in_b += int(arrays.orig[c])
-            return in_b, out_b
-        for c, m, r, T in zip(cs, ms, rs, Ts):  # round-robin, one kvt_compress per context
-            k, v = pool.chunk(c)
-            out_b += codec.compress(m, r, k, v, T, c)
-            in_b += int(arrays.orig[c])
-        return in_b, out_b
+            else:
+                out_b += codec.compress(m, r, k, v, T, c)
+            in_b += int(mine.orig[c - my_lo])
+            if tiered and snap_full["tier_index"][c] > 0:  # leaves HBM: D2H on the lane that produced it
+                li, blob, bm = codec.last
+                srcs = context_sources(blob, bm, k.data_ptr(), v.data_ptr(), L * H * T * D * 2)
+                mv = [A.Move(p_, staging.next(n_), n_, A.KVT_MOVE_D2H, 0) for p_, n_ in srcs]
+                arr = (A.Move * len(mv))(*mv)
+                lanes[li].abi.check(lanes[li].abi.tier_moves(lanes[li].h, arr, len(mv)))
+                moved += sum(n_ for _, n_ in srcs)
+        return in_b, out_b, moved
 
-    def run_steps(n, pset_of=lambda: ps):
-        """n steps, software-pipelined across batches: batch i + 1's placement
-        (one warp on the main stream + host reads of its result) runs while
+    def run_steps(n, upload, exchange, tiered=False):
+        """n steps, software-pipelined: batch i + 1's placement runs while
         batch i compresses on the codec lanes; every step's placement and
         compression happen inside the call."""
-        acts, snap_full = placed(pset_of())
-        n_act, in_b, out_b = len(acts), 0, 0
+        acts, snap_full = placed(upload, exchange)
+        n_act, in_b, out_b, moved = len(acts), 0, 0, 0
         for i in range(n):
-            in_b, out_b = launch_compress(snap_full)
+            in_b, out_b, moved = launch_compress(snap_full, tiered)
             if i + 1 < n:
-                acts, snap_full = placed(pset_of())
+                acts, snap_full = placed(upload, exchange)
         join()
-        return n_act, in_b, out_b, acts, snap_full
+        return n_act, in_b, out_b, moved, acts, snap_full
 
     def barrier():
         torch.cuda.synchronize()
@@ -369,165 +578,311 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    run_steps(args.warmup)
+    def timed(fn):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        res = fn()
+        e1.record(stream)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:  # the job takes as long as its slowest rank
+            t = torch.tensor([ms], device="cpu" if args.ranks_share_gpu else "cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, res
+
+    exchange_value = world > 1  # N > 1: the all-gather + merge is part of every step
+    run_steps(args.warmup, False, exchange_value)
     barrier()
     l0 = eng.abi.launch_count(eng.h) + codec.launches()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        barrier()
-        t0.record(stream)
-        n_act, in_b, out_b, _, _ = run_steps(args.steps)
-        t1.record(stream)
-        barrier()
+        ms, (n_act, in_b, out_b, _, _, _) = timed(lambda: run_steps(args.steps, False, exchange_value))
     launches = eng.abi.launch_count(eng.h) + codec.launches() - l0
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
-    total_bytes = int(arrays.orig.sum())  # all ranks' contexts
     value = total_bytes / (ms_step / 1e3) / 1e9
 
     # ---- e2e: through the C ABI with host buffers, copies inside the timed region
-    h2d = d2h = 0
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    psets = []  # each step's profile set: host rows copied H2D inside the timed region
-
-    def fresh_pset():
-        psets.append(eng.pset(arrays))
-        return psets[-1]
-
-    _, _, _, acts, snap_full = run_steps(args.steps, fresh_pset)  # actions + placement D2H every step
-    e1.record(stream)
-    h2d = (arrays.orig.nbytes + arrays.freq.nbytes + arrays.goff.nbytes + arrays.grid.nbytes +
-           arrays.qual.nbytes + arrays.has.nbytes + order.nbytes * 3)
+    e2e_ms, (_, _, _, _, acts, snap_full) = timed(lambda: run_steps(args.steps, True, True))
+    h2d = rp.h2d_bytes
     d2h = acts.nbytes + snap_full.nbytes
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
     e2e_value = total_bytes / (e2e_ms / args.steps / 1e3) / 1e9
 
-    # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
-    roof = None
-    tier_move = None
-    if rank == 0:
-        roof = kernel_roofline(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, my_lo, my_hi)
-        tier_move = tier_move_rates(eng, stream, codec, pool, store, arrays, space, L, H, D, bpt, my_lo, my_hi)
+    # ---- e2e_tiered: e2e + every below-GPU-tier context's bytes leave HBM over PCIe
+    tiered_steps = max(1, min(args.steps, args.tiered_steps))
+    staging = StagingRing(eng.abi, max(kv_bytes, int(codec._out[0][0].numel())), slots=2)
+    t_ms, (_, _, _, moved, _, snap_t) = timed(lambda: run_steps(tiered_steps, True, True, tiered=True))
+    staging.close()
+    mv_t = torch.tensor([moved], dtype=torch.int64, device="cpu" if args.ranks_share_gpu else "cuda")
+    if world > 1:
+        dist.all_reduce(mv_t)
+    tiered = {"value": round(total_bytes / (t_ms / tiered_steps / 1e3) / 1e9, 2), "unit": "GB/s",
+              "steps": tiered_steps, "ms_per_step": round(t_ms / tiered_steps, 1),
+              "d2h_tier_bytes_per_step": int(mv_t.item()), "h2d_bytes_per_step": int(h2d),
+              "d2h_bytes_per_step": int(d2h) + int(mv_t.item()),
+              "note": "e2e plus the PCIe leg of the placement: every context placed in the CPU or SSD tier "
+                      "(snapshot tier > 0) is copied HBM -> pinned DRAM by kvt_tier_moves on the stream that "
+                      "compressed it; the SSD file write is measured separately (tier_move.ssd)"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
+    # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
+    roof = tier_move = cpu = None
+    if rank == 0:
+        snap_now = store.snapshot()
+        roof = kernel_roofline(eng, stream, codec, pool, store, _Shard(mine, my_lo), space, L, H, D, bpt, my_lo,
+                               my_hi)
+        pk, _ = peaks()
+        roof["step_hbm_frac"] = round(roof["alg_bytes_per_step_rank"] / (ms_step / 1e3) / 1e9 / pk["hbm_gbs"], 4)
+        roof["step_note"] = ("step_hbm_frac = this rank's algorithmic codec bytes per step / ms_per_step / peak: "
+                             "the fraction of the HBM roofline the whole step sustains")
+        tier_move = tier_move_rates(eng, stream, codec, pool, snap_now, _Shard(mine, my_lo), space, L, H, D, bpt,
+                                    my_lo, my_hi)
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
 
     if rank == 0:
         clocks = clk.summary()
+        conf = config_dict(args, W, n_total, world)
+        conf.update({"kv_bytes_per_step": total_bytes, "kv_pool_chunks": args.pool,
+                     "l2": "inputs larger than L2 (1 GiB chunks, pool of distinct chunks)",
+                     "actions_per_step": n_act, "retained_bytes_per_step_rank0": out_b,
+                     "parallelism": f"dp{world} (contexts sharded; per-step NCCL all-gather of profile records + "
+                                    "device merge; global greedy replicated)",
+                     "identity": "contexts placed at ratio 1.0 / 16 bits are the identity configuration: their "
+                                 "compressed chunk is the source KV (no kernel, no copy; kvt_blob_map.identity); "
+                                 "their bytes still count as compressed+scored+placed",
+                     "schedule": "batches software-pipelined: batch i+1's placement overlaps batch i's compression"
+                                 + (f"; {args.streams} codec streams, snapkv scoring alone on stream 0 as "
+                                    f"persistent clusters on {args.snap_sms} SMs, top-k / pack / other scorers on "
+                                    "streams 1.. (pipeline.split_plan)" if args.lanes == "split" else
+                                    f"; {args.streams} codec streams, contexts round-robin")})
         line = {
             "metric": "KV GB/s compressed+scored+placed",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f64 scoring",
             "data": "synthetic (counter-hash KV, generated profiles)",
-            "config": {"workload": f"{args.config}: {cfg['model']} KV, {n_local} contexts/GPU x {cfg['tokens']} tokens, "
-                                   f"{len(space.methods)} methods x {len(space.ratios)} ratios x 3 tiers",
-                       "contexts_total": arrays.n, "methods": space.method_names,
-                       "kv_bytes_per_step": total_bytes, "kv_pool_chunks": args.pool,
-                       "l2": "inputs larger than L2 (1 GiB chunks, pool of distinct chunks)",
-                       "actions_per_step": n_act, "compressed_bytes_per_step_rank0": out_b,
-                       "parallelism": f"dp{world} (contexts sharded, global greedy replicated)",
-                       "schedule": "batches software-pipelined: batch i+1's placement overlaps batch i's compression"
-                                   + (f"; {args.streams} codec streams, snapkv scoring alone on stream 0 as "
-                                      f"persistent clusters on {args.snap_sms} SMs, top-k / pack / other scorers on "
-                                      "streams 1.. (pipeline.split_plan)" if args.lanes == "split" else
-                                      f"; {args.streams} codec streams, contexts round-robin")},
+            "config": conf,
             "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
+            "e2e_tiered": tiered,
             "gpu_launches": int(launches),
             "roofline": roof,
             "tier_move": tier_move,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
+        if world > 1:
+            line["nccl"] = nccl_summary(nccl_log + "*") if nccl_log else None
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
+class _Shard:
+    """This rank's contexts addressed by global index (kernel_roofline /
+    tier_move_rates read arrays.orig[c] for c in [lo, hi))."""
+
+    def __init__(self, mine, lo):
+        self.mine, self.lo = mine, lo
+
+    @property
+    def orig(self):
+        return _Offset(self.mine.orig, self.lo)
+
+
+class _Offset:
+    def __init__(self, a, lo):
+        self.a, self.lo = a, lo
+
+    def __getitem__(self, c):
+        return self.a[c - self.lo]
+
+
 # ------------------------------------------------------------ CPU reference
 
-def cpu_reference_sample(W, seconds=20.0, steps=1):
-    """The reference's own CPU path on a bounded sample of the workload:
-    placement = the reference kvtier library (oracle/_ref) running
-    insert_joint over every context of the batch; codec = the CPU codec port
-    (oracle/liboracle.so; the reference has no codec) on a sample of
-    (layer, head) slices of the placed configurations, extrapolated to full
-    chunks. Returns the cpu_baseline object (value in the bench's unit)."""
+_REF_PLACE_CACHE = {}
+
+
+def _ref_engine():
     from paper_2512_14946_b200 import _abi as A
     from paper_2512_14946_b200.kvtier import Engine
-
     ref_path = os.path.join(ROOT, "oracle", "_ref", "libkvtier_ref.so")
-    orc_path = os.path.join(ROOT, "oracle", "liboracle.so")
-    kind = "reference" if os.path.exists(ref_path) else "port"
-    place_abi = A.Abi(ref_path, "ref_", codec=False) if kind == "reference" else A.Abi(orc_path, "orc_", codec=False)
-    orc = A.Abi(orc_path, "orc_", codec=True)
+    if not os.path.exists(ref_path):
+        return None
+    return Engine(A.Abi(ref_path, "ref_", codec=False))
+
+
+def reference_placement_seconds(W, cap=2000):
+    """The reference's own greedy (insert_joint of every context, single
+    thread, proj/src/placement.cpp:225-250) on this workload, timed once per
+    process. Past `cap` contexts (C4 / C5: 6-12 min per run) it is
+    timed on the first `cap` contexts and extrapolated by the measured N^2
+    growth of the rescan (least_drop_update revisits every resident per
+    step); the line says so."""
+    key = (id(W["arrays"]), W["arrays"].n)
+    if key in _REF_PLACE_CACHE:
+        return _REF_PLACE_CACHE[key]
+    from paper_2512_14946_b200.kvtier import ProfileArrays
+    eng = _ref_engine()
+    arrays, space, params = W["arrays"], W["space"], W["params"]
+    n = arrays.n
+    sub = arrays
+    if n > cap:
+        G = len(arrays.grid) // n
+        sub = ProfileArrays.uniform_grid(arrays.ids[:cap], arrays.orig[:cap], arrays.freq[:cap], arrays.grid[:G],
+                                         arrays.qual.reshape(n, -1, G)[:cap], arrays.has[:cap])
+    from paper_2512_14946_b200 import workload
+    tiers = workload.three_tiers(int(sub.orig.sum()), W["cfg"]["gpu_frac"], 0.30)
+    ps = eng.pset(sub)
+    st = eng.store(tiers, sub.n, space)
+    t0 = time.perf_counter()
+    acts = st.insert_joint(ps, space, params, np.arange(sub.n))
+    t = time.perf_counter() - t0
+    res = {"seconds": t * (n / sub.n) ** 2, "timed_contexts": sub.n, "actions": int(len(acts)),
+           "extrapolated": n > cap}
+    _REF_PLACE_CACHE[key] = res
+    return res
+
+
+def cached_greedy_seconds(W):
+    """The same greedy restructured with a cached per-resident best update
+    (the device greedy's structure), one CPU core, on the
+    reference's own scoring functions (oracle/ref_capi.cpp
+    ref_insert_joint_cached): separates the algorithmic speed-up (quadratic
+    rescan -> N log N) from the hardware one."""
+    eng = _ref_engine()
     arrays, space, params, tiers = W["arrays"], W["space"], W["params"], W["tiers"]
-    L, H = W["shape"]["L"], W["shape"]["H"]
-    bpt = W["bytes_per_token"]
-    eng = Engine(place_abi)
     ps = eng.pset(arrays)
     st = eng.store(tiers, arrays.n, space)
     t0 = time.perf_counter()
-    st.insert_joint(ps, space, params, np.arange(arrays.n))
-    t_place = time.perf_counter() - t0
-    snap = st.snapshot()
-    # codec: time each distinct (method, ratio, T) on a 1-layer slice sample
+    acts = st.insert_joint(ps, space, params, np.arange(arrays.n), cached=True)
+    return {"seconds": round(time.perf_counter() - t0, 4), "actions": int(len(acts)), "threads": 1}
+
+
+def scoring_nproc(W, threads=None):
+    """all_candidates over every context, sharded across `threads` host
+    threads taking shards from a shared counter (the reference's work-queue
+    pattern, proj/tools/kvtier_main.cpp:206-235), each calling the reference
+    library (ref_score_candidates releases the GIL: ctypes)."""
+    import threading
+
+    from paper_2512_14946_b200.kvtier import ProfileArrays
+    eng = _ref_engine()
+    arrays, space, params, tiers = W["arrays"], W["space"], W["params"], W["tiers"]
+    threads = threads or os.cpu_count()
+    n = arrays.n
+    G = len(arrays.grid) // n
+    per = max(1, -(-n // (threads * 4)))
+    shards = []
+    for lo in range(0, n, per):
+        hi = min(n, lo + per)
+        sub = ProfileArrays.uniform_grid(arrays.ids[lo:hi], arrays.orig[lo:hi], arrays.freq[lo:hi], arrays.grid[:G],
+                                         arrays.qual.reshape(n, -1, G)[lo:hi], arrays.has[lo:hi])
+        shards.append(eng.pset(sub))
+    nxt = [0]
+    lock = threading.Lock()
+
+    def worker():
+        while True:
+            with lock:
+                i = nxt[0]
+                nxt[0] += 1
+            if i >= len(shards):
+                return
+            eng.score_candidates(shards[i], tiers, space, params)
+
+    def run(nt):
+        nxt[0] = 0
+        th = [threading.Thread(target=worker) for _ in range(nt)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return time.perf_counter() - t0
+
+    t1, tn = run(1), run(threads)
+    cands = n * len(space.methods) * len(space.ratios) * len(tiers)
+    return {"candidates": int(cands), "threads": threads, "seconds_1_thread": round(t1, 4),
+            "seconds_nproc": round(tn, 4), "candidates_per_s_nproc": round(cands / tn, 1)}
+
+
+def codec_port_seconds(W, snap, budget):
+    """The CPU codec port (oracle/liboracle.so; the reference has no codec)
+    on one layer of every distinct placed (method, ratio, length), timed on
+    all its threads within `budget` seconds, extrapolated to full chunks and
+    to every context of each configuration."""
+    from paper_2512_14946_b200 import _abi as A
+    orc = A.Abi(os.path.join(ROOT, "oracle", "liboracle.so"), "orc_", codec=True)
+    arrays, space = W["arrays"], W["space"]
+    L, H = W["shape"]["L"], W["shape"]["H"]
+    bpt = W["bytes_per_token"]
     groups = {}
     for c in range(arrays.n):
         key = (space.method_names[snap["method"][c]], float(snap["ratio"][c]), int(arrays.orig[c] // bpt))
         groups[key] = groups.get(key, 0) + 1
-    threads = int(orc.lib.orc_parallel_threads()) if hasattr(orc.lib, "orc_parallel_threads") else os.cpu_count()
-    budget = max(1.0, seconds - t_place)
-    t_codec_timed = 0.0  # extrapolated full-chunk codec seconds of the timed groups
-    timed_ctx = 0
-    spent = 0.0
+    threads = int(orc.lib.orc_parallel_threads())
+    t_codec_timed, timed_ctx, spent = 0.0, 0, 0.0
     for (meth, ratio, T), count in sorted(groups.items(), key=lambda kv: -kv[1]):
         if spent > budget:
             break
-        Ls = 1
-        s = A.KvShape(Ls, H, T, 128)
+        s = A.KvShape(1, H, T, 128)
         cfg = A.CodecCfg()
         orc.check(orc.codec_plan(meth.encode(), ratio, C.byref(s), C.byref(cfg)))
         m = A.BlobMap()
         orc.check(orc.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
-        n = Ls * H * T * 128
+        n = H * T * 128
         k = np.zeros(n, np.uint16)
         v = np.zeros(n, np.uint16)
         orc.check(orc.kv_generate(None, C.byref(s), 1, 0, A.ptr(k), A.ptr(v)))
         ws = np.zeros(orc.compress_workspace_bytes(C.byref(s), C.byref(cfg)), np.uint8)
-        blob = np.zeros(m.total_bytes, np.uint8)
+        blob = np.zeros(max(1, m.total_bytes), np.uint8)
         t0 = time.perf_counter()
         orc.check(orc.compress(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
         dt = time.perf_counter() - t0
         spent += dt
-        t_codec_timed += dt * (L / Ls) * count  # full chunk, every context of this group
+        t_codec_timed += dt * L * count
         timed_ctx += count
-    # configurations not timed within the budget cost the timed mean per context
-    t_codec_all = t_codec_timed / max(1, timed_ctx) * arrays.n
-    t_total = t_place + t_codec_all
-    value = float(arrays.orig.sum()) / t_total / 1e9
-    return {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": (f"placement: {'reference kvtier' if kind == 'reference' else 'oracle'} insert_joint over all "
-                       f"{arrays.n} contexts ({t_place:.2f} s, 1 thread); codec: CPU port (no reference codec) on "
-                       f"1 of {L} layers x {H} heads per distinct placed config ({timed_ctx}/{arrays.n} contexts' "
-                       f"configs timed in {spent:.1f} s on {threads} threads), extrapolated x{L} per chunk"),
-            "t_place_s": round(t_place, 3), "t_codec_extrapolated_s": round(t_codec_all, 3)}
+    t_all = t_codec_timed / max(1, timed_ctx) * arrays.n
+    return {"seconds": t_all, "threads": threads, "timed_contexts": timed_ctx, "spent": spent}
+
+
+def cpu_reference_sample(W, seconds=20.0, with_extras=True):
+    """The CPU arm on a bounded sample of the workload: placement = the
+    reference kvtier library's own greedy over every context (timed once per
+    process); codec = the CPU port (the reference has none) on one layer of
+    each distinct placed configuration, extrapolated. kind = "port": the
+    codec port dominates the modelled time. Extras beside it: the cached
+    greedy on one core, an nproc-thread scoring pass, the host CPU."""
+    eng = _ref_engine()
+    if eng is None:
+        return {"unavailable": "oracle/_ref not built"}
+    place = reference_placement_seconds(W)
+    ps = eng.pset(W["arrays"])
+    st = eng.store(W["tiers"], W["arrays"].n, W["space"])
+    st.insert_joint(ps, W["space"], W["params"], np.arange(W["arrays"].n), cached=True)  # same placement, fast
+    snap = st.snapshot()
+    codec = codec_port_seconds(W, snap, max(1.0, seconds))
+    t_total = place["seconds"] + codec["seconds"]
+    value = float(W["arrays"].orig.sum()) / t_total / 1e9
+    L = W["shape"]["L"]
+    out = {"value": round(value, 4), "unit": "GB/s", "cores": codec["threads"], "kind": "port",
+           "sample": (f"placement: the reference kvtier library's insert_joint over "
+                      f"{place['timed_contexts']} contexts on 1 thread ({place['seconds']:.2f} s"
+                      f"{', extrapolated N^2 to ' + str(W['arrays'].n) if place['extrapolated'] else ''}); "
+                      f"codec: CPU port of the codec spec (the reference has no codec) on 1 of {L} layers per "
+                      f"distinct placed config ({codec['timed_contexts']}/{W['arrays'].n} contexts' configs timed "
+                      f"in {codec['spent']:.1f} s on {codec['threads']} threads), extrapolated x{L}"),
+           "place": {"kind": "reference", "seconds": round(place["seconds"], 3), "threads": 1,
+                     "actions": place["actions"], "extrapolated": place["extrapolated"]},
+           "codec": {"kind": "port", "seconds": round(codec["seconds"], 3), "threads": codec["threads"]}}
+    out.update(cpu_info())
+    if with_extras:
+        out["cached_greedy"] = cached_greedy_seconds(W)
+        out["scoring_nproc"] = scoring_nproc(W)
+    return out
 
 
 def run_reference(args):
@@ -536,25 +891,39 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2512_14946_b200 import workload
-    W = workload.build(args.config, n_ctx=args.n_ctx)
+    W = workload.build(args.config, n_ctx=args.n_ctx, seed=7)
     vals = []
     cpu = None
+    budget = max(1.0, min(args.cpu_seconds, 120.0 / max(1, args.warmup + args.steps)))
     for i in range(args.warmup + args.steps):
-        cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
+        cpu = cpu_reference_sample(W, seconds=budget, with_extras=(i == 0))
+        if i == 0:
+            extras = {k: cpu[k] for k in ("cached_greedy", "scoring_nproc") if k in cpu}
         if i >= args.warmup:
             vals.append(cpu["value"])
     value = statistics.median(vals)
-    cfg = W["cfg"]
     line = {"impl": "reference", "metric": "KV GB/s compressed+scored+placed", "value": value, "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 scoring, bf16 KV",
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f64 scoring",
             "data": "synthetic (counter-hash KV, generated profiles)",
-            "config": {"workload": f"{args.config}: {cfg['model']} KV, {W['arrays'].n} contexts x {cfg['tokens']} tokens",
-                       "methods": W["space"].method_names},
+            "config": config_dict(args, W, W["arrays"].n * world, world),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cpu["cores"], "kind": cpu["kind"],
-                             "sample": cpu["sample"]},
+                             "sample": cpu["sample"], "place": cpu["place"], "codec": cpu["codec"], **extras,
+                             **cpu_info()},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch(args):
+    """--gpus N > 1 without torchrun: one process per GPU under
+    torch.distributed.run on 127.0.0.1 (the driver's own launch line)."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -567,16 +936,22 @@ def main():
     ap.add_argument("--pool", type=int, default=8, help="distinct resident KV chunks")
     ap.add_argument("--streams", type=int, default=3, help="codec CUDA streams")
     ap.add_argument("--lanes", choices=["split", "rr"], default="split",
-                    help="split: snapkv scoring alone on stream 0 (--snap-clusters clusters), every other codec "
+                    help="split: snapkv scoring alone on stream 0 (--snap-sms SM budget), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
     ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
     ap.add_argument("--snap-sms", type=int, default=64,
                     help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS)")
+    ap.add_argument("--tiered-steps", type=int, default=2, help="steps of the e2e_tiered leg (PCIe-bound)")
+    ap.add_argument("--ranks-share-gpu", action="store_true",
+                    help="test mode for 1-GPU boxes: every rank on cuda:0, profile exchange over gloo (host "
+                         "buffers); exercises the N > 1 step logic without NCCL. Not a scaling measurement.")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

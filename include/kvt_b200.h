@@ -344,6 +344,22 @@ int kvt_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
 /* the CPU restatement: plain memcpy (host pointers only) */
 int orc_tier_moves(kvt_handle* h, const kvt_move* moves, int64_t n);
 
+/* SSD tier: pinned host pieces <-> a file (O_DIRECT when 4 KiB aligned, else
+ * buffered), spread over `threads` worker threads; writes end with
+ * fdatasync. The bytes reach the file through the CPU-tier staging arena
+ * (HBM -> pinned DRAM by kvt_tier_moves, DRAM -> file here). */
+typedef struct kvt_tier_file kvt_tier_file;
+typedef struct {
+  void* host;     /* pinned host memory */
+  int64_t bytes;
+  int64_t offset; /* file offset */
+} kvt_file_io;
+int kvt_tier_file_open(const char* path, int64_t bytes, kvt_tier_file** out); /* create, reserve */
+int kvt_tier_file_direct(const kvt_tier_file* f); /* 1 if O_DIRECT is available on this file system */
+int kvt_tier_file_close(kvt_tier_file* f);
+int kvt_tier_file_write(kvt_tier_file* f, const kvt_file_io* ios, int64_t n, int32_t threads);
+int kvt_tier_file_read(kvt_tier_file* f, const kvt_file_io* ios, int64_t n, int32_t threads);
+
 /* ---- oracle_mckp (proj/src/placement.cpp:300-372): the exact
  * one-configuration-per-context optimum under the tier capacities, by
  * branch and bound over every context's candidates in candidate_preferred
@@ -359,6 +375,36 @@ int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int
 int ref_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier* tiers, int32_t n_tiers,
                     const kvt_space* space, const kvt_params* params, double max_assignments,
                     double* total_utility, kvt_best* out);
+
+/* ---- Multi-GPU profile exchange. Contexts shard by rank; the
+ * greedy's argmin spans every resident of a tier (proj/src/placement.cpp:
+ * 179-197), so every rank needs every context's profile before placement.
+ * Each rank packs its rows into one flat RECORD (host), the records are
+ * all-gathered over NCCL (ncclAllGather / all_gather_into_tensor: equal
+ * sizes, rank-major), and kvt_pset_merge builds the global profile set from
+ * the gathered records ON THE DEVICE (concatenation in rank order + grid
+ * offsets rebased by rank; no host round trip). Context index = rank *
+ * n_ctx + local index, i.e. rank-major ids ("r000-...", "r001-...") in
+ * byte-lexicographic ProfileMap order.
+ *
+ * Record layout (256-byte aligned sections, offsets from the record start):
+ *   i64 original_size_bytes[n] | f64 frequency[n] | f64 grid[g] |
+ *   f64 quality[g*M] | i32 grid_offset[n+1] (local, 0..g) | u8 has_method[n*M]
+ * with n = n_ctx, g = grid_len = grid_offset[n], M = n_methods. */
+int64_t kvt_pset_record_bytes(int32_t n_ctx, int32_t grid_len, int32_t n_methods);
+/* host: validate `profiles` like pset_create and write its record */
+int kvt_pset_record_pack(const kvt_profiles* profiles, void* record);
+/* device: `records` = world records of equal (n_ctx, grid_len, n_methods),
+ * rank-major (the all-gather output). *out: NULL to allocate a profile set,
+ * or a set from an earlier merge of the same dimensions to refill in place
+ * (stream-ordered, no allocation, no host synchronisation). */
+int kvt_pset_merge(kvt_handle* h, const void* records, int32_t world, int32_t n_ctx, int32_t grid_len,
+                   int32_t n_methods, kvt_pset** out);
+/* the CPU restatement (host pointers) */
+int64_t orc_pset_record_bytes(int32_t n_ctx, int32_t grid_len, int32_t n_methods);
+int orc_pset_record_pack(const kvt_profiles* profiles, void* record);
+int orc_pset_merge(kvt_handle* h, const void* records, int32_t world, int32_t n_ctx, int32_t grid_len,
+                   int32_t n_methods, kvt_pset** out);
 
 /* Device-pointer variants and timing helpers used by the bench. */
 /* Synchronise the handle's stream. */

@@ -88,6 +88,82 @@ int orc_pset_create(kvt_handle* h, const kvt_profiles* pr, kvt_pset** out) {
   return KVT_OK;
 }
 
+/* ---- multi-GPU profile exchange (include/kvt_b200.h "record"): restated on
+ * host memory so the gloo multi-process tests can run the rank logic */
+typedef struct {
+  int64_t orig, freq, grid, qual, goff, has, total;
+} rec_layout_t;
+
+static int64_t rec_al(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+static rec_layout_t rec_layout(int64_t n, int64_t g, int64_t M) {
+  rec_layout_t L;
+  L.orig = 0;
+  L.freq = L.orig + rec_al(8 * n);
+  L.grid = L.freq + rec_al(8 * n);
+  L.qual = L.grid + rec_al(8 * g);
+  L.goff = L.qual + rec_al(8 * g * M);
+  L.has = L.goff + rec_al(4 * (n + 1));
+  L.total = L.has + rec_al(n * M);
+  return L;
+}
+
+int64_t orc_pset_record_bytes(int32_t n_ctx, int32_t grid_len, int32_t n_methods) {
+  return rec_layout(n_ctx, grid_len, n_methods).total;
+}
+
+int orc_pset_record_pack(const kvt_profiles* pr, void* record) {
+  if (!pr || !record || pr->n_ctx < 0 || pr->n_methods <= 0) return orc_fail(KVT_EINVAL, "bad profiles");
+  const int32_t n = pr->n_ctx, M = pr->n_methods, g = pr->grid_offset[n];
+  for (int32_t c = 0; c < n; ++c) {
+    if (pr->grid_offset[c + 1] <= pr->grid_offset[c])
+      return orc_fail(KVT_EVALIDATION, "profile ratio grid is empty for context %d", c);
+    if (pr->original_size_bytes[c] <= 0) return orc_fail(KVT_EVALIDATION, "original size must be > 0");
+  }
+  const rec_layout_t L = rec_layout(n, g, M);
+  uint8_t* b = (uint8_t*)record;
+  memset(b, 0, (size_t)L.total);
+  memcpy(b + L.orig, pr->original_size_bytes, 8 * (size_t)n);
+  memcpy(b + L.freq, pr->frequency, 8 * (size_t)n);
+  memcpy(b + L.grid, pr->grid, 8 * (size_t)g);
+  memcpy(b + L.qual, pr->quality, 8 * (size_t)g * M);
+  memcpy(b + L.goff, pr->grid_offset, 4 * (size_t)(n + 1));
+  memcpy(b + L.has, pr->has_method, (size_t)n * M);
+  return KVT_OK;
+}
+
+int orc_pset_merge(kvt_handle* h, const void* records, int32_t world, int32_t n_ctx, int32_t grid_len,
+                   int32_t n_methods, kvt_pset** out) {
+  (void)h;
+  if (!records || !out || world < 1 || n_ctx < 0 || grid_len < 0 || n_methods <= 0)
+    return orc_fail(KVT_EINVAL, "bad merge request");
+  const rec_layout_t L = rec_layout(n_ctx, grid_len, n_methods);
+  const int64_t N = (int64_t)world * n_ctx, G = (int64_t)world * grid_len, M = n_methods;
+  if (*out) orc_pset_destroy(*out);
+  kvt_pset* p = (kvt_pset*)calloc(1, sizeof(kvt_pset));
+  p->n = (int32_t)N;
+  p->M = n_methods;
+  p->orig = (int64_t*)malloc(8 * (size_t)(N ? N : 1));
+  p->freq = (double*)malloc(8 * (size_t)(N ? N : 1));
+  p->goff = (int32_t*)malloc(4 * (size_t)(N + 1));
+  p->grid = (double*)malloc(8 * (size_t)(G ? G : 1));
+  p->qual = (double*)malloc(8 * (size_t)(G * M + 1));
+  p->has = (uint8_t*)malloc((size_t)(N * M + 1));
+  for (int32_t r = 0; r < world; ++r) {
+    const uint8_t* b = (const uint8_t*)records + (size_t)r * L.total;
+    memcpy(p->orig + (size_t)r * n_ctx, b + L.orig, 8 * (size_t)n_ctx);
+    memcpy(p->freq + (size_t)r * n_ctx, b + L.freq, 8 * (size_t)n_ctx);
+    memcpy(p->grid + (size_t)r * grid_len, b + L.grid, 8 * (size_t)grid_len);
+    memcpy(p->qual + (size_t)r * grid_len * M, b + L.qual, 8 * (size_t)grid_len * M);
+    memcpy(p->has + (size_t)r * n_ctx * M, b + L.has, (size_t)n_ctx * M);
+    const int32_t* go = (const int32_t*)(b + L.goff);
+    for (int32_t i = 0; i < n_ctx; ++i) p->goff[(size_t)r * n_ctx + i] = r * grid_len + go[i];
+  }
+  p->goff[N] = (int32_t)G;
+  *out = p;
+  return KVT_OK;
+}
+
 int orc_pset_destroy(kvt_pset* p) {
   if (!p) return KVT_OK;
   free(p->orig);

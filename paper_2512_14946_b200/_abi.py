@@ -94,6 +94,10 @@ class Move(C.Structure):
 
 KVT_MOVE_D2H, KVT_MOVE_H2D, KVT_MOVE_D2D, KVT_MOVE_H2H = 0, 1, 2, 3
 
+
+class FileIo(C.Structure):
+    _fields_ = [("host", C.c_void_p), ("bytes", C.c_int64), ("offset", C.c_int64)]
+
 ACTION_DTYPE = np.dtype([("kind", "<i4"), ("ctx", "<i4"), ("tier_id", "<i4"), ("method", "<i4"),
                          ("ratio", "<f8")])
 ENTRY_DTYPE = np.dtype([("tier_index", "<i4"), ("method", "<i4"), ("ratio", "<f8"),
@@ -161,6 +165,15 @@ PRODUCT_EXTRA_SIGS = {
     "tier_host_free": (C.c_int, [P]),
 }
 TIER_SIGS = {"tier_moves": (C.c_int, [P, C.POINTER(Move), i64])}
+FILE_SIGS = {"tier_file_open": (C.c_int, [C.c_char_p, i64, PP]),
+             "tier_file_direct": (C.c_int, [P]),
+             "tier_file_close": (C.c_int, [P]),
+             "tier_file_write": (C.c_int, [P, P, i64, i32]),
+             "tier_file_read": (C.c_int, [P, P, i64, i32])}
+# multi-GPU profile exchange (kvt_ product, orc_ restatement)
+MERGE_SIGS = {"pset_record_bytes": (i64, [i32, i32, i32]),
+              "pset_record_pack": (C.c_int, [C.POINTER(Profiles), P]),
+              "pset_merge": (C.c_int, [P, P, i32, i32, i32, i32, PP])}
 # ref_insert_joint_cached: the CPU cached-greedy baseline (oracle/ref_capi.cpp), same signature
 CACHED_SIGS = {"insert_joint_cached": PLACEMENT_SIGS["insert_joint"]}
 # kvt_oracle_mckp (product) / ref_oracle_mckp (reference glue): bound when exported
@@ -195,8 +208,12 @@ class Abi:
             sigs.update(PRODUCT_EXTRA_SIGS)
         if hasattr(self.lib, prefix + "tier_moves"):
             sigs.update(TIER_SIGS)
+        if hasattr(self.lib, prefix + "tier_file_open"):
+            sigs.update(FILE_SIGS)
         if hasattr(self.lib, prefix + "oracle_mckp"):
             sigs.update(MCKP_SIGS)
+        if hasattr(self.lib, prefix + "pset_merge"):
+            sigs.update(MERGE_SIGS)
         if hasattr(self.lib, prefix + "insert_joint_cached"):
             sigs.update(CACHED_SIGS)
         for name, (res, args) in sigs.items():

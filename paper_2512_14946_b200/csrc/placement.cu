@@ -295,6 +295,148 @@ extern "C" int kvt_pset_create(kvt_handle* h, const kvt_profiles* pr, kvt_pset**
   return KVT_OK;
 }
 
+// ---------------------------------------------- multi-GPU profile exchange
+// include/kvt_b200.h "record": one rank's profile rows as a flat byte record
+// (NCCL all-gathers equal-sized records); kvt_pset_merge concatenates the
+// gathered records in rank order on the device and rebases grid offsets.
+namespace kvt_rec {  // named: kernel parameter types cannot live in an anonymous namespace
+struct RecLayout {
+  int64_t orig, freq, grid, qual, goff, has, total;
+};
+int64_t rec_al(int64_t x) { return (x + 255) & ~int64_t(255); }
+RecLayout rec_layout(int64_t n, int64_t g, int64_t M) {
+  RecLayout L;
+  L.orig = 0;
+  L.freq = L.orig + rec_al(8 * n);
+  L.grid = L.freq + rec_al(8 * n);
+  L.qual = L.grid + rec_al(8 * g);
+  L.goff = L.qual + rec_al(8 * g * M);
+  L.has = L.goff + rec_al(4 * (n + 1));
+  L.total = L.has + rec_al(n * M);
+  return L;
+}
+// pset buffer sections (same layout as kvt_pset_create)
+struct PsetLayout {
+  size_t orig, freq, goff, grid, qual, has, total;
+};
+PsetLayout pset_layout(size_t n, size_t G, size_t M) {
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  PsetLayout P;
+  P.orig = 0;
+  P.freq = P.orig + align(sizeof(long long) * (n + 1));
+  P.goff = P.freq + align(sizeof(double) * (n + 1));
+  P.grid = P.goff + align(sizeof(int) * (n + 1));
+  P.qual = P.grid + align(sizeof(double) * (G + 1));
+  P.has = P.qual + align(sizeof(double) * (G * M + 1));
+  P.total = P.has + align(n * M + 1);
+  return P;
+}
+}  // namespace kvt_rec
+using namespace kvt_rec;
+
+// One block-row per (rank, section): 8-byte (or 1-byte for has) grid-stride
+// copies of the record sections into the global arrays, goff rebased.
+__global__ void __launch_bounds__(256) k_pset_merge(const uint8_t* __restrict__ rec, RecLayout L, int n, int g, int M,
+                                                    char* __restrict__ dst, PsetLayout P) {
+  const int r = blockIdx.y, sec = blockIdx.z;
+  const uint8_t* b = rec + static_cast<size_t>(r) * L.total;
+  const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x, step = size_t(gridDim.x) * blockDim.x;
+  auto copy8 = [&](int64_t src_off, size_t dst_off, size_t n8) {
+    const unsigned long long* s = reinterpret_cast<const unsigned long long*>(b + src_off);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(dst + dst_off);
+    for (size_t i = tid; i < n8; i += step) d[i] = s[i];
+  };
+  switch (sec) {
+    case 0: copy8(L.orig, P.orig + 8 * size_t(r) * n, n); break;
+    case 1: copy8(L.freq, P.freq + 8 * size_t(r) * n, n); break;
+    case 2: copy8(L.grid, P.grid + 8 * size_t(r) * g, g); break;
+    case 3: copy8(L.qual, P.qual + 8 * size_t(r) * g * M, size_t(g) * M); break;
+    case 4: {
+      const int* s = reinterpret_cast<const int*>(b + L.goff);
+      int* d = reinterpret_cast<int*>(dst + P.goff) + size_t(r) * n;
+      for (size_t i = tid; i < size_t(n); i += step) d[i] = r * g + s[i];
+      if (r == gridDim.y - 1 && tid == 0) d[n] = (r + 1) * g;  // goff[world * n] = world * g
+      break;
+    }
+    default: {
+      const uint8_t* s = b + L.has;
+      uint8_t* d = reinterpret_cast<uint8_t*>(dst + P.has) + size_t(r) * n * M;
+      for (size_t i = tid; i < size_t(n) * M; i += step) d[i] = s[i];
+    }
+  }
+}
+
+extern "C" int64_t kvt_pset_record_bytes(int32_t n_ctx, int32_t grid_len, int32_t n_methods) {
+  return rec_layout(n_ctx, grid_len, n_methods).total;
+}
+
+extern "C" int kvt_pset_record_pack(const kvt_profiles* pr, void* record) {
+  if (!pr || !record || pr->n_ctx < 0 || pr->n_methods <= 0 || pr->n_methods > KVT_MAX_METHODS)
+    return set_error(KVT_EINVAL, "bad profile set dimensions");
+  const int n = pr->n_ctx, M = pr->n_methods, g = pr->grid_offset[n];
+  for (int c = 0; c < n; ++c) {
+    if (pr->grid_offset[c + 1] <= pr->grid_offset[c])
+      return set_error(KVT_EVALIDATION, "profile ratio grid is empty for context " + std::to_string(c));
+    if (pr->original_size_bytes[c] <= 0) return set_error(KVT_EVALIDATION, "original size must be > 0");
+  }
+  const RecLayout L = rec_layout(n, g, M);
+  char* b = static_cast<char*>(record);
+  std::memset(b, 0, static_cast<size_t>(L.total));
+  std::memcpy(b + L.orig, pr->original_size_bytes, 8 * size_t(n));
+  std::memcpy(b + L.freq, pr->frequency, 8 * size_t(n));
+  std::memcpy(b + L.grid, pr->grid, 8 * size_t(g));
+  std::memcpy(b + L.qual, pr->quality, 8 * size_t(g) * M);
+  std::memcpy(b + L.goff, pr->grid_offset, 4 * size_t(n + 1));
+  std::memcpy(b + L.has, pr->has_method, size_t(n) * M);
+  return KVT_OK;
+}
+
+extern "C" int kvt_pset_merge(kvt_handle* h, const void* records, int32_t world, int32_t n_ctx, int32_t grid_len,
+                              int32_t n_methods, kvt_pset** out) {
+  KVT_ON_DEVICE(h);
+  if (!records || !out || world < 1 || n_ctx < 0 || grid_len < 0 || n_methods <= 0 || n_methods > KVT_MAX_METHODS)
+    return set_error(KVT_EINVAL, "bad merge request");
+  const size_t N = size_t(world) * n_ctx, G = size_t(world) * grid_len, M = n_methods;
+  const PsetLayout P = pset_layout(N, G, M);
+  kvt_pset* p = *out;
+  if (p && (p->dev.n != static_cast<int>(N) || p->dev.M != n_methods || p->h != h))
+    return set_error(KVT_EINVAL, "kvt_pset_merge: the set to refill has other dimensions");
+  if (!p) {
+    p = new kvt_pset();
+    p->h = h;
+    cudaError_t e = cudaMalloc(&p->buf, P.total);
+    if (e != cudaSuccess) {
+      delete p;
+      return set_error(KVT_ECUDA, std::string("cudaMalloc profiles: ") + cudaGetErrorString(e));
+    }
+    char* b = static_cast<char*>(p->buf);
+    p->dev.n = static_cast<int>(N);
+    p->dev.M = n_methods;
+    p->dev.orig = reinterpret_cast<const long long*>(b + P.orig);
+    p->dev.freq = reinterpret_cast<const double*>(b + P.freq);
+    p->dev.goff = reinterpret_cast<const int*>(b + P.goff);
+    p->dev.grid = reinterpret_cast<const double*>(b + P.grid);
+    p->dev.qual = reinterpret_cast<const double*>(b + P.qual);
+    p->dev.has = reinterpret_cast<const unsigned char*>(b + P.has);
+  }
+  const RecLayout L = rec_layout(n_ctx, grid_len, n_methods);
+  const int bx = static_cast<int>(std::min<size_t>(64, (std::max<size_t>(size_t(grid_len) * M, n_ctx) + 255) / 256 + 1));
+  k_pset_merge<<<dim3(bx, world, 6), 256, 0, h->stream>>>(static_cast<const uint8_t*>(records), L, n_ctx, grid_len,
+                                                           n_methods, static_cast<char*>(p->buf), P);
+  h->launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (!*out) {
+      cudaFree(p->buf);
+      delete p;
+    }
+    return set_error(KVT_ECUDA, std::string("k_pset_merge: ") + cudaGetErrorString(e));
+  }
+  p->id = ++g_pset_counter;  // new contents: scoring caches keyed by the set id refresh
+  *out = p;
+  return KVT_OK;
+}
+
 extern "C" int kvt_pset_destroy(kvt_pset* p) {
   KVT_ON_DEVICE((p ? p->h : nullptr));
   if (!p) return KVT_OK;

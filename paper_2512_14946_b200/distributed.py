@@ -1,5 +1,12 @@
 """Multi-GPU plumbing of the hot path, one process per GPU.
 
+Per step (bench.py, `RankPlacement`): each rank's profile rows live as one
+flat record (kvt_pset_record_pack) in a device send buffer; NCCL
+all-gathers the records rank-major (all_gather_into_tensor on the step's
+stream) and kvt_pset_merge assembles the global profile set from them on the
+device; every rank then runs the identical deterministic greedy over all
+contexts and compresses only its own shard.
+
 KV chunks shard naturally: rank r owns a contiguous range of contexts,
 compresses and scores them alone (no cross-context term in
 proj/src/utility.cpp:129-145). The one exchange is before the global
@@ -17,13 +24,15 @@ rank-major: rank r's contexts are the index range shard(n_total, world, r).
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Tuple
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
-from .kvtier import ProfileArrays
+from . import _abi as A
+from .kvtier import Engine, MergedPSet, ProfileArrays
 
 
 def shard(n_total: int, world: int, rank: int) -> Tuple[int, int]:
@@ -74,3 +83,56 @@ def gather_profiles(mine: ProfileArrays, group=None, device=None) -> ProfileArra
     qual = gather(mine.qual.reshape(n, -1)).reshape(world * n, M, G)
     has = gather(mine.has)
     return ProfileArrays.uniform_grid(context_ids(n, world), orig, freq, mine.grid[:G], qual, has)
+
+
+def pack_record(abi: A.Abi, arrays: ProfileArrays) -> np.ndarray:
+    """One rank's profile rows as the flat record of include/kvt_b200.h."""
+    g = int(arrays.goff[-1]) if arrays.n else 0
+    out = np.zeros(int(abi.pset_record_bytes(arrays.n, g, arrays.M)), np.uint8)
+    st = arrays.c_struct()
+    abi.check(abi.pset_record_pack(C.byref(st), A.ptr(out)))
+    return out
+
+
+class RankPlacement:
+    """The exchange step of one rank: its record in a send buffer on
+    `device` (CUDA for NCCL, CPU for gloo), all-gathered into a receive
+    buffer and merged into the global profile set by the engine's
+    kvt_pset_merge (orc_pset_merge for the CPU restatement). Equal context
+    counts and grid lengths on every rank (all_gather_into_tensor)."""
+
+    def __init__(self, eng: Engine, mine: ProfileArrays, group=None, device=None, pin: bool = False,
+                 merge_on=None):
+        self.eng, self.group = eng, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.n, self.M = mine.n, mine.M
+        self.g = int(mine.goff[-1]) if mine.n else 0
+        rec = pack_record(eng.abi, mine)
+        self.host = torch.from_numpy(rec)
+        if pin:
+            self.host = self.host.pin_memory()
+        dev = torch.device(device) if device is not None else torch.device("cpu")
+        self.send = self.host.to(dev).clone() if dev.type == "cuda" else self.host.clone()
+        self.recv = torch.empty(self.world * self.send.numel(), dtype=torch.uint8, device=dev)
+        self.pset = MergedPSet(eng, self.world * self.n)
+        self.h2d_bytes = int(self.send.numel())
+        # merge_on: a CUDA device when the collective runs on host buffers
+        # (gloo) but the engine merges on the GPU (bench --ranks-share-gpu)
+        self.stage = (torch.empty(self.recv.numel(), dtype=torch.uint8, device=merge_on)
+                      if merge_on is not None else None)
+
+    def upload(self):
+        """Copy the host record into the send buffer (the e2e leg's H2D)."""
+        self.send.copy_(self.host, non_blocking=True)
+
+    def exchange(self) -> MergedPSet:
+        """All-gather every rank's record, merge on the engine's device."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+            src = self.recv
+        else:
+            src = self.send
+        if self.stage is not None:
+            self.stage[:src.numel()].copy_(src, non_blocking=True)
+            src = self.stage
+        return self.pset.merge(src, self.world, self.n, self.g, self.M)

@@ -239,6 +239,25 @@ class PSet:
             pass
 
 
+class MergedPSet(PSet):
+    """A profile set assembled on the device from gathered rank records
+    (kvt_pset_merge); refilled in place by later merges of the same size."""
+
+    class _Dims:
+        def __init__(self, n):
+            self.n = n
+
+    def __init__(self, eng: Engine, n_total: int):  # noqa: super().__init__ uploads host rows; not here
+        self.eng = eng
+        self.arrays = MergedPSet._Dims(n_total)
+        self.p = C.c_void_p()
+
+    def merge(self, records, world: int, n_ctx: int, grid_len: int, n_methods: int) -> "MergedPSet":
+        self.eng.abi.check(self.eng.abi.pset_merge(self.eng.h, A.ptr(records), world, n_ctx, grid_len, n_methods,
+                                                   C.byref(self.p)))
+        return self
+
+
 class StoreState:  # proj/include/kvtier/placement.hpp:29-70
     def __init__(self, eng: Engine, tiers: Sequence[TierSpec], n_ctx: int,
                  space: Optional[CandidateSpace] = None):

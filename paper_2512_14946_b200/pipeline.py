@@ -53,6 +53,7 @@ class Codec:
         self.out: List[torch.Tensor] = []
         self._ws: List[torch.Tensor] = []
         self._out: List[List[torch.Tensor]] = []
+        self.last = None  # (lane, blob address, BlobMap) of the latest compress: the tier executor's source
 
     def plan(self, method: str, ratio: float, T: int):
         key = (method, ratio, T)
@@ -91,6 +92,7 @@ class Codec:
         out = outs[(slot // len(self.lanes)) % len(outs)]
         eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(self._ws[li]),
                                        A.ptr(out)))
+        self.last = (li, out.data_ptr(), m)
         return self.retained_bytes(m, T)
 
     def retained_bytes(self, m: A.BlobMap, T: int) -> int:
@@ -133,6 +135,7 @@ class Codec:
         outs = self._out[pack_lane]
         out = outs[(slot // len(self.lanes)) % len(outs)]
         pe.abi.check(pe.abi.pack(pe.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), A.ptr(idx), A.ptr(out)))
+        self.last = (pack_lane, out.data_ptr(), m)
         return self.retained_bytes(m, T)
 
     def launches(self) -> int:

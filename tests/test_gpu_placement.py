@@ -42,6 +42,20 @@ def test_gpu_matches_reference_random(eng, ref_abi, seed):
         compare_runs(rg, rr, f"seed{seed}/rule{rule}")
 
 
+@pytest.mark.parametrize("seed,n_ctx", [(0, 1100), (1, 1500), (2, 1025)])
+def test_gpu_matches_reference_random_deep_trees(eng, ref_abi, seed, n_ctx):
+    """Past 1,024 residents the device's per-tier tournament trees grow a
+    third level: seeded random instances there, live against the reference
+    (insert_joint of every context, then rearrange)."""
+    arrays, tiers, space, params = random_instance(seed + 4000, n_ctx=n_ctx, n_methods=3, n_tiers=3)
+    er = Engine(ref_abi)
+    order = np.random.default_rng(seed).permutation(arrays.n)
+    rr = run_inserts(er, arrays, tiers, space, params, order, then_rearrange=True)
+    rg = run_inserts(eng, arrays, tiers, space, params, order, then_rearrange=True)
+    compare_runs(rg, rr, f"deep{n_ctx}")
+    assert len(rr["actions"]) > 2 * n_ctx
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_gpu_least_drop_every_step(eng, ref_abi, seed):
     """least_drop_update on every over-full tier after every insert."""

@@ -62,3 +62,49 @@ def test_gpu_blob_round_trip_through_host_tier(gpu_abi):
     for (b, _), t in zip(blobs, back):
         assert torch.equal(b, t)
     arena.close()
+
+
+def test_ssd_tier_file_round_trip(tmp_path):
+    """kvt_tier_file_* (host code, no GPU needed): aligned pieces take
+    O_DIRECT where the file system allows it, unaligned ones the buffered
+    descriptor; every byte reads back."""
+    import paper_2512_14946_b200 as pkg
+    from paper_2512_14946_b200.tiers import SsdTier
+    abi = pkg.product()
+    rng = np.random.default_rng(1)
+    sizes = [4096 * 300, 70 << 20, 12345, 0, 4096]
+    bufs = []
+    for n in sizes:  # 4 KiB-aligned host buffers
+        raw = np.zeros(n + 8192, np.uint8)
+        off = (-raw.ctypes.data) % 4096
+        b = raw[off:off + n]
+        b[:] = rng.integers(0, 255, n, dtype=np.uint8)
+        bufs.append((raw, b))
+    ssd = SsdTier(abi, str(tmp_path / "ssd.tier"), sum(sizes) + 10 * 4096, threads=4)
+    offs = [ssd.alloc(n) for n in sizes]
+    ssd.write([(b.ctypes.data, n, o) for (_, b), n, o in zip(bufs, sizes, offs)])
+    back = [np.zeros(n + 8192, np.uint8) for n in sizes]
+    views = [r[(-r.ctypes.data) % 4096:][:n] for r, n in zip(back, sizes)]
+    ssd.read([(v.ctypes.data, n, o) for v, n, o in zip(views, sizes, offs)])
+    for (_, b), v in zip(bufs, views):
+        assert np.array_equal(b, v)
+    ssd.close()
+    assert not (tmp_path / "ssd.tier").exists()
+
+
+def test_net_placement_folds_actions_into_the_snapshot(oracle_abi):
+    """The executor's view of a batch (its action list folded in order)
+    equals the store's final state (proj/src/placement.cpp:213-221)."""
+    from cases import random_instance
+    from paper_2512_14946_b200.kvtier import Engine, sorted_tiers
+    from paper_2512_14946_b200.tiers import net_placement
+    eng = Engine(oracle_abi)
+    arrays, tiers, space, params = random_instance(77, n_ctx=120, n_methods=3, n_tiers=3)
+    ps = eng.pset(arrays)
+    st = eng.store(tiers, arrays.n, space)
+    acts = st.insert_joint(ps, space, params, np.arange(arrays.n))
+    net = net_placement(acts, arrays.n, [t.tier_id for t in sorted_tiers(tiers)])
+    snap = st.snapshot()
+    assert np.array_equal(net["tier_index"], snap["tier_index"])
+    assert np.array_equal(net["method"], snap["method"]) and np.array_equal(net["ratio"], snap["ratio"])
+    assert net["inserts"].sum() == arrays.n and net["evicts"].sum() + net["recompress"].sum() == len(acts) - arrays.n
