@@ -643,7 +643,7 @@ def run_b200(args):
     if rank == 0:
         clocks = clk.summary()
         conf = config_dict(args, W, n_total, world)
-        conf.update({"kv_bytes_per_step": total_bytes, "kv_pool_chunks": args.pool,
+        details = ({"kv_bytes_per_step": total_bytes, "kv_pool_chunks": args.pool,
                      "l2": "inputs larger than L2 (1 GiB chunks, pool of distinct chunks)",
                      "actions_per_step": n_act, "retained_bytes_per_step_rank0": out_b,
                      "parallelism": f"dp{world} (contexts sharded; per-step NCCL all-gather of profile records + "
@@ -663,6 +663,7 @@ def run_b200(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 KV, f64 scoring",
             "data": "synthetic (counter-hash KV, generated profiles)",
             "config": conf,
+            "details": details,
             "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "e2e_tiered": tiered,
