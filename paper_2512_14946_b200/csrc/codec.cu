@@ -1590,38 +1590,107 @@ extern "C" int kvt_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cf
 
 // ------------------------------------------------------------------ unpack
 
-__global__ void __launch_bounds__(256) k_unpack(const uint8_t* __restrict__ blob, kvt_blob_map m,
-                                                uint4* __restrict__ ko, uint4* __restrict__ vo, int k, int bits) {
-  const int slice = blockIdx.y, l16 = threadIdx.x & 15;
-  const int j = blockIdx.x * 16 + (threadIdx.x >> 4);
-  if (j >= k) return;
-  const size_t row = static_cast<size_t>(slice) * k + j;
-  const int wpr = kD * bits / 32, ng = (k + KVT_QGROUP - 1) / KVT_QGROUP, g = j / KVT_QGROUP;
-  const uint32_t* kc = reinterpret_cast<const uint32_t*>(blob + m.kcode_off) + row * wpr;
-  const uint32_t* vc = reinterpret_cast<const uint32_t*>(blob + m.vcode_off) + row * wpr;
-  const uint16_t* ks = reinterpret_cast<const uint16_t*>(blob + m.kscale_off) + (static_cast<size_t>(slice) * ng + g) * kD;
-  const uint16_t* kz = reinterpret_cast<const uint16_t*>(blob + m.kzero_off) + (static_cast<size_t>(slice) * ng + g) * kD;
-  const float vsf = __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(blob + m.vscale_off)[row]));
-  const float vzf = __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(blob + m.vzero_off)[row]));
-  const uint32_t mask = (1u << bits) - 1u;
-  const int per = 32 / bits;
-  uint32_t ok[4], ov[4];
-#pragma unroll
-  for (int i = 0; i < 8; i += 2) {
-    uint32_t pk[2], pv[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int d = l16 * 8 + i + e;
-      const uint32_t kcode = (kc[d / per] >> (bits * (d % per))) & mask;
-      const uint32_t vcode = (vc[d / per] >> (bits * (d % per))) & mask;
-      pk[e] = dequant_bf16(kcode, __half2float(__ushort_as_half(ks[d])), __half2float(__ushort_as_half(kz[d])));
-      pv[e] = dequant_bf16(vcode, vsf, vzf);
-    }
-    ok[i / 2] = pk[0] | (pk[1] << 16);
-    ov[i / 2] = pv[0] | (pv[1] << 16);
+// Unpack + dequantise (north-star item 1, decompression half): a half-warp
+// per kept row, kURows rows in flight per half-warp (every code / parameter
+// load of the rows is issued before any arithmetic). Lane l16 owns channels
+// 8*l16 .. 8*l16+7: its K and V codes are one contiguous b-byte piece of the
+// row (u16 / u32 / uint2 for 2 / 4 / 8 bits), its 8 K scales and zeros one
+// 16-byte load each (shared by the 128 rows of a group: L1 hits), the row's V
+// scale and zero a half-warp broadcast. x' = bf16_rn(fl(code * scale) + zero)
+// with separate correctly rounded ops (spec §4.3; __fmul_rn / __fadd_rn are
+// never contracted), stored as one 16-byte bf16x8 per lane per row.
+constexpr int kURows = 4;
+
+template <int BITS>
+__device__ __forceinline__ void load_codes(const uint8_t* base, size_t row, int l16, uint32_t (&c)[2]) {
+  constexpr int row_bytes = kD * BITS / 8;
+  const uint8_t* p = base + row * row_bytes + l16 * BITS;  // this lane's 8 channels: BITS bytes
+  if (BITS == 8) {
+    const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
+    c[0] = u.x;
+    c[1] = u.y;
+  } else if (BITS == 4) {
+    c[0] = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    c[1] = 0;
+  } else {
+    c[0] = __ldcs(reinterpret_cast<const unsigned short*>(p));
+    c[1] = 0;
   }
-  ko[row * 16 + l16] = make_uint4(ok[0], ok[1], ok[2], ok[3]);
-  vo[row * 16 + l16] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+}
+
+template <int BITS>
+__device__ __forceinline__ uint32_t code_at(const uint32_t (&c)[2], int e) {
+  if (BITS == 8) return (c[e >> 2] >> (8 * (e & 3))) & 0xffu;
+  return (c[0] >> (BITS * e)) & ((1u << BITS) - 1u);
+}
+
+// 8 codes -> 8 bf16 (one uint4); per-channel or per-row parameters
+template <int BITS>
+__device__ __forceinline__ uint4 dequant8(const uint32_t (&c)[2], const float (&sf)[8], const float (&zf)[8]) {
+  uint32_t o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float y[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * q + h;
+      const float x = __fsub_rn(__uint_as_float(0x4B000000u | code_at<BITS>(c, e)), 8388608.0f);  // exact
+      y[h] = __fadd_rn(__fmul_rn(x, sf[e]), zf[e]);
+    }
+    const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[0], y[1]);
+    o[q] = *reinterpret_cast<const uint32_t*>(&b2);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(256) k_unpack(const uint8_t* __restrict__ blob, kvt_blob_map m,
+                                                uint4* __restrict__ ko, uint4* __restrict__ vo, int k) {
+  const int slice = blockIdx.y, l16 = threadIdx.x & 15;
+  const int j0 = (blockIdx.x * 16 + (threadIdx.x >> 4)) * kURows;
+  if (j0 >= k) return;
+  const int ng = (k + KVT_QGROUP - 1) / KVT_QGROUP;
+  const uint8_t* kc = blob + m.kcode_off;
+  const uint8_t* vc = blob + m.vcode_off;
+  const uint16_t* vs = reinterpret_cast<const uint16_t*>(blob + m.vscale_off);
+  const uint16_t* vz = reinterpret_cast<const uint16_t*>(blob + m.vzero_off);
+  uint32_t kcw[kURows][2], vcw[kURows][2];
+  uint16_t vsw[kURows], vzw[kURows];
+  uint4 ksw[kURows], kzw[kURows];
+#pragma unroll
+  for (int i = 0; i < kURows; ++i) {
+    const int j = min(j0 + i, k - 1);  // tail rows re-read the last row (not stored)
+    const size_t row = static_cast<size_t>(slice) * k + j;
+    load_codes<BITS>(kc, row, l16, kcw[i]);
+    load_codes<BITS>(vc, row, l16, vcw[i]);
+    vsw[i] = vs[row];
+    vzw[i] = vz[row];
+    const size_t po = (static_cast<size_t>(slice) * ng + j / KVT_QGROUP) * kD + 8 * l16;
+    ksw[i] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(blob + m.kscale_off) + po));
+    kzw[i] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(blob + m.kzero_off) + po));
+  }
+#pragma unroll
+  for (int i = 0; i < kURows; ++i) {
+    if (j0 + i >= k) break;
+    const size_t row = static_cast<size_t>(slice) * k + j0 + i;
+    float ks[8], kz[8], vsf[8], vzf[8];
+    const uint32_t sw[4] = {ksw[i].x, ksw[i].y, ksw[i].z, ksw[i].w}, zw[4] = {kzw[i].x, kzw[i].y, kzw[i].z, kzw[i].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ks[2 * q] = __half2float(__ushort_as_half(static_cast<unsigned short>(sw[q] & 0xffffu)));
+      ks[2 * q + 1] = __half2float(__ushort_as_half(static_cast<unsigned short>(sw[q] >> 16)));
+      kz[2 * q] = __half2float(__ushort_as_half(static_cast<unsigned short>(zw[q] & 0xffffu)));
+      kz[2 * q + 1] = __half2float(__ushort_as_half(static_cast<unsigned short>(zw[q] >> 16)));
+    }
+    const float s1 = __half2float(__ushort_as_half(vsw[i])), z1 = __half2float(__ushort_as_half(vzw[i]));
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      vsf[e] = s1;
+      vzf[e] = z1;
+    }
+    __stcs(ko + row * 16 + l16, dequant8<BITS>(kcw[i], ks, kz));
+    __stcs(vo + row * 16 + l16, dequant8<BITS>(vcw[i], vsf, vzf));
+  }
 }
 
 extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const void* blob,
@@ -1640,9 +1709,13 @@ extern "C" int kvt_unpack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_
     KVT_CUDA_TRY(cudaMemcpyAsync(v_out, b + m.vcode_off, m.vcode_bytes, cudaMemcpyDeviceToDevice, h->stream));
     return KVT_OK;
   }
-  dim3 grid((kk + 15) / 16, S);
-  k_unpack<<<grid, 256, 0, h->stream>>>(reinterpret_cast<const uint8_t*>(blob), m, reinterpret_cast<uint4*>(k_out),
-                                        reinterpret_cast<uint4*>(v_out), kk, c->bits);
+  dim3 grid((kk + 16 * kURows - 1) / (16 * kURows), S);
+  const auto* bp = reinterpret_cast<const uint8_t*>(blob);
+  auto* kop = reinterpret_cast<uint4*>(k_out);
+  auto* vop = reinterpret_cast<uint4*>(v_out);
+  if (c->bits == 8) k_unpack<8><<<grid, 256, 0, h->stream>>>(bp, m, kop, vop, kk);
+  else if (c->bits == 4) k_unpack<4><<<grid, 256, 0, h->stream>>>(bp, m, kop, vop, kk);
+  else k_unpack<2><<<grid, 256, 0, h->stream>>>(bp, m, kop, vop, kk);
   LAUNCHED(h);
   return KVT_OK;
 }

@@ -618,7 +618,12 @@ static int num_sms_p() {
 // order. Pruning: the reference's own test within a thread (bound <= its
 // best), and a strict test against the best total any thread has reached
 // (never cuts a subtree that could tie), shared as an order-preserving key.
-constexpr int kMckpMaxCtx = 24;
+// Per-thread DFS state lives in fixed arrays: 24 contexts (registers /
+// L1-resident local memory) or 256 (an instance with more than 24 contexts
+// passes the reference's max_assignments guard only when most of its
+// contexts have a single candidate; those are forced levels of the same DFS).
+constexpr int kMckpSmallCtx = 24;
+constexpr int kMckpMaxCtx = 256;
 
 __device__ __forceinline__ unsigned long long mckp_key(double v) {
   const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(v, 0.0)));
@@ -629,6 +634,7 @@ __device__ __forceinline__ double mckp_val(unsigned long long k) {
   return __longlong_as_double(static_cast<long long>(b));
 }
 
+template <int NMAX>
 __global__ void __launch_bounds__(128) k_mckp(const double* __restrict__ cu, const long long* __restrict__ csz,
                                               const int* __restrict__ ctier, const int* __restrict__ off,
                                               const int* __restrict__ cnt, const double* __restrict__ suffix,
@@ -640,8 +646,8 @@ __global__ void __launch_bounds__(128) k_mckp(const double* __restrict__ cu, con
   // persistent threads take prefixes from a counter (in increasing order per
   // thread, so a thread's first maximal leaf is its lexicographically first)
   const long long me = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  int choice[kMckpMaxCtx], k[kMckpMaxCtx], best_choice[kMckpMaxCtx];
-  double tot[kMckpMaxCtx + 1];
+  int choice[NMAX], k[NMAX], best_choice[NMAX];
+  double tot[NMAX + 1];
   long long used[KVT_MAX_TIERS];
   double best = 0.0;
   long long best_pfx = -1;
@@ -768,7 +774,9 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
   if ((rc = resolve_tiers(tiers, n_tiers, &T))) return rc;
   if (p->dev.M != S.M) return set_error(KVT_EINVAL, "profile set / space method count mismatch");
   const int n = p->dev.n, M = S.M, R = S.R, TT = T.T, MR = M * R;
-  if (n > kMckpMaxCtx) return set_error(KVT_EVALIDATION, "instance too large for the exact solver");
+  if (n > kMckpMaxCtx)
+    return set_error(KVT_EVALIDATION, "instance too large for the exact solver: more than " +
+                                          std::to_string(kMckpMaxCtx) + " contexts");
   // K1 candidate tables for every (context, tier, method, ratio)
   std::vector<int64_t> size(size_t(n) * R);
   std::vector<double> q(size_t(n) * MR), tt(size_t(n) * TT * MR), u(size_t(n) * TT * MR);
@@ -892,9 +900,10 @@ extern "C" int kvt_oracle_mckp(kvt_handle* h, const kvt_pset* p, const kvt_tier*
     KVT_CUDA_TRY(cudaStreamSynchronize(st));  // key lives on this frame
   }
   KVT_CUDA_TRY(cudaMemsetAsync(d_next, 0, 8, st));
-  k_mckp<<<static_cast<int>((nthreads + 127) / 128), 128, 0, st>>>(d_cu, d_csz, d_ct, d_off, d_cnt, d_suf, T, n, d,
-                                                                   nprefix, d_gbest, d_next, d_tot, d_found, d_pfx,
-                                                                   d_choice);
+  auto kern = n <= kMckpSmallCtx ? k_mckp<kMckpSmallCtx> : k_mckp<kMckpMaxCtx>;
+  kern<<<static_cast<int>((nthreads + 127) / 128), 128, 0, st>>>(d_cu, d_csz, d_ct, d_off, d_cnt, d_suf, T, n, d,
+                                                                 nprefix, d_gbest, d_next, d_tot, d_found, d_pfx,
+                                                                 d_choice);
   h->launches++;
   KVT_CUDA_TRY(cudaGetLastError());
   auto* d_win = reinterpret_cast<long long*>(d_gbest);  // gbest is dead once the search is done

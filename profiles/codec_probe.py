@@ -67,7 +67,10 @@ def main():
             "topk": S * s.T * 4 + S * kk * 4,
             "pack": 2 * S * kk * 256 + m.total_bytes,
             "compress": S * s.T * 256 + S * kk * 256 + m.total_bytes,
+            "unpack": m.total_bytes + 2 * S * kk * 256,
         }
+        ku = torch.empty(S * kk * 128, dtype=torch.int16, device="cuda")
+        vu = torch.empty_like(ku)
         acc = {p: 0.0 for p in alg}
         for r in range(args.reps + 1):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -80,10 +83,13 @@ def main():
             ev[3].record()
             ab.check(ab.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(ws), A.ptr(blob)))
             ev[4].record()
+            if cfg.bits < 16:
+                ab.check(ab.unpack(eng.h, C.byref(s), C.byref(cfg), A.ptr(blob), A.ptr(ku), A.ptr(vu)))
+            ev[5].record()
             torch.cuda.synchronize()
             if r == 0:
                 continue  # warm-up
-            for i, p in enumerate(("scores", "topk", "pack", "compress")):
+            for i, p in enumerate(("scores", "topk", "pack", "compress", "unpack")):
                 acc[p] += ev[i].elapsed_time(ev[i + 1]) / max(1, args.reps)
         out = {"method": meth, "ratio": float(ratio), "bits": cfg.bits, "keep": kk, "T": s.T, "L": s.L}
         for p in alg:

@@ -67,3 +67,36 @@ def test_gpu_mckp_refusals_match_reference(gpu_abi, ref_abi):
 def test_reference_mckp_glue(ref_abi):
     total, best = _solve(Engine(ref_abi), *_instance(1, 3))
     assert np.isfinite(total) and len(best) == 3 and (best["status"] == 0).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,free", [(40, 5), (200, 6)])
+def test_gpu_mckp_many_forced_contexts(gpu_abi, ref_abi, n, free):
+    """More than 24 contexts: the reference refuses only when the product of
+    candidate counts exceeds max_assignments, so an instance of mostly
+    single-candidate contexts (profile grid {1.0} under a {0.5, 0.75, 1.0}
+    space: one scorable ratio) is solved exactly; one finite tier keeps the
+    capacity test live at every level."""
+    rng = np.random.default_rng(n)
+    grid_free = [0.5, 0.75, 1.0]
+    ids, orig, freq, goff, gridv, qual = [], [], [], [0], [], []
+    for i in range(n):
+        g = grid_free if i % (n // free) == 0 else [1.0]
+        ids.append(f"c{i:04d}")
+        orig.append(int(rng.integers(1, 9)) * 1_000_000_000)
+        freq.append(float(rng.uniform(0.5, 3.0)))
+        gridv += g
+        qual += sorted(rng.uniform(0.5, 1.0, len(g)).tolist())[:-1] + [1.0]
+        goff.append(len(gridv))
+    arrays = ProfileArrays(ids, np.array(orig), np.array(freq), np.array(goff), np.array(gridv), np.array(qual),
+                           np.ones((n, 1), np.uint8))
+    free_bytes = sum(o for i, o in enumerate(orig) if i % (n // free) == 0)
+    tiers = [TierSpec(0, "only", int(sum(orig) - 0.3 * free_bytes), 20e9, 1e-4)]  # the free contexts must shrink
+    space = CandidateSpace([CompressionMethod("keydiff", 0.0)], grid_free)
+    params = UtilityParams(alpha=2.0)
+    tg, bg = _solve(Engine(gpu_abi), arrays, tiers, space, params)
+    tr, br = _solve(Engine(ref_abi), arrays, tiers, space, params)
+    assert tg == tr
+    for f in ("tier_id", "method", "ratio", "size_bytes", "utility"):
+        assert np.array_equal(bg[f], br[f]), f
+    assert (br["ratio"] < 1.0).any()  # the capacity forces some compression
