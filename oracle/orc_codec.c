@@ -356,23 +356,24 @@ static void keydiff_slice(void* a, int64_t sl) {
   free(inv);
 }
 
-/* snapkv, exact-integer formulation v2.
+/* snapkv, exact-integer formulation v3.
  * Window queries quantised to int8 per row, prefix keys to int8 per
  * 128-token tile, so every logit is an exact int8 dot product I_rt times
  * a per-(tile, row) fp32 factor a_jr (log2 units). Softmax over the prefix
  * per query row uses a per-(row, 32-token block) integer shift M_br =
- * ceil(max_block y): E_rt = round(2^15 * 2^(y_rt - M_br)) by a fixed fp32
- * FMA polynomial; the row sum and the vote weights rescale blocks by exact
- * integer shifts. Votes (sum over rows of probabilities, 2^45 fixed point)
- * are max-pooled. Only IEEE single ops with a fixed association and
- * integer arithmetic appear, so the CUDA path (int8 tensor cores) matches
- * it bit for bit. */
+ * ceil(max_block y): E_rt = round(2^7 * 2^(y_rt - M_br)), an 8-bit value,
+ * by a fixed degree-2 fp32 FMA polynomial; the row sum and the vote weights
+ * rescale blocks by exact integer shifts; votes (sum over rows of
+ * probabilities, 2^37 fixed point: integer dot products of 8-bit E with
+ * 30-bit weights, which the GPU computes on the integer tensor cores) are
+ * max-pooled. Only IEEE single ops with a fixed association and integer
+ * arithmetic appear, so the CUDA path matches it bit for bit. */
 #define SNAP_C0 0.12751743082459868f /* log2(e) / sqrt(128) */
-#define SNAP_E0 32767.927734375f     /* 2^15 * 2^f on [-1/2, 1/2], degree 4 */
-#define SNAP_E1 22712.50390625f
-#define SNAP_E2 7874.56103515625f
-#define SNAP_E3 1830.2916259765625f
-#define SNAP_E4 303.2661437988281f
+#define SNAP_E0 0x1.ffec2ep+6f        /* 2^7 * 2^f on [-1/2, 1/2], degree 2 */
+#define SNAP_E1 0x1.683ef2p+6f
+#define SNAP_E2 0x1.f22ab4p+4f
+#define SNAP_LSH 24                   /* block sums scaled by 2^24 in the row sum */
+#define SNAP_VOTE_SCALE 0x1p-37f      /* vote = 2^37 x sum of probabilities */
 #define SNAP_BLK 32   /* tokens per softmax shift block */
 #define SNAP_TILE 128 /* tokens per K quantisation tile */
 
@@ -407,16 +408,15 @@ static float quant_i8(const float* x, int n, int8_t* q) {
   return a / 127.0f;
 }
 
-/* E(d) = round(2^15 * 2^max(d, -16)) with the fixed polynomial above:
- * n = rint(d), f = d - n, p = poly(f), x = p * 2^n (exponent add), rint(x). */
-static uint32_t snap_exp_u16(float d) {
+/* E(d) = round(2^7 * 2^max(d, -16)) with the fixed polynomial above:
+ * n = rint(d), f = d - n, p = poly(f), x = p * 2^n (exponent add), rint(x);
+ * 0 <= E <= 128 for d <= 0. */
+static uint32_t snap_exp_u8(float d) {
   const float dc = d > -16.0f ? d : -16.0f;
   const float t = dc + 12582912.0f;
   const float n = t - 12582912.0f;
   const float f = dc - n;
-  float p = fmaf(SNAP_E4, f, SNAP_E3);
-  p = fmaf(p, f, SNAP_E2);
-  p = fmaf(p, f, SNAP_E1);
+  float p = fmaf(SNAP_E2, f, SNAP_E1);
   p = fmaf(p, f, SNAP_E0);
   const float x = u2f(f2u(p) + (f2u(t) << 23));
   return f2u(x + 8388608.0f) - 0x4B000000u;
@@ -451,7 +451,7 @@ static void snapkv_slice(void* a, int64_t sl) {
     for (int i = 0; i < n * D_HEAD; ++i) tile[i] = bf2f(K[(size_t)t0 * D_HEAD + i]);
     tau[j] = quant_i8(tile, n * D_HEAD, k8 + (size_t)t0 * D_HEAD);
   }
-  uint16_t* E = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)R * P);
+  uint8_t* E = (uint8_t*)malloc((size_t)R * P);
   int32_t* Mb = (int32_t*)malloc(sizeof(int32_t) * (size_t)R * nblk);
   uint32_t* Lb = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)R * nblk);
   uint32_t* Wr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)R * nblk);
@@ -477,8 +477,8 @@ static void snapkv_slice(void* a, int64_t sl) {
       uint32_t L = 0;
       for (int i = 0; i < n; ++i) {
         const float X = u2f((uint32_t)(I[i] + 0x4B400000));
-        const uint32_t e = snap_exp_u16(fmaf(X, a_jr, cb));
-        E[(size_t)r * P + t0 + i] = (uint16_t)e;
+        const uint32_t e = snap_exp_u8(fmaf(X, a_jr, cb));
+        E[(size_t)r * P + t0 + i] = (uint8_t)e;
         L += e;
       }
       Mb[(size_t)r * nblk + b] = M;
@@ -489,7 +489,7 @@ static void snapkv_slice(void* a, int64_t sl) {
     uint64_t Lr = 0;
     for (int b = 0; b < nblk; ++b) {
       const int sh = m - Mb[(size_t)r * nblk + b];
-      if (sh < 64) Lr += ((uint64_t)Lb[(size_t)r * nblk + b] << 16) >> sh;
+      if (sh < 64) Lr += ((uint64_t)Lb[(size_t)r * nblk + b] << SNAP_LSH) >> sh;
     }
     const uint64_t Wt = Lr ? (1ull << 61) / Lr : 0;
     for (int b = 0; b < nblk; ++b) {
@@ -506,7 +506,7 @@ static void snapkv_slice(void* a, int64_t sl) {
     uint64_t m = vote[t];
     for (int j = t - half; j <= t + half; ++j)
       if (j >= 0 && j < P && vote[j] > m) m = vote[j];
-    out[t] = (float)m * 2.8421709430404007e-14f; /* 2^-45 */
+    out[t] = (float)m * SNAP_VOTE_SCALE;
   }
   free(q8);
   free(sig);

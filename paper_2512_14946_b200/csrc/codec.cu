@@ -431,13 +431,15 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
 
 static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKdC - 1) / kKdC)); }
 
-// snapkv on the integer tensor cores, exact-integer spec v2
+// snapkv on the integer tensor cores, exact-integer spec v3
 // of DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): window queries
 // quantised to int8 per row, prefix keys to int8 per 128-token tile, so every
 // logit is an exact s8 x s8 -> s32 dot product I (tcgen05.mma kind::i8,
 // M = N = K = 128) times a per-(tile, row) factor a. The softmax shift is per
-// (row, 32-token block): M = ceil(max y), E = round(2^15 * 2^(y - M)) by a
-// fixed FMA polynomial, blocks are combined with exact integer shifts.
+// (row, 32-token block): M = ceil(max y), E = round(2^7 * 2^(y - M)), an
+// 8-bit value, by a fixed degree-2 FMA polynomial; blocks are combined with
+// exact integer shifts; the votes sum_r E * W (W: the row's 30-bit weight of
+// the token's block) run on the integer tensor cores too.
 //
 // A thread-block cluster (<= 16 CTAs) works on one (layer, kv-head) slice
 // at a time; the clusters are persistent (as many as fit, each looping over
@@ -445,13 +447,17 @@ static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKd
 // warps bulk-copy each tile (bf16) into smem, quantise it to int8 (SW128
 // K-major UMMA layout) and multiply it against the slice's Q8 tile into a
 // double-buffered TMEM accumulator; the 16 consumer warps (lane quadrant x
-// 32-token block) turn their 32 logits into u16 E values kept in smem. The
+// 32-token block) turn their 32 logits into u8 E values stored in smem as
+// the A operand of the vote MMA ([row][token], MN-major SW128). The
 // consumers then run the slice's tail while the producers already load and
 // multiply the next slice's first tiles: row shifts and row sums are
 // all-reduced by red.async (max / add) from every CTA into every CTA,
-// completing bytes on the receiver's mbarrier; every thread votes a token
-// pair from the stored E (no second exp); boundary votes go to the
-// neighbours by st.async; pooling.
+// completing bytes on the receiver's mbarrier; the block weights are split
+// into four bytes (the B operand: n = block x limb, K = rows) and ONE
+// elected thread issues u8 x u8 -> s32 MMAs D[token][block, limb] = sum_r
+// E[r][token] * W_limb[r][block] into TMEM; each token's vote is its own
+// block's four limbs recombined; boundary votes go to the neighbours by
+// st.async; pooling.
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
 constexpr int kSnapProd = 8;           // producer warps: K tile absmax + int8 quantisation + MMA issue
 constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
@@ -474,10 +480,14 @@ struct SnapSmemT {
   uint8_t k8[2][128 * 128];  // offset 0 of the 1024-aligned base; double-buffered
   uint8_t q8[128 * 128];
   uint4 stage[128 * 16];     // one bf16 tile (32 KB), producers only
-  uint8_t e[EG ? 16 : 128 * 1024];
+  // E (u8) of TPC tiles: tile j, row r, 16-token chunk c at
+  // j * 16384 + (r / 8) * 1024 + (r % 8) * 128 + ((c ^ (r % 8)) * 16) —
+  // the MN-major SW128 layout of the vote MMA's A operand (M = tokens, K = rows)
+  uint8_t e[EG ? 16 : TPC * 16384];
   union {
     int32_t mb[TPC * 4][128];             // per (block, row) shift M
-    unsigned long long vote[TPC * 128];   // after the block weights: per-token votes
+    uint8_t btile[TPC][2048];             // after the block weights: the vote MMA's B operand
+    unsigned long long vote[TPC * 128];   // after the vote MMA: per-token votes
   };
   uint32_t lb[TPC * 4][128];  // per (block, row) sum of E, then the block weight
   unsigned long long lglob[128];  // row sums, summed in by every CTA (red.async.add)
@@ -486,7 +496,7 @@ struct SnapSmemT {
   float sig[128];
   float tau[4];  // per-tile scale, ring over the CTA's tile count
   uint32_t amax[kSnapProd];
-  uint64_t full, qbar, tfull[2], tempty[2];
+  uint64_t full, qbar, tfull[2], tempty[2], vbar;
   uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
   uint32_t tmem_base;
 };
@@ -495,14 +505,15 @@ __device__ __forceinline__ uint32_t snap_e_off(int r, int byte) {  // swizzled b
   return static_cast<uint32_t>(r) * 1024u + ((((byte >> 4) ^ r) & 7) | ((byte >> 4) & ~7)) * 16u + (byte & 15);
 }
 
-// 2^15 * 2^f on [-1/2, 1/2], degree 4 (oracle SNAP_E*)
-constexpr float kE0 = 32767.927734375f, kE1 = 22712.50390625f, kE2 = 7874.56103515625f,
-                kE3 = 1830.2916259765625f, kE4 = 303.2661437988281f;
+// 2^7 * 2^f on [-1/2, 1/2], degree 2 (oracle SNAP_E*, spec v3)
+constexpr float kE0 = 0x1.ffec2ep+6f, kE1 = 0x1.683ef2p+6f, kE2 = 0x1.f22ab4p+4f;
+constexpr int kSnapLsh = 24;             // block sums scaled by 2^24 in the row sum
+constexpr float kSnapVoteScale = 0x1p-37f;  // vote = 2^37 x sum of probabilities
 
 // Two E values: x = 12582912 + I (exact), d = fma(x, a, c) = rint-exact
-// I * a - M; E = round(2^15 * 2^max(d, -16)) (oracle snap_exp_u16), packed
+// I * a - M; E = round(2^7 * 2^max(d, -16)) (oracle snap_exp_u8), packed
 // fp32x2 ops (each lane rounds like the scalar op). Returns the raw
-// float-as-int words 0x4B000000 + E (the caller strips the bias).
+// float-as-int words 0x4B000000 + E, E <= 128.
 __device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a, float c, uint32_t& u0,
                                               uint32_t& u1) {
   const float2 x = make_float2(__uint_as_float(i0 + 0x4B400000u), __uint_as_float(i1 + 0x4B400000u));
@@ -511,9 +522,7 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a,
   const float2 t = __fadd2_rn(dc, make_float2(12582912.0f, 12582912.0f));
   const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(dc, make_float2(-n.x, -n.y));
-  float2 p = __ffma2_rn(make_float2(kE4, kE4), f, make_float2(kE3, kE3));
-  p = __ffma2_rn(p, f, make_float2(kE2, kE2));
-  p = __ffma2_rn(p, f, make_float2(kE1, kE1));
+  float2 p = __ffma2_rn(make_float2(kE2, kE2), f, make_float2(kE1, kE1));
   p = __ffma2_rn(p, f, make_float2(kE0, kE0));
   const float2 xs = make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                                 __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
@@ -522,29 +531,34 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a,
   u1 = __float_as_uint(r.y);
 }
 
-// One (row, 32-token block) of the epilogue: block shift M, E values packed
-// as u16 pairs, returns the block sum L. Ragged blocks mask tokens >= nv.
+// One (row, 32-token block) of the epilogue: block shift M, the 32 E bytes
+// packed 4 per word (token order), returns the block sum L. Ragged blocks
+// mask tokens >= nv (E = 0).
 template <bool kRagged>
-__device__ __forceinline__ uint32_t snap_block(uint32_t (&I)[32], int nv, float a, int32_t& M, uint32_t (&pk)[16]) {
+__device__ __forceinline__ uint32_t snap_block(uint32_t (&I)[32], int nv, float a, int32_t& M, uint32_t (&pk)[8]) {
   int32_t m = INT_MIN;
 #pragma unroll
   for (int i = 0; i < 32; ++i)
     if (!kRagged || i < nv) m = max(m, static_cast<int32_t>(I[i]));
   M = static_cast<int32_t>(ceilf(__fmul_rn(__int2float_rn(m), a)));
   const float c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
-  uint32_t Lraw = 0;
+  uint32_t L = 0;
 #pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    uint32_t u0, u1;
-    snap_exp_pair(I[i], I[i + 1], a, c, u0, u1);
+  for (int i = 0; i < 32; i += 4) {
+    uint32_t u[4];
+    snap_exp_pair(I[i], I[i + 1], a, c, u[0], u[1]);
+    snap_exp_pair(I[i + 2], I[i + 3], a, c, u[2], u[3]);
     if (kRagged) {
-      if (i >= nv) u0 = 0x4B000000u;
-      if (i + 1 >= nv) u1 = 0x4B000000u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i + q >= nv) u[q] = 0x4B000000u;
     }
-    Lraw += u0 + u1;
-    pk[i >> 1] = __byte_perm(u0, u1, 0x5410);  // low 16 bits of each = E (E < 2^16)
+    // low byte of each word = E (E <= 128)
+    const uint32_t w = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+    pk[i >> 2] = w;
+    L = __dp4a(w, 0x01010101u, L);
   }
-  return Lraw - 32u * 0x4B000000u;
+  return L;
 }
 
 // Half-warp int8 quantisation of one 128-channel row (lane: channels
@@ -639,12 +653,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   const uint32_t align_off = (1024u - (smem_u32(snap_raw) & 1023u)) & 1023u;
   if (align_off > static_cast<uint32_t>(slack)) __trap();  // the launch reserved less than the misalignment
   SnapSmem& sm = *reinterpret_cast<SnapSmem*>(snap_raw + align_off);
-  uint16_t* Eg = nullptr;  // EG: E[r][t] at Eg[r * TPC * 128 + t] (this SM's slot; one CTA per SM)
+  uint8_t* Eg = nullptr;  // EG: E[r][t] (u8) at Eg[r * TPC * 128 + t] (this SM's slot; one CTA per SM)
   if (EG) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     if (smid >= kSnapESlots) __trap();
-    Eg = reinterpret_cast<uint16_t*>(escr + smid * kSnapESlotBytes);
+    Eg = escr + smid * kSnapESlotBytes;
   }
 
   if (tid == 0) {
@@ -654,6 +668,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     mbar_init(&sm.tfull[1], 2);
     mbar_init(&sm.tempty[0], kSnapCons);
     mbar_init(&sm.tempty[1], kSnapCons);
+    mbar_init(&sm.vbar, 1);
     for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], 1);
     mbar_fence_init();
   }
@@ -661,7 +676,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     sm.mglob[tid] = INT_MIN;
     sm.lglob[tid] = 0;
   }
-  if (warp == 0) tmem_alloc(&sm.tmem_base, 256);
+  constexpr uint32_t kTmemCols = EG ? 256 : 512;  // logits double buffer (+ the vote MMA's TPC x 16 columns)
+  if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   cluster_sync_smem();  // every CTA's round barriers initialised before any remote arrive
   tc_fence_after();
@@ -795,23 +811,22 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
         int32_t M = INT_MIN;
         uint32_t L = 0;
-        uint32_t pk[16];
+        uint32_t pk[8];
         if (r < R && nv > 0) {
           const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
           L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = 0;
+          for (int i = 0; i < 8; ++i) pk[i] = 0;
         }
         if (EG) {
           uint4* erow = reinterpret_cast<uint4*>(Eg + r * (TPC * 128) + tok0);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) __stcg(erow + i, make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            *reinterpret_cast<uint4*>(sm.e + snap_e_off(r, tok0 * 2 + 16 * i)) =
-                make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          __stcg(erow, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+          __stcg(erow + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+        } else {  // chunks 2cb, 2cb + 1 of row r in tile j (swizzled by r % 8)
+          uint8_t* et = sm.e + j * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
+          *reinterpret_cast<uint4*>(et + (((2 * cb) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(et + (((2 * cb + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
         sm.mb[j * 4 + cb][r] = M;
         sm.lb[j * 4 + cb][r] = L;
@@ -853,7 +868,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         unsigned long long Ls = 0;
         for (int b = cq; b < nblk; b += 4) {
           const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
-          if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][crow]) << 16) >> sh;
+          if (sh < 64) Ls += (static_cast<unsigned long long>(sm.lb[b][crow]) << kSnapLsh) >> sh;
         }
         Ls += __shfl_xor_sync(0xffffffffu, Ls, 1);
         Ls += __shfl_xor_sync(0xffffffffu, Ls, 2);
@@ -872,57 +887,88 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const unsigned long long wt = (crow < R && Ls) ? div_2p61(Ls) : 0ull;
         for (int b = cq; b < nblk; b += 4) {
           const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
-          sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
+          sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
         }
       }
-      named_bar_sync(2, kCT);  // block weights complete; mb dead (vote reuses it)
-      // ---- votes: thread = token pair (2p, 2p + 1) x half of the rows (rq 0, 1);
-      // TPC / 4 rounds of 256 pairs; rows >= R have zero weight
-      for (int round = 0; round < TPC / 4; ++round) {
-        const int p = (ctid % 256) + 256 * round, rq = ctid / 256;
-        unsigned long long a0 = 0, a1 = 0;
-        if (2 * p < n_loc) {
-          const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
-          if (EG) {
+      named_bar_sync(2, kCT);  // block weights complete; mb dead (btile / vote reuse it)
+      if (!EG) {
+        // ---- votes on the tensor cores: B[n = block * 4 + limb][k = row] =
+        // byte `limb` of the row's block weight (K-major SW128, 16 x 128 per
+        // tile); D[token][n] = sum_r E[r][token] * B[n][r] (u8 x u8 -> s32,
+        // <= 128 * 128 * 255); a token's vote is its own block's four limbs
+        {
+          const int rr = ctid & 127, j = ctid >> 7;  // one (row, tile) per thread: 128 x TPC == kCT
+          if (j < ntl) {
+            uint8_t* bt = sm.btile[j];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const uint32_t w = (j * 4 + b < nblk) ? sm.lb[j * 4 + b][rr] : 0u;
+#pragma unroll
+              for (int l = 0; l < 4; ++l) {
+                const int n = b * 4 + l;
+                bt[(n >> 3) * 1024 + (n & 7) * 128 + ((((rr >> 4) ^ (n & 7)) << 4) | (rr & 15))] =
+                    static_cast<uint8_t>(w >> (8 * l));
+              }
+            }
+          }
+          fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        }
+        named_bar_sync(2, kCT);
+        if (ctid == 0) {
+          tc_fence_after();
+          constexpr uint32_t kVdesc = idesc_u8_amn(128, 16);
+          for (int j = 0; j < ntl; ++j) {
+            const uint64_t da = umma_desc_sw128(sm.e + j * 16384), db = umma_desc_sw128(sm.btile[j]);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)  // K = 32 rows per MMA: 4 atoms of 8 rows (A), 32 bytes (B)
+              umma_i8(tmem + 256 + j * 16, da + ks * (4096 >> 4), db + 2 * ks, kVdesc, ks > 0);
+          }
+          umma_commit(&sm.vbar);
+        }
+        mbar_wait(&sm.vbar, it & 1);
+        tc_fence_after();
+        if (cb < ntl) {  // warp (quad, cb): tile cb, tokens 32 quad .. (block quad of the tile)
+          uint32_t d[4];
+          tmem_ld4(tmem + (uint32_t(quad * 32) << 16) + 256 + cb * 16 + quad * 4, d);
+          const unsigned long long v = static_cast<unsigned long long>(d[0]) +
+                                       (static_cast<unsigned long long>(d[1]) << 8) +
+                                       (static_cast<unsigned long long>(d[2]) << 16) +
+                                       (static_cast<unsigned long long>(d[3]) << 24);
+          sm.vote[cb * 128 + quad * 32 + lane] = v;
+        }
+        tc_fence_before();
+      } else {
+        // ---- votes on the CUDA cores (E in global scratch): thread = token
+        // pair (2p, 2p + 1) x half of the rows (rq 0, 1); TPC / 4 rounds of 256
+        // pairs; rows >= R have zero weight
+        for (int round = 0; round < TPC / 4; ++round) {
+          const int p = (ctid % 256) + 256 * round, rq = ctid / 256;
+          unsigned long long a0 = 0, a1 = 0;
+          if (2 * p < n_loc) {
+            const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
 #pragma unroll 4
             for (int r0 = 0; r0 < 64; r0 += 4) {
               const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
               const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const uint32_t e2 = __ldcg(reinterpret_cast<const uint32_t*>(Eg + (rq * 64 + r0 + q) * (TPC * 128)) + p);
-                a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
-                a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
-              }
-            }
-          } else {
-            // the pair's swizzled byte offset in row r depends on r & 7 only:
-            // 8 offsets, the row stride folds into the load's immediate
-            const uint8_t* eb[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) eb[q] = sm.e + rq * 64 * 1024 + snap_e_off(q, 4 * p);
-#pragma unroll
-            for (int r0 = 0; r0 < 64; r0 += 8) {
-              const uint4 wa = *reinterpret_cast<const uint4*>(wb + r0);
-              const uint4 wc = *reinterpret_cast<const uint4*>(wb + r0 + 4);
-              const uint32_t ww[8] = {wa.x, wa.y, wa.z, wa.w, wc.x, wc.y, wc.z, wc.w};
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const uint32_t e2 = *reinterpret_cast<const uint32_t*>(eb[q] + r0 * 1024);  // row rq*64 + r0 + q
-                a0 += static_cast<unsigned long long>(e2 & 0xffffu) * ww[q];
-                a1 += static_cast<unsigned long long>(e2 >> 16) * ww[q];
+                const uint32_t e2 =
+                    __ldcg(reinterpret_cast<const unsigned short*>(Eg + (rq * 64 + r0 + q) * (TPC * 128)) + p);
+                a0 += static_cast<unsigned long long>(e2 & 0xffu) * ww[q];
+                a1 += static_cast<unsigned long long>(e2 >> 8) * ww[q];
               }
             }
           }
-        }
-        if (rq == 1) {
-          sm.vote[2 * p] = a0;
-          sm.vote[2 * p + 1] = a1;
-        }
-        named_bar_sync(2, kCT);
-        if (rq == 0) {
-          sm.vote[2 * p] += a0;
-          sm.vote[2 * p + 1] += a1;
+          named_bar_sync(2, kCT);  // (round > 0) the previous round's weight reads are done
+          if (rq == 1) {
+            sm.vote[2 * p] = a0;
+            sm.vote[2 * p + 1] = a1;
+          }
+          named_bar_sync(2, kCT);
+          if (rq == 0) {
+            sm.vote[2 * p] += a0;
+            sm.vote[2 * p + 1] += a1;
+          }
         }
       }
       named_bar_sync(2, kCT);  // votes complete
@@ -947,7 +993,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           const unsigned long long x = li < 0 ? sm.lhalo[li + half] : (li >= n_loc ? sm.rhalo[li - n_loc] : sm.vote[li]);
           m = x > m ? x : m;
         }
-        out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), 2.8421709430404007e-14f);  // 2^-45 (exact)
+        out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), kSnapVoteScale);  // 2^-37 (exact)
       }
       if (rank == C - 1)
         for (int t = P + ctid; t < T; t += kCT) out[t] = INFINITY;  // window tokens always kept
@@ -958,7 +1004,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   // once every CTA's consumers are past their last round.
   tc_fence_before();
   cluster_sync_smem();
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
 __global__ void k_fill_inf(float* __restrict__ out, long long n) {

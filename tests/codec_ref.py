@@ -101,8 +101,10 @@ def keydiff_similarity(k):
 
 
 SNAP_C0 = np.float32(0.12751743082459868)  # log2(e) / sqrt(128)
-SNAP_E = [np.float32(x) for x in (32767.927734375, 22712.50390625, 7874.56103515625, 1830.2916259765625,
-                                  303.2661437988281)]  # 2^15 * 2^f on [-1/2, 1/2], degree 4
+SNAP_E = [np.float32(float.fromhex(x)) for x in ("0x1.ffec2ep+6", "0x1.683ef2p+6", "0x1.f22ab4p+4")]
+# 2^7 * 2^f on [-1/2, 1/2], degree 2 (spec v3)
+SNAP_LSH = 24  # block sums scaled by 2^24 in the row sum
+SNAP_VOTE_SCALE = np.float32(2.0 ** -37)
 
 
 def fma32(a, b, c):
@@ -139,22 +141,21 @@ def quant_i8(x, axis):
     return q, scale.astype(np.float32)
 
 
-def snap_exp_u16(d):
-    """round(2^15 * 2^max(d, -16)) with the fixed fp32 FMA polynomial."""
+def snap_exp_u8(d):
+    """round(2^7 * 2^max(d, -16)) with the fixed fp32 FMA polynomial (v3)."""
     d = np.asarray(d, np.float32)
     dc = np.maximum(d, np.float32(-16))
     t = (dc + np.float32(12582912)).astype(np.float32)
     n = (t - np.float32(12582912)).astype(np.float32)
     f = (dc - n).astype(np.float32)
-    p = fma32(SNAP_E[4], f, SNAP_E[3])
-    for cst in (SNAP_E[2], SNAP_E[1], SNAP_E[0]):
-        p = fma32(p, f, cst)
+    p = fma32(SNAP_E[2], f, SNAP_E[1])
+    p = fma32(p, f, SNAP_E[0])
     x = (p.view(np.uint32) + (t.view(np.uint32) << np.uint32(23))).astype(np.uint32).view(np.float32)
     return ((x + np.float32(8388608)).astype(np.float32).view(np.uint32) - np.uint32(0x4B000000)).astype(np.uint64)
 
 
 def snapkv_scores(k, q, W, G, pool):
-    """Exact-integer snapkv v2, vectorised numpy, float32 ops."""
+    """Exact-integer snapkv v3, vectorised numpy, float32 ops."""
     L, H, T, D = k.shape
     P = T - W
     out = np.full((L, H, T), np.inf, np.float32)
@@ -184,16 +185,16 @@ def snapkv_scores(k, q, W, G, pool):
             M = np.ceil((mx.astype(np.float32) * ab).astype(np.float32)).astype(np.int64)
             cb = ((-M).astype(np.float32) - (np.float32(12582912) * ab).astype(np.float32)).astype(np.float32)
             X = ((I + 0x4B400000).astype(np.uint32)).view(np.float32)
-            E = snap_exp_u16(fma32(X, a, cb[:, blk]))
+            E = snap_exp_u8(fma32(X, a, cb[:, blk]))
             Lb = np.add.reduceat(E, np.arange(0, P, 32), axis=1).astype(np.uint64)
             m = M.max(1, keepdims=True)
             sh = (m - M)
-            Lr = np.where(sh < 64, (Lb << np.uint64(16)) >> np.minimum(sh, 63).astype(np.uint64), 0).sum(1)
+            Lr = np.where(sh < 64, (Lb << np.uint64(SNAP_LSH)) >> np.minimum(sh, 63).astype(np.uint64), 0).sum(1)
             Wt = np.where(Lr > 0, (np.uint64(1) << np.uint64(61)) // np.maximum(Lr, 1), 0).astype(np.uint64)
             Wb = np.where(sh < 64, Wt[:, None] >> np.minimum(sh, 63).astype(np.uint64), 0).astype(np.uint64)
             vote = (E * Wb[:, blk]).sum(0)
             pooled = np.array([vote[max(0, t - pool // 2):t + pool // 2 + 1].max() for t in range(P)], np.uint64)
-            out[l, h, :P] = (pooled.astype(np.float64).astype(np.float32) * np.float32(2.0 ** -45)).astype(np.float32)
+            out[l, h, :P] = (pooled.astype(np.float64).astype(np.float32) * SNAP_VOTE_SCALE).astype(np.float32)
     return out
 
 
