@@ -464,20 +464,20 @@ constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane qu
 constexpr int kSnapThreads = (kSnapProd + kSnapCons) * 32;
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
 constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
-// Two configurations of one kernel: prefixes up to 16 x 4 tiles (8192
-// tokens) keep the u16 E matrix in smem (TPC = 4, 218 KB); longer ones
-// (up to 16 x 16 tiles) keep it in a global scratch slot per SM (TPC = 16,
-// E [128 rows][2048 tokens] = 512 KB per CTA, one CTA per SM).
-constexpr int kSnapTpcSmem = 4, kSnapTpcGlobal = 16;
+// Two configurations of one kernel: prefixes up to 16 x 8 tiles (16384
+// tokens) keep the u8 E matrix in smem (TPC = 8: 1,024 tokens per CTA, so a
+// Llama 8,192-token chunk is one 8-CTA cluster per slice and two clusters
+// fit a GPC; 218 KB); longer ones (up to 16 x 16 tiles) keep it in a global
+// scratch slot per SM (TPC = 16, E [128 rows][2048 tokens] = 256 KB per CTA,
+// one CTA per SM) and vote on the CUDA cores.
+constexpr int kSnapTpcSmem = 8, kSnapTpcGlobal = 16;
 constexpr int kSnapESlots = 256;  // >= %nsmid on B200
-constexpr int64_t kSnapESlotBytes = 128LL * kSnapTpcGlobal * 128 * 2;
+constexpr int64_t kSnapESlotBytes = 128LL * kSnapTpcGlobal * 128;
 
-// E in smem is [row][512 tokens] u16, 1 KiB per row, 16-byte chunk c of row
-// r stored at chunk c ^ (r & 7): conflict-free row-wise STS.128 and
-// token-wise LDS.32.
 template <int TPC, bool EG>
 struct SnapSmemT {
-  uint8_t k8[2][128 * 128];  // offset 0 of the 1024-aligned base; double-buffered
+  static constexpr int KB = EG ? 2 : 1;  // k8 buffers (the smem-E configuration single-buffers to fit)
+  uint8_t k8[KB][128 * 128];  // offset 0 of the 1024-aligned base
   uint8_t q8[128 * 128];
   uint4 stage[128 * 16];     // one bf16 tile (32 KB), producers only
   // E (u8) of TPC tiles: tile j, row r, 16-token chunk c at
@@ -489,7 +489,9 @@ struct SnapSmemT {
     uint8_t btile[TPC][2048];             // after the block weights: the vote MMA's B operand
     unsigned long long vote[TPC * 128];   // after the vote MMA: per-token votes
   };
-  uint32_t lb[TPC * 4][128];  // per (block, row) sum of E, then the block weight
+  // per (block, row) sum of E (<= 4096); the CUDA-core vote (EG) then keeps
+  // the block weight (< 2^30) here, the tensor-core vote writes it into btile
+  typename std::conditional<EG, uint32_t, uint16_t>::type lb[TPC * 4][128];
   unsigned long long lglob[128];  // row sums, summed in by every CTA (red.async.add)
   int32_t mglob[128];             // row shifts, max-ed in by every CTA (red.async.max)
   unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
@@ -500,6 +502,9 @@ struct SnapSmemT {
   uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
   uint32_t tmem_base;
 };
+
+static_assert(sizeof(SnapSmemT<kSnapTpcSmem, false>) + 1024 <= 232448, "snapkv smem configuration exceeds 227 KB");
+static_assert(sizeof(SnapSmemT<kSnapTpcGlobal, true>) + 1024 <= 232448, "snapkv global-E configuration exceeds 227 KB");
 
 __device__ __forceinline__ uint32_t snap_e_off(int r, int byte) {  // swizzled byte offset of E[r][byte / 2]
   return static_cast<uint32_t>(r) * 1024u + ((((byte >> 4) ^ r) & 7) | ((byte >> 4) & ~7)) * 16u + (byte & 15);
@@ -743,9 +748,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
         const float Af = bf2f(mx);
         const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
-        if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
+        if (SnapSmem::KB == 2) {
+          if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
+        } else if (g >= 1) {
+          mbar_wait(&sm.tfull[(g - 1) & 1], ((g - 1) >> 1) & 1);  // MMA of tile g - 1 done reading k8
+        }
         if (ptid == 0) sm.tau[g & 3] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;  // tile g - 4 long consumed
-        uint8_t* k8 = sm.k8[buf];
+        uint8_t* k8 = sm.k8[SnapSmem::KB == 2 ? buf : 0];
 #pragma unroll
         for (int i = 0; i < kRowsPT; ++i) {
           const int row = rbase + kSnapProd * 8 * i;
@@ -885,35 +894,42 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         Ls = __shfl_sync(0xffffffffu, Ls, lane & ~3);
         if (cq == 0) sm.lglob[crow] = 0;
         const unsigned long long wt = (crow < R && Ls) ? div_2p61(Ls) : 0ull;
-        for (int b = cq; b < nblk; b += 4) {
-          const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
-          sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
-        }
-      }
-      named_bar_sync(2, kCT);  // block weights complete; mb dead (btile / vote reuse it)
-      if (!EG) {
-        // ---- votes on the tensor cores: B[n = block * 4 + limb][k = row] =
-        // byte `limb` of the row's block weight (K-major SW128, 16 x 128 per
-        // tile); D[token][n] = sum_r E[r][token] * B[n][r] (u8 x u8 -> s32,
-        // <= 128 * 128 * 255); a token's vote is its own block's four limbs
-        {
-          const int rr = ctid & 127, j = ctid >> 7;  // one (row, tile) per thread: 128 x TPC == kCT
-          if (j < ntl) {
+        if (EG) {
+          for (int b = cq; b < nblk; b += 4) {
+            const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
+            sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
+          }
+        } else {
+          // ---- votes on the tensor cores: B[n = block * 4 + limb][k = row] =
+          // byte `limb` of the row's block weight (K-major SW128, 16 x 128 per
+          // tile); D[token][n] = sum_r E[r][token] * B[n][r] (u8 x u8 -> s32,
+          // <= 128 * 128 * 255); a token's vote is its own block's four limbs.
+          // The weights go through registers: btile aliases mb, which the
+          // shifts still read
+          uint32_t w[TPC];
+#pragma unroll
+          for (int i = 0; i < TPC; ++i) {
+            const int b = cq + 4 * i;
+            const int64_t sh = b < nblk ? int64_t(mrow) - sm.mb[b][crow] : 64;
+            w[i] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
+          }
+          named_bar_sync(2, kCT);  // every shift read: mb is free for btile
+#pragma unroll
+          for (int i = 0; i < TPC; ++i) {
+            const int b = cq + 4 * i, j = b >> 2;
             uint8_t* bt = sm.btile[j];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const uint32_t w = (j * 4 + b < nblk) ? sm.lb[j * 4 + b][rr] : 0u;
-#pragma unroll
-              for (int l = 0; l < 4; ++l) {
-                const int n = b * 4 + l;
-                bt[(n >> 3) * 1024 + (n & 7) * 128 + ((((rr >> 4) ^ (n & 7)) << 4) | (rr & 15))] =
-                    static_cast<uint8_t>(w >> (8 * l));
-              }
+            for (int l = 0; l < 4; ++l) {
+              const int n = (b & 3) * 4 + l;
+              bt[(n >> 3) * 1024 + (n & 7) * 128 + ((((crow >> 4) ^ (n & 7)) << 4) | (crow & 15))] =
+                  static_cast<uint8_t>(w[i] >> (8 * l));
             }
           }
           fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
         }
-        named_bar_sync(2, kCT);
+      }
+      named_bar_sync(2, kCT);  // block weights complete; mb dead (btile / vote reuse it)
+      if (!EG) {
         if (ctid == 0) {
           tc_fence_after();
           constexpr uint32_t kVdesc = idesc_u8_amn(128, 16);
@@ -927,14 +943,14 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         }
         mbar_wait(&sm.vbar, it & 1);
         tc_fence_after();
-        if (cb < ntl) {  // warp (quad, cb): tile cb, tokens 32 quad .. (block quad of the tile)
+        for (int j = cb; j < ntl; j += 4) {  // warp (quad, cb): tiles cb, cb + 4; tokens 32 quad .. (block quad)
           uint32_t d[4];
-          tmem_ld4(tmem + (uint32_t(quad * 32) << 16) + 256 + cb * 16 + quad * 4, d);
+          tmem_ld4(tmem + (uint32_t(quad * 32) << 16) + 256 + j * 16 + quad * 4, d);
           const unsigned long long v = static_cast<unsigned long long>(d[0]) +
                                        (static_cast<unsigned long long>(d[1]) << 8) +
                                        (static_cast<unsigned long long>(d[2]) << 16) +
                                        (static_cast<unsigned long long>(d[3]) << 24);
-          sm.vote[cb * 128 + quad * 32 + lane] = v;
+          sm.vote[j * 128 + quad * 32 + lane] = v;
         }
         tc_fence_before();
       } else {
@@ -945,7 +961,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           const int p = (ctid % 256) + 256 * round, rq = ctid / 256;
           unsigned long long a0 = 0, a1 = 0;
           if (2 * p < n_loc) {
-            const uint32_t* wb = sm.lb[p >> 4] + rq * 64;
+            const uint32_t* wb = reinterpret_cast<const uint32_t*>(sm.lb[p >> 4]) + rq * 64;  // (EG: u32 weights)
 #pragma unroll 4
             for (int r0 = 0; r0 < 64; r0 += 4) {
               const uint4 w4 = *reinterpret_cast<const uint4*>(wb + r0);
