@@ -471,6 +471,7 @@ constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) 
 // scratch slot per SM (TPC = 16, E [128 rows][2048 tokens] = 256 KB per CTA,
 // one CTA per SM) and vote on the CUDA cores.
 constexpr int kSnapTpcSmem = 8, kSnapTpcGlobal = 16;
+constexpr int kSnapAcc = 3;  // TMEM logit accumulators (128 columns each): producers run up to 3 tiles ahead
 constexpr int kSnapESlots = 256;  // >= %nsmid on B200
 constexpr int64_t kSnapESlotBytes = 128LL * kSnapTpcGlobal * 128;
 
@@ -498,7 +499,7 @@ struct SnapSmemT {
   float sig[128];
   float tau[4];  // per-tile scale, ring over the CTA's tile count
   uint32_t amax[kSnapProd];
-  uint64_t full, qbar, tfull[2], tempty[2], vbar;
+  uint64_t full, qbar, tfull[kSnapAcc], tempty[kSnapAcc], vbar;
   uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
   uint32_t tmem_base;
 };
@@ -669,10 +670,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   if (tid == 0) {
     mbar_init(&sm.full, 1);
     mbar_init(&sm.qbar, 1);
-    mbar_init(&sm.tfull[0], 2);  // tcgen05.commit + the issuing producer thread (orders sm.tau)
-    mbar_init(&sm.tfull[1], 2);
-    mbar_init(&sm.tempty[0], kSnapCons);
-    mbar_init(&sm.tempty[1], kSnapCons);
+    for (int i = 0; i < kSnapAcc; ++i) {
+      mbar_init(&sm.tfull[i], 2);  // tcgen05.commit + the issuing producer thread (orders sm.tau)
+      mbar_init(&sm.tempty[i], kSnapCons);
+    }
     mbar_init(&sm.vbar, 1);
     for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], 1);
     mbar_fence_init();
@@ -681,7 +682,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     sm.mglob[tid] = INT_MIN;
     sm.lglob[tid] = 0;
   }
-  constexpr uint32_t kTmemCols = EG ? 256 : 512;  // logits double buffer (+ the vote MMA's TPC x 16 columns)
+  // kSnapAcc x 128 logit columns, then (smem-E configuration) the vote MMA's TPC x 16
+  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kVoteCol = kSnapAcc * 128;
+  static_assert(EG || kVoteCol + TPC * 16 <= kTmemCols, "TMEM columns");
   if (warp == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   tc_fence_before();
   cluster_sync_smem();  // every CTA's round barriers initialised before any remote arrive
@@ -703,7 +707,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       const int g0 = it * ntl;
       if (ptid == 0 && ntl > 0) {
         // q8 / sig are free once the previous slice's last MMA has completed
-        if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) & 1], ((g0 - 1) >> 1) & 1);
+        if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) % kSnapAcc], ((g0 - 1) / kSnapAcc) & 1);
         mbar_expect_tx(&sm.qbar, kSnapQBytes);
         bulk_g2s_hint(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar,
                       l2_evict_last());  // the Q8 tiles serve every chunk
@@ -712,9 +716,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         fence_async_smem();
         mbar_expect_tx(&sm.full, rows * 256);
         bulk_g2s_hint(sm.stage, Ks, rows * 256, &sm.full, l2_evict_first());  // K is read once
+        if (ntl > 1) bulk_prefetch_l2(Ks + 128 * 16, min(128, n_loc - 128) * 256);  // tile 1 on its way to L2
       }
       for (int j = 0; j < ntl; ++j) {
-        const int g = g0 + j, buf = g & 1;
+        const int g = g0 + j, buf = g % kSnapAcc;
         const int rows = min(128, n_loc - j * 128);
         mbar_wait(&sm.full, g & 1);
         uint4 v[kRowsPT][4];
@@ -743,18 +748,27 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           mbar_expect_tx(&sm.full, nrows * 256);
           bulk_g2s_hint(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full, l2_evict_first());
         }
+        if (ptid == 0) {  // the tile after that into L2 (this slice's, or the next slice's first)
+          if (j + 2 < ntl) {
+            bulk_prefetch_l2(Ks + static_cast<size_t>(j + 2) * 128 * 16, min(128, n_loc - (j + 2) * 128) * 256);
+          } else if (j + 2 - ntl < ntl && slice + static_cast<int>(gridDim.y) < nslice) {
+            const int jn = j + 2 - ntl;
+            bulk_prefetch_l2(K + (static_cast<size_t>(slice + gridDim.y) * T + t_lo + jn * 128) * 16,
+                             min(128, n_loc - jn * 128) * 256);
+          }
+        }
         uint32_t mx = 0;
 #pragma unroll
         for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
         const float Af = bf2f(mx);
         const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
         if (SnapSmem::KB == 2) {
-          if (g >= 2) mbar_wait(&sm.tfull[buf], ((g >> 1) - 1) & 1);  // MMA of tile g - 2 done reading k8[buf]
+          if (g >= 2) mbar_wait(&sm.tfull[(g - 2) % kSnapAcc], ((g - 2) / kSnapAcc) & 1);  // MMA g - 2 done with k8[g & 1]
         } else if (g >= 1) {
-          mbar_wait(&sm.tfull[(g - 1) & 1], ((g - 1) >> 1) & 1);  // MMA of tile g - 1 done reading k8
+          mbar_wait(&sm.tfull[(g - 1) % kSnapAcc], ((g - 1) / kSnapAcc) & 1);  // MMA of tile g - 1 done reading k8
         }
         if (ptid == 0) sm.tau[g & 3] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;  // tile g - 4 long consumed
-        uint8_t* k8 = sm.k8[SnapSmem::KB == 2 ? buf : 0];
+        uint8_t* k8 = sm.k8[SnapSmem::KB == 2 ? (g & 1) : 0];
 #pragma unroll
         for (int i = 0; i < kRowsPT; ++i) {
           const int row = rbase + kSnapProd * 8 * i;
@@ -783,7 +797,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         named_bar_sync(1, kSnapProd * 32);
         if (ptid == 0) {
           if (j == 0) mbar_wait(&sm.qbar, it & 1);  // this slice's Q8 tile landed
-          if (g >= 2) mbar_wait(&sm.tempty[buf], ((g >> 1) - 1) & 1);  // consumers drained acc[buf]
+          if (g >= kSnapAcc) mbar_wait(&sm.tempty[buf], ((g / kSnapAcc) - 1) & 1);  // consumers drained acc[buf]
           tc_fence_after();
           mbar_arrive(&sm.tfull[buf]);  // release: sm.tau visible to the consumers
           const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
@@ -807,8 +821,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       // in place once tile g0's accumulator is (ntl == 0: the tail reads no sig)
       float sig_r = 0.0f;
       for (int j = 0; j < ntl; ++j) {
-        const int g = g0 + j, buf = g & 1;
-        mbar_wait(&sm.tfull[buf], (g >> 1) & 1);
+        const int g = g0 + j, buf = g % kSnapAcc;
+        mbar_wait(&sm.tfull[buf], (g / kSnapAcc) & 1);
         tc_fence_after();
         if (j == 0) sig_r = sm.sig[r];
         uint32_t I[32];
@@ -816,7 +830,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const float tau = sm.tau[g & 3];
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile g + 2 may overwrite it
+        if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile g + kSnapAcc may overwrite it
         const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
         int32_t M = INT_MIN;
         uint32_t L = 0;
@@ -937,7 +951,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             const uint64_t da = umma_desc_sw128(sm.e + j * 16384), db = umma_desc_sw128(sm.btile[j]);
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)  // K = 32 rows per MMA: 4 atoms of 8 rows (A), 32 bytes (B)
-              umma_i8(tmem + 256 + j * 16, da + ks * (4096 >> 4), db + 2 * ks, kVdesc, ks > 0);
+              umma_i8(tmem + kVoteCol + j * 16, da + ks * (4096 >> 4), db + 2 * ks, kVdesc, ks > 0);
           }
           umma_commit(&sm.vbar);
         }
@@ -945,7 +959,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         tc_fence_after();
         for (int j = cb; j < ntl; j += 4) {  // warp (quad, cb): tiles cb, cb + 4; tokens 32 quad .. (block quad)
           uint32_t d[4];
-          tmem_ld4(tmem + (uint32_t(quad * 32) << 16) + 256 + j * 16 + quad * 4, d);
+          tmem_ld4(tmem + (uint32_t(quad * 32) << 16) + kVoteCol + j * 16 + quad * 4, d);
           const unsigned long long v = static_cast<unsigned long long>(d[0]) +
                                        (static_cast<unsigned long long>(d[1]) << 8) +
                                        (static_cast<unsigned long long>(d[2]) << 16) +
