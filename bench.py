@@ -401,6 +401,31 @@ def _alias(ptr, n):
     return torch.as_tensor(_Cai(), device="cuda")
 
 
+def north_star_pass(args):
+    """BASELINE configs[4] beside the headline config: the full compress +
+    score + place pass over 13,889 varied-length contexts x 72 candidates =
+    1,000,008 chunk-configs (the north-star target), one warm-up and
+    `--n1-steps` timed steps in a child process on the same GPU. Its
+    placement is the reference's own, bit for bit
+    (tests/test_large_placement.py, fixture from the reference greedy)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "c5", "--steps", str(args.n1_steps), "--warmup", "1",
+           "--no-cpu-baseline", "--tiered-steps", "0", "--no-n1", "--snap-sms", str(args.snap_sms),
+           "--streams", str(args.streams), "--lanes", args.lanes]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal for the headline line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    roof = d.get("roofline") or {}
+    return {"workload": d["config"]["workload"], "candidates": 13889 * 72, "value": d["value"], "unit": "GB/s",
+            "ms_per_step": d["ms_per_step"], "steps": d["steps"], "e2e": d["e2e"],
+            "actions_per_step": d["details"]["actions_per_step"], "step_hbm_frac": roof.get("step_hbm_frac"),
+            "dominant_kernel": roof.get("kernel"), "dominant_frac": roof.get("frac"),
+            "gpu_launches": d.get("gpu_launches"), "clocks": d.get("clocks"),
+            "parity": "placement bit-exact to the reference greedy on this instance (tests/test_large_placement.py "
+                      "c5 fixture); codec kernels bit-exact to the codec oracle (tests/test_gpu_codec.py)"}
+
+
 def cpu_info():
     model = None
     try:
@@ -610,20 +635,22 @@ def run_b200(args):
     e2e_value = total_bytes / (e2e_ms / args.steps / 1e3) / 1e9
 
     # ---- e2e_tiered: e2e + every below-GPU-tier context's bytes leave HBM over PCIe
-    tiered_steps = max(1, min(args.steps, args.tiered_steps))
-    staging = StagingRing(eng.abi, max(kv_bytes, int(codec._out[0][0].numel())), slots=2)
-    t_ms, (_, _, _, moved, _, snap_t) = timed(lambda: run_steps(tiered_steps, True, True, tiered=True))
-    staging.close()
-    mv_t = torch.tensor([moved], dtype=torch.int64, device="cpu" if args.ranks_share_gpu else "cuda")
-    if world > 1:
-        dist.all_reduce(mv_t)
-    tiered = {"value": round(total_bytes / (t_ms / tiered_steps / 1e3) / 1e9, 2), "unit": "GB/s",
-              "steps": tiered_steps, "ms_per_step": round(t_ms / tiered_steps, 1),
-              "d2h_tier_bytes_per_step": int(mv_t.item()), "h2d_bytes_per_step": int(h2d),
-              "d2h_bytes_per_step": int(d2h) + int(mv_t.item()),
-              "note": "e2e plus the PCIe leg of the placement: every context placed in the CPU or SSD tier "
-                      "(snapshot tier > 0) is copied HBM -> pinned DRAM by kvt_tier_moves on the stream that "
-                      "compressed it; the SSD file write is measured separately (tier_move.ssd)"}
+    tiered_steps = min(args.steps, args.tiered_steps)
+    tiered = None
+    if tiered_steps > 0:
+        staging = StagingRing(eng.abi, max(kv_bytes, int(codec._out[0][0].numel())), slots=2)
+        t_ms, (_, _, _, moved, _, snap_t) = timed(lambda: run_steps(tiered_steps, True, True, tiered=True))
+        staging.close()
+        mv_t = torch.tensor([moved], dtype=torch.int64, device="cpu" if args.ranks_share_gpu else "cuda")
+        if world > 1:
+            dist.all_reduce(mv_t)
+        tiered = {"value": round(total_bytes / (t_ms / tiered_steps / 1e3) / 1e9, 2), "unit": "GB/s",
+                  "steps": tiered_steps, "ms_per_step": round(t_ms / tiered_steps, 1),
+                  "d2h_tier_bytes_per_step": int(mv_t.item()), "h2d_bytes_per_step": int(h2d),
+                  "d2h_bytes_per_step": int(d2h) + int(mv_t.item()),
+                  "note": "e2e plus the PCIe leg of the placement: every context placed in the CPU or SSD tier "
+                          "(snapshot tier > 0) is copied HBM -> pinned DRAM by kvt_tier_moves on the stream that "
+                          "compressed it; the SSD file write is measured separately (tier_move.ssd)"}
 
     # ---- per-phase shares + roofline of the dominant kernel (one instrumented pass)
     roof = tier_move = cpu = None
@@ -639,6 +666,9 @@ def run_b200(args):
                                     my_lo, my_hi)
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_reference_sample(W, seconds=args.cpu_seconds)
+    n1 = None
+    if rank == 0 and world == 1 and args.n1 and args.config != "c5":
+        n1 = north_star_pass(args)
 
     if rank == 0:
         clocks = clk.summary()
@@ -673,6 +703,8 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "clocks": clocks,
         }
+        if n1 is not None:
+            line["n1_pass"] = n1
         if world > 1:
             line["nccl"] = nccl_summary(nccl_log + "*") if nccl_log else None
         print(json.dumps(line), flush=True)
@@ -943,7 +975,10 @@ def main():
     ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
     ap.add_argument("--snap-sms", type=int, default=64,
                     help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS)")
-    ap.add_argument("--tiered-steps", type=int, default=2, help="steps of the e2e_tiered leg (PCIe-bound)")
+    ap.add_argument("--tiered-steps", type=int, default=2, help="steps of the e2e_tiered leg (PCIe-bound); 0 = skip")
+    ap.add_argument("--no-n1", dest="n1", action="store_false",
+                    help="skip the north-star pass (c5: 1,000,008 chunk-configs) reported beside the headline line")
+    ap.add_argument("--n1-steps", type=int, default=2)
     ap.add_argument("--ranks-share-gpu", action="store_true",
                     help="test mode for 1-GPU boxes: every rank on cuda:0, profile exchange over gloo (host "
                          "buffers); exercises the N > 1 step logic without NCCL. Not a scaling measurement.")
