@@ -471,6 +471,7 @@ constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) 
 // scratch slot per SM (TPC = 16, E [128 rows][2048 tokens] = 256 KB per CTA,
 // one CTA per SM) and vote on the CUDA cores.
 constexpr int kSnapTpcSmem = 8, kSnapTpcGlobal = 16;
+constexpr int kVotePad = 8;  // vote array padding either side (>= pool / 2)
 constexpr int kSnapAcc = 3;  // TMEM logit accumulators (128 columns each): producers run up to 3 tiles ahead
 constexpr int kSnapESlots = 256;  // >= %nsmid on B200
 constexpr int64_t kSnapESlotBytes = 128LL * kSnapTpcGlobal * 128;
@@ -488,16 +489,16 @@ struct SnapSmemT {
   union {
     int32_t mb[TPC * 4][128];             // per (block, row) shift M
     uint8_t btile[TPC][2048];             // after the block weights: the vote MMA's B operand
-    unsigned long long vote[TPC * 128];   // after the vote MMA: per-token votes
+    unsigned long long vote[TPC * 128 + 2 * kVotePad];  // after the vote MMA: per-token votes at kVotePad + t, halos either side
   };
   // per (block, row) sum of E (<= 4096); the CUDA-core vote (EG) then keeps
   // the block weight (< 2^30) here, the tensor-core vote writes it into btile
   typename std::conditional<EG, uint32_t, uint16_t>::type lb[TPC * 4][128];
-  unsigned long long lglob[128];  // row sums, summed in by every CTA (red.async.add)
-  int32_t mglob[128];             // row shifts, max-ed in by every CTA (red.async.max)
+  alignas(16) unsigned long long lglob[128];  // row sums, summed in by every CTA (red.async.add); then the row weights
+  alignas(16) int32_t mglob[128];             // row shifts, max-ed in by every CTA (red.async.max)
   unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
   float sig[128];
-  float tau[4];  // per-tile scale, ring over the CTA's tile count
+  float tau[kSnapAcc];  // per-tile scale of the tile in each accumulator
   uint32_t amax[kSnapProd];
   uint64_t full, qbar, tfull[kSnapAcc], tempty[kSnapAcc], vbar;
   uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
@@ -516,15 +517,22 @@ constexpr float kE0 = 0x1.ffec2ep+6f, kE1 = 0x1.683ef2p+6f, kE2 = 0x1.f22ab4p+4f
 constexpr int kSnapLsh = 24;             // block sums scaled by 2^24 in the row sum
 constexpr float kSnapVoteScale = 0x1p-37f;  // vote = 2^37 x sum of probabilities
 
+// The epilogue works on X = 0x4B400000 + I (the int32 logit plus a bias):
+// read as fp32 that is exactly 12582912 + I.
+constexpr uint32_t kSnapBias = 0x4B400000u;
+
 // Two E values: x = 12582912 + I (exact), d = fma(x, a, c) = rint-exact
 // I * a - M; E = round(2^7 * 2^max(d, -16)) (oracle snap_exp_u8), packed
 // fp32x2 ops (each lane rounds like the scalar op). Returns the raw
-// float-as-int words 0x4B000000 + E, E <= 128.
-__device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a, float c, uint32_t& u0,
+// float-as-int words 0x4B000000 + E, E <= 128. kClamp = false when every d
+// of the block is >= -120: then n = rint(d) >= -120 keeps the exponent add
+// in range and E (0 for any d < -9) equals the clamped value bit for bit.
+template <bool kClamp>
+__device__ __forceinline__ void snap_exp_pair(uint32_t x0, uint32_t x1, float a, float c, uint32_t& u0,
                                               uint32_t& u1) {
-  const float2 x = make_float2(__uint_as_float(i0 + 0x4B400000u), __uint_as_float(i1 + 0x4B400000u));
+  const float2 x = make_float2(__uint_as_float(x0), __uint_as_float(x1));
   const float2 d = __ffma2_rn(x, make_float2(a, a), make_float2(c, c));
-  const float2 dc = make_float2(fmaxf(d.x, -16.0f), fmaxf(d.y, -16.0f));
+  const float2 dc = kClamp ? make_float2(fmaxf(d.x, -16.0f), fmaxf(d.y, -16.0f)) : d;
   const float2 t = __fadd2_rn(dc, make_float2(12582912.0f, 12582912.0f));
   const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(dc, make_float2(-n.x, -n.y));
@@ -537,23 +545,36 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t i0, uint32_t i1, float a,
   u1 = __float_as_uint(r.y);
 }
 
-// One (row, 32-token block) of the epilogue: block shift M, the 32 E bytes
-// packed 4 per word (token order), returns the block sum L. Ragged blocks
-// mask tokens >= nv (E = 0).
+// One (row, 32-token block), phase 1: block shift M = ceil(max I * a), the
+// fma offset c, and whether the block's smallest d is >= -120 (no clamp
+// needed). Ragged blocks only look at tokens < nv.
 template <bool kRagged>
-__device__ __forceinline__ uint32_t snap_block(uint32_t (&I)[32], int nv, float a, int32_t& M, uint32_t (&pk)[8]) {
-  int32_t m = INT_MIN;
+__device__ __forceinline__ void snap_block_stats(const uint32_t (&X)[32], int nv, float a, int32_t& M, float& c,
+                                                 bool& noclamp) {
+  uint32_t mx = 0, mn = 0xffffffffu;
 #pragma unroll
   for (int i = 0; i < 32; ++i)
-    if (!kRagged || i < nv) m = max(m, static_cast<int32_t>(I[i]));
-  M = static_cast<int32_t>(ceilf(__fmul_rn(__int2float_rn(m), a)));
-  const float c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
+    if (!kRagged || i < nv) {
+      mx = max(mx, X[i]);
+      mn = min(mn, X[i]);
+    }
+  // X - 12582912 is exact (both in [2^23, 2^24)): the int32 max I as fp32
+  M = static_cast<int32_t>(ceilf(__fmul_rn(__fsub_rn(__uint_as_float(mx), 12582912.0f), a)));
+  c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
+  noclamp = __fmaf_rn(__uint_as_float(mn), a, c) >= -120.0f;
+}
+
+// Phase 2: the 32 E bytes packed 4 per word (token order); returns the
+// block sum L. Ragged blocks mask tokens >= nv (E = 0).
+template <bool kRagged, bool kClamp>
+__device__ __forceinline__ uint32_t snap_block_e(const uint32_t (&X)[32], int nv, float a, float c,
+                                                 uint32_t (&pk)[8]) {
   uint32_t L = 0;
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
     uint32_t u[4];
-    snap_exp_pair(I[i], I[i + 1], a, c, u[0], u[1]);
-    snap_exp_pair(I[i + 2], I[i + 3], a, c, u[2], u[3]);
+    snap_exp_pair<kClamp>(X[i], X[i + 1], a, c, u[0], u[1]);
+    snap_exp_pair<kClamp>(X[i + 2], X[i + 3], a, c, u[2], u[3]);
     if (kRagged) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -641,6 +662,30 @@ __device__ __forceinline__ unsigned long long div_2p61(unsigned long long d) {
   return static_cast<unsigned long long>(q0);
 }
 
+#ifdef KVT_SNAP_TRACE
+// Timeline probe (profiles/snap_trace.py; never in the product build): the
+// first cluster's rank-0 CTA stamps %globaltimer at the pipeline events.
+__device__ unsigned long long g_snap_trace[4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SNAP_TR(cond, idx) \
+  do {                       \
+    if ((cond) && blockIdx.y == 0 && rank == 0 && (idx) < 4096) g_snap_trace[(idx)] = gtimer(); \
+  } while (0)
+__device__ int g_snap_dbg;  // bit 0: force the clamped E path
+extern "C" int kvt_debug_snap_set(int v) { return cudaMemcpyToSymbol(g_snap_dbg, &v, sizeof v) == cudaSuccess ? 0 : -1; }
+#define SNAP_DBG(bit) (g_snap_dbg & (bit))
+extern "C" int kvt_debug_snap_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_snap_trace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define SNAP_TR(cond, idx) do {} while (0)
+#define SNAP_DBG(bit) 0
+#endif
+
 template <int TPC, bool EG>
 __global__ void __launch_bounds__(kSnapThreads, 1)
     k_snapkv_tc(const uint4* __restrict__ K, const uint8_t* __restrict__ qbuf, uint8_t* __restrict__ escr,
@@ -674,7 +719,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       mbar_init(&sm.tfull[i], 2);  // tcgen05.commit + the issuing producer thread (orders sm.tau)
       mbar_init(&sm.tempty[i], kSnapCons);
     }
-    mbar_init(&sm.vbar, 1);
+    mbar_init(&sm.vbar, TPC);  // one commit per tile's vote-MMA issuer
     for (int i = 0; i < 3; ++i) mbar_init(&sm.rb[i], 1);
     mbar_fence_init();
   }
@@ -691,6 +736,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   cluster_sync_smem();  // every CTA's round barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  SNAP_TR(tid == 0, 4000);
 
   // Persistent clusters: this cluster's slices are blockIdx.y, + gridDim.y, ...
   // The producers run ahead into the next slice (Q8 + first tiles into TMEM)
@@ -722,6 +768,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const int g = g0 + j, buf = g % kSnapAcc;
         const int rows = min(128, n_loc - j * 128);
         mbar_wait(&sm.full, g & 1);
+        SNAP_TR(ptid == 0, it * 64 + j * 2);
         uint4 v[kRowsPT][4];
 #pragma unroll
         for (int i = 0; i < kRowsPT; ++i) {
@@ -767,7 +814,6 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         } else if (g >= 1) {
           mbar_wait(&sm.tfull[(g - 1) % kSnapAcc], ((g - 1) / kSnapAcc) & 1);  // MMA of tile g - 1 done reading k8
         }
-        if (ptid == 0) sm.tau[g & 3] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;  // tile g - 4 long consumed
         uint8_t* k8 = sm.k8[SnapSmem::KB == 2 ? (g & 1) : 0];
 #pragma unroll
         for (int i = 0; i < kRowsPT; ++i) {
@@ -797,13 +843,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         named_bar_sync(1, kSnapProd * 32);
         if (ptid == 0) {
           if (j == 0) mbar_wait(&sm.qbar, it & 1);  // this slice's Q8 tile landed
-          if (g >= kSnapAcc) mbar_wait(&sm.tempty[buf], ((g / kSnapAcc) - 1) & 1);  // consumers drained acc[buf]
+          if (g >= kSnapAcc) mbar_wait(&sm.tempty[buf], ((g / kSnapAcc) - 1) & 1);  // consumers drained acc[buf] (and read its tau)
+          sm.tau[buf] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;
           tc_fence_after();
           mbar_arrive(&sm.tfull[buf]);  // release: sm.tau visible to the consumers
           const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
+          for (int ks = 0; ks < 4; ++ks)
+            umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
           umma_commit(&sm.tfull[buf]);
+          SNAP_TR(true, it * 64 + j * 2 + 1);
         }
       }
     }
@@ -815,46 +864,67 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     const int r = quad * 32 + lane;
     const int crow = (ctid >> 2) & 127, cq = ctid & 3;  // tail: 4 threads per row, blocks split 4 ways
     constexpr int kCT = kSnapCons * 32;
+    const uint32_t t_warp = tmem + (uint32_t(quad * 32) << 16) + cb * 32;  // this warp's 32 lanes x 32 columns
+    const uint32_t e_row = smem_u32(sm.e) + (r >> 3) * 1024 + (r & 7) * 128;  // chunks 2cb, 2cb + 1 of row r
+    const uint32_t e_o0 = e_row + (((2 * cb) ^ (r & 7)) << 4);  // chunk 2cb + 1 is at e_o0 ^ 16
+    int buf = 0;  // accumulator ring position over this CTA's tiles (across slices)
+    uint32_t ph = 0;
     for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
-      const int g0 = it * ntl;
       // the producers wait for this slice's Q8 before its first MMA, so sig is
       // in place once tile g0's accumulator is (ntl == 0: the tail reads no sig)
       float sig_r = 0.0f;
       for (int j = 0; j < ntl; ++j) {
-        const int g = g0 + j, buf = g % kSnapAcc;
-        mbar_wait(&sm.tfull[buf], (g / kSnapAcc) & 1);
+        mbar_wait(&sm.tfull[buf], ph);
+        SNAP_TR(ctid == 0, it * 64 + 16 + j * 2);
         tc_fence_after();
         if (j == 0) sig_r = sm.sig[r];
-        uint32_t I[32];
-        tmem_ld32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + cb * 32, I);
-        const float tau = sm.tau[g & 3];
+        uint32_t X[32];
+        const uint32_t ta = t_warp + buf * 128;
+        tmem_ld32(ta, X);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) X[i] += kSnapBias;  // X = 0x4B400000 + I: as fp32, 12582912 + I exactly
+        const float tau = sm.tau[buf];
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile g + kSnapAcc may overwrite it
+        if (++buf == kSnapAcc) {
+          buf = 0;
+          ph ^= 1u;
+        }
         const int tok0 = j * 128 + cb * 32, nv = max(0, min(32, n_loc - tok0));
         int32_t M = INT_MIN;
         uint32_t L = 0;
-        uint32_t pk[8];
-        if (r < R && nv > 0) {
+        uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (nv > 0) {  // warp-uniform (one 32-token block per warp)
           const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
-          L = nv == 32 ? snap_block<false>(I, nv, a, M, pk) : snap_block<true>(I, nv, a, M, pk);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) pk[i] = 0;
+          float c;
+          bool nc;
+          int32_t Mb;
+          if (nv == 32) snap_block_stats<false>(X, nv, a, Mb, c, nc);
+          else snap_block_stats<true>(X, nv, a, Mb, c, nc);
+          const bool act = r < R;
+          const bool fast = __all_sync(0xffffffffu, nc || !act) && !SNAP_DBG(1);
+          if (act) {
+            M = Mb;
+            if (nv < 32) L = snap_block_e<true, true>(X, nv, a, c, pk);
+            else if (fast) L = snap_block_e<false, false>(X, nv, a, c, pk);
+            else L = snap_block_e<false, true>(X, nv, a, c, pk);
+          }
         }
         if (EG) {
           uint4* erow = reinterpret_cast<uint4*>(Eg + r * (TPC * 128) + tok0);
           __stcg(erow, make_uint4(pk[0], pk[1], pk[2], pk[3]));
           __stcg(erow + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]));
         } else {  // chunks 2cb, 2cb + 1 of row r in tile j (swizzled by r % 8)
-          uint8_t* et = sm.e + j * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
-          *reinterpret_cast<uint4*>(et + (((2 * cb) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(et + (((2 * cb + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          sts128(e_o0 + j * 16384, pk[0], pk[1], pk[2], pk[3]);
+          sts128((e_o0 ^ 16u) + j * 16384, pk[4], pk[5], pk[6], pk[7]);
         }
         sm.mb[j * 4 + cb][r] = M;
         sm.lb[j * 4 + cb][r] = L;
+        SNAP_TR(ctid == 0, it * 64 + 16 + j * 2 + 1);
       }
       named_bar_sync(2, kCT);  // every tile's E, mb, lb in place
+      SNAP_TR(ctid == 0, it * 64 + 32);
 
       // ---- row shift and sum across the cluster. Every CTA pushes its per-row
       // values into every CTA's mglob / lglob with red.async (max / add),
@@ -884,9 +954,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           }
       }
       round_wait(0);
+      SNAP_TR(ctid == 0, it * 64 + 33);
       int32_t mrow = sm.mglob[crow];
       mrow = __shfl_sync(0xffffffffu, mrow, lane & ~3);  // all four readers saw it before the reset
-      if (cq == 0) sm.mglob[crow] = INT_MIN;            // peers' next contributions come after round 2
+      // EG: reset now. Smem-E: the weight step still reads mglob (reset after
+      // it, before the halo push: peers' next contributions come after round 2)
+      if (EG && cq == 0) sm.mglob[crow] = INT_MIN;
       {
         unsigned long long Ls = 0;
         for (int b = cq; b < nblk; b += 4) {
@@ -903,51 +976,77 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           }
       }
       round_wait(1);
-      {
+      SNAP_TR(ctid == 0, it * 64 + 34);
+      if (EG) {
         unsigned long long Ls = sm.lglob[crow];
         Ls = __shfl_sync(0xffffffffu, Ls, lane & ~3);
         if (cq == 0) sm.lglob[crow] = 0;
         const unsigned long long wt = (crow < R && Ls) ? div_2p61(Ls) : 0ull;
-        if (EG) {
-          for (int b = cq; b < nblk; b += 4) {
-            const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
-            sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
-          }
-        } else {
-          // ---- votes on the tensor cores: B[n = block * 4 + limb][k = row] =
-          // byte `limb` of the row's block weight (K-major SW128, 16 x 128 per
-          // tile); D[token][n] = sum_r E[r][token] * B[n][r] (u8 x u8 -> s32,
-          // <= 128 * 128 * 255); a token's vote is its own block's four limbs.
-          // The weights go through registers: btile aliases mb, which the
-          // shifts still read
-          uint32_t w[TPC];
-#pragma unroll
-          for (int i = 0; i < TPC; ++i) {
-            const int b = cq + 4 * i;
-            const int64_t sh = b < nblk ? int64_t(mrow) - sm.mb[b][crow] : 64;
-            w[i] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
-          }
-          named_bar_sync(2, kCT);  // every shift read: mb is free for btile
-#pragma unroll
-          for (int i = 0; i < TPC; ++i) {
-            const int b = cq + 4 * i, j = b >> 2;
-            uint8_t* bt = sm.btile[j];
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-              const int n = (b & 3) * 4 + l;
-              bt[(n >> 3) * 1024 + (n & 7) * 128 + ((((crow >> 4) ^ (n & 7)) << 4) | (crow & 15))] =
-                  static_cast<uint8_t>(w[i] >> (8 * l));
-            }
-          }
-          fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        for (int b = cq; b < nblk; b += 4) {
+          const int64_t sh = int64_t(mrow) - sm.mb[b][crow];
+          sm.lb[b][crow] = sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;  // < 2^30
         }
+      } else {
+        // ---- votes on the tensor cores: B[n = block * 4 + limb][k = row] =
+        // byte `limb` of the row's block weight (K-major SW128, 16 x 128 per
+        // tile); D[token][n] = sum_r E[r][token] * B[n][r] (u8 x u8 -> s32,
+        // <= 128 * 128 * 255); a token's vote is its own block's four limbs.
+        // Row weights first (lglob: row sum -> weight, one thread per row);
+        // then each thread writes (block, 4 consecutive rows) items as one
+        // 32-bit word per limb. btile aliases mb: every shift is read into
+        // registers before any weight is stored.
+        if (cq == 0) {
+          const unsigned long long Ls = sm.lglob[crow];
+          sm.lglob[crow] = (crow < R && Ls) ? div_2p61(Ls) : 0ull;
+        }
+        named_bar_sync(2, kCT);  // row weights in lglob
+        constexpr int kItems = TPC * 4 * 32 / kCT;  // (block, row quad) items per thread
+        int4 mbq[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const int item = ctid + kCT * k, b = item >> 5, rq = item & 31;
+          mbq[k] = b < nblk ? *reinterpret_cast<const int4*>(&sm.mb[b][4 * rq]) : make_int4(INT_MIN, INT_MIN, INT_MIN, INT_MIN);
+        }
+        named_bar_sync(2, kCT);  // every shift read: mb is free for btile
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          const int item = ctid + kCT * k, b = item >> 5, rq = item & 31;
+          const int4 m4 = *reinterpret_cast<const int4*>(&sm.mglob[4 * rq]);
+          const ulonglong2 w01 = *reinterpret_cast<const ulonglong2*>(&sm.lglob[4 * rq]);
+          const ulonglong2 w23 = *reinterpret_cast<const ulonglong2*>(&sm.lglob[4 * rq + 2]);
+          auto wgt = [](int32_t m, int32_t mb, unsigned long long wt) -> uint32_t {
+            const int64_t sh = int64_t(m) - mb;  // mb = INT_MIN (no block): >= 64
+            return sh < 64 ? static_cast<uint32_t>(wt >> sh) : 0u;
+          };
+          const uint32_t w0 = wgt(m4.x, mbq[k].x, w01.x), w1 = wgt(m4.y, mbq[k].y, w01.y);
+          const uint32_t w2 = wgt(m4.z, mbq[k].z, w23.x), w3 = wgt(m4.w, mbq[k].w, w23.y);
+          const uint32_t lo01 = __byte_perm(w0, w1, 0x5140), hi01 = __byte_perm(w0, w1, 0x7362);
+          const uint32_t lo23 = __byte_perm(w2, w3, 0x5140), hi23 = __byte_perm(w2, w3, 0x7362);
+          const uint32_t limb[4] = {__byte_perm(lo01, lo23, 0x5410), __byte_perm(lo01, lo23, 0x7632),
+                                    __byte_perm(hi01, hi23, 0x5410), __byte_perm(hi01, hi23, 0x7632)};
+          uint8_t* bt = sm.btile[b >> 2];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const int n = (b & 3) * 4 + l;
+            *reinterpret_cast<uint32_t*>(bt + (n >> 3) * 1024 + (n & 7) * 128 + ((((rq >> 2) ^ (n & 7)) << 4) | ((4 * rq) & 15))) =
+                limb[l];
+          }
+        }
+        fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
       }
       named_bar_sync(2, kCT);  // block weights complete; mb dead (btile / vote reuse it)
+      SNAP_TR(ctid == 0, it * 64 + 35);
       if (!EG) {
-        if (ctid == 0) {
-          tc_fence_after();
-          constexpr uint32_t kVdesc = idesc_u8_amn(128, 16);
-          for (int j = 0; j < ntl; ++j) {
+        if (ctid < 128) {  // peers' next-slice contributions come after round 2 (our halo push)
+          sm.mglob[ctid] = INT_MIN;
+          sm.lglob[ctid] = 0;
+        }
+        // one issuing thread per tile (lane 0 of consumer warp j), each commits once
+        if (lane == 0 && cw < TPC) {
+          const int j = cw;
+          if (j < ntl) {
+            tc_fence_after();
+            constexpr uint32_t kVdesc = idesc_u8_amn(128, 16);
             const uint64_t da = umma_desc_sw128(sm.e + j * 16384), db = umma_desc_sw128(sm.btile[j]);
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)  // K = 32 rows per MMA: 4 atoms of 8 rows (A), 32 bytes (B)
@@ -956,6 +1055,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           umma_commit(&sm.vbar);
         }
         mbar_wait(&sm.vbar, it & 1);
+        SNAP_TR(ctid == 0, it * 64 + 36);
         tc_fence_after();
         for (int j = cb; j < ntl; j += 4) {  // warp (quad, cb): tiles cb, cb + 4; tokens 32 quad .. (block quad)
           uint32_t d[4];
@@ -964,7 +1064,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                                        (static_cast<unsigned long long>(d[1]) << 8) +
                                        (static_cast<unsigned long long>(d[2]) << 16) +
                                        (static_cast<unsigned long long>(d[3]) << 24);
-          sm.vote[j * 128 + quad * 32 + lane] = v;
+          sm.vote[kVotePad + j * 128 + quad * 32 + lane] = v;
         }
         tc_fence_before();
       } else {
@@ -991,13 +1091,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           }
           named_bar_sync(2, kCT);  // (round > 0) the previous round's weight reads are done
           if (rq == 1) {
-            sm.vote[2 * p] = a0;
-            sm.vote[2 * p + 1] = a1;
+            sm.vote[kVotePad + 2 * p] = a0;
+            sm.vote[kVotePad + 2 * p + 1] = a1;
           }
           named_bar_sync(2, kCT);
           if (rq == 0) {
-            sm.vote[2 * p] += a0;
-            sm.vote[2 * p + 1] += a1;
+            sm.vote[kVotePad + 2 * p] += a0;
+            sm.vote[kVotePad + 2 * p + 1] += a1;
           }
         }
       }
@@ -1007,31 +1107,47 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       const int half = half_of(pool);
       if (ctid < half) {
         if (rank > 0 && ctid < n_loc)
-          st_async_u64(mapa_u32(&sm.rhalo[ctid], rank - 1), sm.vote[ctid], mapa_u32(&sm.rb[2], rank - 1));
+          st_async_u64(mapa_u32(&sm.rhalo[ctid], rank - 1), sm.vote[kVotePad + ctid], mapa_u32(&sm.rb[2], rank - 1));
         if (rank < C - 1)
-          st_async_u64(mapa_u32(&sm.lhalo[ctid], rank + 1), sm.vote[n_loc - half + ctid], mapa_u32(&sm.rb[2], rank + 1));
+          st_async_u64(mapa_u32(&sm.lhalo[ctid], rank + 1), sm.vote[kVotePad + n_loc - half + ctid],
+                       mapa_u32(&sm.rb[2], rank + 1));
       }
       round_wait(2);  // halos in place
-      // ---- pooling (max over +-pool/2 within the prefix) and scores
+      SNAP_TR(ctid == 0, it * 64 + 37);
+      // halos into the padded vote array: 0 (neutral: votes >= 0) outside the
+      // prefix and where the right neighbour has fewer tokens
+      if (ctid < half) {
+        const int n_right = min(half, max(0, min(P - (tile0 + tpc) * 128, tpc * 128)));
+        sm.vote[kVotePad - half + ctid] = rank > 0 ? sm.lhalo[ctid] : 0ull;
+        sm.vote[kVotePad + n_loc + ctid] = (rank < C - 1 && ctid < n_right) ? sm.rhalo[ctid] : 0ull;
+      }
+      named_bar_sync(2, kCT);
+      // ---- pooling (max over +-pool/2 within the prefix), two tokens per
+      // thread and pass, and scores
       float* out = scores + static_cast<size_t>(slice) * T;
-      for (int tl = ctid; tl < n_loc; tl += kCT) {
-        unsigned long long m = 0;
-        for (int dj = -half; dj <= half; ++dj) {
-          const int tg = t_lo + tl + dj;  // global prefix token
-          if (tg < 0 || tg >= P) continue;
-          const int li = tl + dj;
-          const unsigned long long x = li < 0 ? sm.lhalo[li + half] : (li >= n_loc ? sm.rhalo[li - n_loc] : sm.vote[li]);
-          m = x > m ? x : m;
+      for (int tl = 2 * ctid; tl < n_loc; tl += 2 * kCT) {
+        const unsigned long long* vp = sm.vote + kVotePad + tl;
+        unsigned long long m0 = vp[-half], m1 = 0;
+        for (int dj = 1 - half; dj <= half; ++dj) {
+          const unsigned long long x = vp[dj];
+          m0 = x > m0 ? x : m0;
+          m1 = x > m1 ? x : m1;
         }
-        out[t_lo + tl] = __fmul_rn(__ull2float_rn(m), kSnapVoteScale);  // 2^-37 (exact)
+        const unsigned long long x = vp[half + 1];
+        m1 = x > m1 ? x : m1;
+        out[t_lo + tl] = __fmul_rn(__ull2float_rn(m0), kSnapVoteScale);  // 2^-37 (exact)
+        if (tl + 1 < n_loc) out[t_lo + tl + 1] = __fmul_rn(__ull2float_rn(m1), kSnapVoteScale);
       }
       if (rank == C - 1)
         for (int t = P + ctid; t < T; t += kCT) out[t] = INFINITY;  // window tokens always kept
       named_bar_sync(2, kCT);  // vote / halos / E / mb / lb free for the next slice
+      SNAP_TR(ctid == 0, it * 64 + 38);
     }
   }
   // Peers' remote arrives and DSMEM reads of this CTA's smem are all done
   // once every CTA's consumers are past their last round.
+  SNAP_TR(tid == 0, 4001);
+  SNAP_TR(tid == kSnapProd * 32, 4002);
   tc_fence_before();
   cluster_sync_smem();
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
