@@ -356,10 +356,10 @@ static void keydiff_slice(void* a, int64_t sl) {
   free(inv);
 }
 
-/* snapkv, exact-integer formulation v3.
+/* snapkv, exact-integer formulation v4.
  * Window queries quantised to int8 per row, prefix keys to int8 per
- * 128-token tile, so every logit is an exact int8 dot product I_rt times
- * a per-(tile, row) fp32 factor a_jr (log2 units). Softmax over the prefix
+ * 16-token group, so every logit is an exact int8 dot product I_rt times
+ * a per-(group, row) fp32 factor a (log2 units). Softmax over the prefix
  * per query row uses a per-(row, 32-token block) integer shift M_br =
  * ceil(max_block y): E_rt = round(2^7 * 2^(y_rt - M_br)), an 8-bit value,
  * by a fixed degree-2 fp32 FMA polynomial; the row sum and the vote weights
@@ -375,7 +375,7 @@ static void keydiff_slice(void* a, int64_t sl) {
 #define SNAP_LSH 24                   /* block sums scaled by 2^24 in the row sum */
 #define SNAP_VOTE_SCALE 0x1p-37f      /* vote = 2^37 x sum of probabilities */
 #define SNAP_BLK 32   /* tokens per softmax shift block */
-#define SNAP_TILE 128 /* tokens per K quantisation tile */
+#define SNAP_KGRP 16  /* tokens per K int8 scale (spec v4) */
 
 static uint32_t f2u(float f) {
   uint32_t u;
@@ -432,7 +432,7 @@ static void snapkv_slice(void* a, int64_t sl) {
   float* out = J->scores + (size_t)sl * T;
   for (int t = P > 0 ? P : 0; t < T; ++t) out[t] = INFINITY; /* window always kept */
   if (P <= 0) return;
-  const int ntiles = (P + SNAP_TILE - 1) / SNAP_TILE, nblk = (P + SNAP_BLK - 1) / SNAP_BLK;
+  const int ngrp = (P + SNAP_KGRP - 1) / SNAP_KGRP, nblk = (P + SNAP_BLK - 1) / SNAP_BLK;
   int8_t* q8 = (int8_t*)malloc((size_t)R * D_HEAD);
   float* sig = (float*)malloc(sizeof(float) * (size_t)R);
   float row[D_HEAD];
@@ -442,12 +442,12 @@ static void snapkv_slice(void* a, int64_t sl) {
       for (int d = 0; d < D_HEAD; ++d) row[d] = bf2f(window_q(s, c, J->q, l, h * G + g, w, d));
       sig[r] = quant_i8(row, D_HEAD, q8 + (size_t)r * D_HEAD);
     }
-  /* K: one int8 scale per 128-token tile of the prefix */
+  /* K: one int8 scale per 16-token group of the prefix (v4) */
   int8_t* k8 = (int8_t*)malloc((size_t)P * D_HEAD);
-  float* tau = (float*)malloc(sizeof(float) * (size_t)ntiles);
-  float* tile = (float*)malloc(sizeof(float) * SNAP_TILE * D_HEAD);
-  for (int j = 0; j < ntiles; ++j) {
-    const int t0 = j * SNAP_TILE, n = (P - t0 < SNAP_TILE ? P - t0 : SNAP_TILE);
+  float* tau = (float*)malloc(sizeof(float) * (size_t)ngrp);
+  float* tile = (float*)malloc(sizeof(float) * SNAP_KGRP * D_HEAD);
+  for (int j = 0; j < ngrp; ++j) {
+    const int t0 = j * SNAP_KGRP, n = (P - t0 < SNAP_KGRP ? P - t0 : SNAP_KGRP);
     for (int i = 0; i < n * D_HEAD; ++i) tile[i] = bf2f(K[(size_t)t0 * D_HEAD + i]);
     tau[j] = quant_i8(tile, n * D_HEAD, k8 + (size_t)t0 * D_HEAD);
   }
@@ -460,24 +460,26 @@ static void snapkv_slice(void* a, int64_t sl) {
     const int8_t* qr = q8 + (size_t)r * D_HEAD;
     for (int b = 0; b < nblk; ++b) {
       const int t0 = b * SNAP_BLK, n = (P - t0 < SNAP_BLK ? P - t0 : SNAP_BLK);
-      int32_t mx = INT32_MIN;
+      /* log2 units per unit of I for each token's 16-group, low 2 mantissa
+       * bits cleared: then 12582912 * a and -M - 12582912 * a are exact, and
+       * the fma below is the single correctly rounded value of I * a - M */
+      float a_t[SNAP_BLK];
+      float ymax = -INFINITY;
       for (int i = 0; i < n; ++i) {
         int32_t acc = 0;
         const int8_t* kt = k8 + (size_t)(t0 + i) * D_HEAD;
         for (int d = 0; d < D_HEAD; ++d) acc += (int32_t)qr[d] * (int32_t)kt[d];
         I[i] = acc;
-        mx = acc > mx ? acc : mx;
+        a_t[i] = u2f(f2u((tau[(t0 + i) / SNAP_KGRP] * sig[r]) * SNAP_C0) & ~3u);
+        const float y = (float)acc * a_t[i];
+        ymax = y > ymax ? y : ymax;
       }
-      /* log2 units per unit of I, low 2 mantissa bits cleared: then
-       * 12582912 * a_jr and -M - 12582912 * a_jr are exact, and the fma
-       * below is the single correctly rounded value of I * a_jr - M */
-      const float a_jr = u2f(f2u((tau[t0 / SNAP_TILE] * sig[r]) * SNAP_C0) & ~3u);
-      const int32_t M = (int32_t)ceilf((float)mx * a_jr);
-      const float cb = (float)(-M) - 12582912.0f * a_jr;
+      const int32_t M = (int32_t)ceilf(ymax); /* ceil of the block's largest fl(I a) */
       uint32_t L = 0;
       for (int i = 0; i < n; ++i) {
         const float X = u2f((uint32_t)(I[i] + 0x4B400000));
-        const uint32_t e = snap_exp_u8(fmaf(X, a_jr, cb));
+        const float cb = (float)(-M) - 12582912.0f * a_t[i];
+        const uint32_t e = snap_exp_u8(fmaf(X, a_t[i], cb));
         E[(size_t)r * P + t0 + i] = (uint8_t)e;
         L += e;
       }

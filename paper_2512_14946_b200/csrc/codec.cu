@@ -459,9 +459,11 @@ static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKd
 // block's four limbs recombined; boundary votes go to the neighbours by
 // st.async; pooling.
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
-constexpr int kSnapProd = 8;           // producer warps: K tile absmax + int8 quantisation + MMA issue
+constexpr int kSnapProd = 8;           // quantiser warps: 16 tokens of every K tile each (own bulk copy, absmax, int8)
 constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
-constexpr int kSnapThreads = (kSnapProd + kSnapCons) * 32;
+constexpr int kSnapCtl = kSnapProd + kSnapCons;  // control warp: Q8 loads, logit MMA issue
+constexpr int kSnapThreads = (kSnapCtl + 1) * 32;
+constexpr int kSnapKGrp = 16;          // tokens per K int8 scale (spec v4)
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
 constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
 // Two configurations of one kernel: prefixes up to 16 x 8 tiles (16384
@@ -481,7 +483,7 @@ struct SnapSmemT {
   static constexpr int KB = EG ? 2 : 1;  // k8 buffers (the smem-E configuration single-buffers to fit)
   uint8_t k8[KB][128 * 128];  // offset 0 of the 1024-aligned base
   uint8_t q8[128 * 128];
-  uint4 stage[128 * 16];     // one bf16 tile (32 KB), producers only
+  uint4 stage[128 * 16];     // one bf16 tile (32 KB): quantiser warp w's 16 rows at stage + 256 w
   // E (u8) of TPC tiles: tile j, row r, 16-token chunk c at
   // j * 16384 + (r / 8) * 1024 + (r % 8) * 128 + ((c ^ (r % 8)) * 16) —
   // the MN-major SW128 layout of the vote MMA's A operand (M = tokens, K = rows)
@@ -498,9 +500,10 @@ struct SnapSmemT {
   alignas(16) int32_t mglob[128];             // row shifts, max-ed in by every CTA (red.async.max)
   unsigned long long lhalo[8], rhalo[8];  // neighbours' boundary votes (pushed through DSMEM), pool <= 15
   float sig[128];
-  float tau[kSnapAcc];  // per-tile scale of the tile in each accumulator
-  uint32_t amax[kSnapProd];
-  uint64_t full, qbar, tfull[kSnapAcc], tempty[kSnapAcc], vbar;
+  alignas(128) uint32_t bias[1024];  // 4 KB of kSnapBias: the tcgen05.cp source that resets an accumulator
+  alignas(16) float tau[kSnapAcc][kSnapProd];  // K scales (per 16-token group) of the tile in each accumulator
+  alignas(16) float tau_st[2][kSnapProd];                   // quantisers' scales of tile g at [g & 1], copied by the control thread
+  uint64_t fullw[kSnapProd], kfull[2], qbar, tfull[kSnapAcc], tempty[kSnapAcc], vbar;
   uint64_t rb[3];  // tail rounds (row shifts, row sums, halos): local expect_tx + peers' complete_tx
   uint32_t tmem_base;
 };
@@ -517,8 +520,9 @@ constexpr float kE0 = 0x1.ffec2ep+6f, kE1 = 0x1.683ef2p+6f, kE2 = 0x1.f22ab4p+4f
 constexpr int kSnapLsh = 24;             // block sums scaled by 2^24 in the row sum
 constexpr float kSnapVoteScale = 0x1p-37f;  // vote = 2^37 x sum of probabilities
 
-// The epilogue works on X = 0x4B400000 + I (the int32 logit plus a bias):
-// read as fp32 that is exactly 12582912 + I.
+// The logit accumulators start at kSnapBias (tcgen05.cp before each tile's
+// MMAs), so TMEM holds X = 0x4B400000 + I: read as fp32 that is exactly
+// 12582912 + I.
 constexpr uint32_t kSnapBias = 0x4B400000u;
 
 // Two E values: x = 12582912 + I (exact), d = fma(x, a, c) = rint-exact
@@ -545,33 +549,48 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t x0, uint32_t x1, float a,
   u1 = __float_as_uint(r.y);
 }
 
-// One (row, 32-token block), phase 1: block shift M = ceil(max I * a), the
-// fma offset c, and whether the block's smallest d is >= -120 (no clamp
-// needed). Ragged blocks only look at tokens < nv.
+// One (row, 32-token block), phase 1. Tokens 0-15 and 16-31 are two K
+// scale groups (a0, a1): block shift M = ceil(max over tokens of fl(I * a))
+// (per group fl(max I * a): fl is monotone), the fma offsets c0, c1, and
+// whether the block's smallest d is >= -120 (no clamp needed). Ragged blocks
+// only look at tokens < nv.
 template <bool kRagged>
-__device__ __forceinline__ void snap_block_stats(const uint32_t (&X)[32], int nv, float a, int32_t& M, float& c,
-                                                 bool& noclamp) {
-  uint32_t mx = 0, mn = 0xffffffffu;
+__device__ __forceinline__ void snap_block_stats(const uint32_t (&X)[32], int nv, float a0, float a1, int32_t& M,
+                                                 float& c0, float& c1, bool& noclamp) {
+  uint32_t mx0 = 0, mn0 = 0xffffffffu, mx1 = 0, mn1 = 0xffffffffu;
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < 16; ++i)
     if (!kRagged || i < nv) {
-      mx = max(mx, X[i]);
-      mn = min(mn, X[i]);
+      mx0 = max(mx0, X[i]);
+      mn0 = min(mn0, X[i]);
     }
+#pragma unroll
+  for (int i = 16; i < 32; ++i)
+    if (!kRagged || i < nv) {
+      mx1 = max(mx1, X[i]);
+      mn1 = min(mn1, X[i]);
+    }
+  const bool h1 = !kRagged || nv > 16;  // the second group has tokens
   // X - 12582912 is exact (both in [2^23, 2^24)): the int32 max I as fp32
-  M = static_cast<int32_t>(ceilf(__fmul_rn(__fsub_rn(__uint_as_float(mx), 12582912.0f), a)));
-  c = __fsub_rn(__int2float_rn(-M), __fmul_rn(12582912.0f, a));
-  noclamp = __fmaf_rn(__uint_as_float(mn), a, c) >= -120.0f;
+  const float y0 = __fmul_rn(__fsub_rn(__uint_as_float(mx0), 12582912.0f), a0);
+  const float y1 = h1 ? __fmul_rn(__fsub_rn(__uint_as_float(mx1), 12582912.0f), a1) : -INFINITY;
+  M = static_cast<int32_t>(ceilf(fmaxf(y0, y1)));
+  const float fm = __int2float_rn(-M);
+  c0 = __fsub_rn(fm, __fmul_rn(12582912.0f, a0));
+  c1 = __fsub_rn(fm, __fmul_rn(12582912.0f, a1));
+  noclamp = __fmaf_rn(__uint_as_float(mn0), a0, c0) >= -120.0f &&
+            (!h1 || __fmaf_rn(__uint_as_float(mn1), a1, c1) >= -120.0f);
 }
 
 // Phase 2: the 32 E bytes packed 4 per word (token order); returns the
 // block sum L. Ragged blocks mask tokens >= nv (E = 0).
 template <bool kRagged, bool kClamp>
-__device__ __forceinline__ uint32_t snap_block_e(const uint32_t (&X)[32], int nv, float a, float c,
-                                                 uint32_t (&pk)[8]) {
+__device__ __forceinline__ uint32_t snap_block_e(const uint32_t (&X)[32], int nv, float a0, float a1, float c0,
+                                                 float c1, uint32_t (&pk)[8]) {
   uint32_t L = 0;
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
+    const float a = i < 16 ? a0 : a1, c = i < 16 ? c0 : c1;
     uint32_t u[4];
     snap_exp_pair<kClamp>(X[i], X[i + 1], a, c, u[0], u[1]);
     snap_exp_pair<kClamp>(X[i + 2], X[i + 3], a, c, u[2], u[3]);
@@ -713,10 +732,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   }
 
   if (tid == 0) {
-    mbar_init(&sm.full, 1);
+    for (int i = 0; i < kSnapProd; ++i) mbar_init(&sm.fullw[i], 1);
+    mbar_init(&sm.kfull[0], kSnapProd);  // every quantiser warp's rows of tile g in k8 (+ its scale)
+    mbar_init(&sm.kfull[1], kSnapProd);
     mbar_init(&sm.qbar, 1);
     for (int i = 0; i < kSnapAcc; ++i) {
-      mbar_init(&sm.tfull[i], 2);  // tcgen05.commit + the issuing producer thread (orders sm.tau)
+      mbar_init(&sm.tfull[i], 2);  // tcgen05.commit + the control thread's arrive (orders sm.tau)
       mbar_init(&sm.tempty[i], kSnapCons);
     }
     mbar_init(&sm.vbar, TPC);  // one commit per tile's vote-MMA issuer
@@ -727,6 +748,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     sm.mglob[tid] = INT_MIN;
     sm.lglob[tid] = 0;
   }
+  for (int i = tid; i < 1024; i += kSnapThreads) sm.bias[i] = kSnapBias;
+  fence_async_smem();  // read by tcgen05.cp (async proxy)
   // kSnapAcc x 128 logit columns, then (smem-E configuration) the vote MMA's TPC x 16
   constexpr uint32_t kTmemCols = 512;
   constexpr uint32_t kVoteCol = kSnapAcc * 128;
@@ -743,120 +766,109 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
   // while the consumers do this slice's tail; mbarrier phases run on across
   // slices (g = this CTA's tile count, it = its slice count).
   if (warp < kSnapProd) {
-    // ================= producers: absmax, int8 quantisation, MMA issue
-    constexpr uint32_t kIdesc = idesc_i8(128, 128);
-    constexpr int kRowsPT = 128 * 4 / (kSnapProd * 32);  // rows per producer thread
-    const int ptid = tid;  // rows ptid/4 + (kSnapProd * 8) * i, 32-channel quarter ptid & 3
-    const int q4 = ptid & 3, rbase = ptid >> 2;
-    for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
-      const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
-      const int g0 = it * ntl;
-      if (ptid == 0 && ntl > 0) {
-        // q8 / sig are free once the previous slice's last MMA has completed
-        if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) % kSnapAcc], ((g0 - 1) / kSnapAcc) & 1);
-        mbar_expect_tx(&sm.qbar, kSnapQBytes);
-        bulk_g2s_hint(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar,
-                      l2_evict_last());  // the Q8 tiles serve every chunk
-        bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
-        const int rows = min(128, n_loc);
-        fence_async_smem();
-        mbar_expect_tx(&sm.full, rows * 256);
-        bulk_g2s_hint(sm.stage, Ks, rows * 256, &sm.full, l2_evict_first());  // K is read once
-        if (ntl > 1) bulk_prefetch_l2(Ks + 128 * 16, min(128, n_loc - 128) * 256);  // tile 1 on its way to L2
+    // ================= quantiser warps: warp w owns tokens 16w .. 16w + 15 of
+    // every tile: its own bulk copy into its 4 KB stage slot (issued one tile
+    // ahead), absmax, int8 quantisation into k8, arrive on kfull. No barrier
+    // between the quantiser warps.
+    const int w = warp, sub = lane >> 4, ch = lane & 15;  // load i: row 2i + sub, 16-byte chunk ch
+    uint4* slot = sm.stage + w * 256;
+    const uint64_t pol = l2_evict_first();  // K is read once
+    uint32_t nld = 0;                       // bulk copies issued into the slot (its full barrier's phase)
+    auto rows_of = [&](int jj) { return max(0, min(kSnapKGrp, n_loc - jj * 128 - kSnapKGrp * w)); };
+    auto src_of = [&](int sl, int jj) {
+      return K + (static_cast<size_t>(sl) * T + t_lo + jj * 128 + kSnapKGrp * w) * 16;
+    };
+    auto load = [&](int sl, int jj) {
+      const int rw = rows_of(jj);
+      if (lane == 0 && rw > 0) {
+        fence_async_smem();  // the slot's previous contents were read by this warp (generic proxy)
+        mbar_expect_tx(&sm.fullw[w], rw * 256);
+        bulk_g2s_hint(slot, src_of(sl, jj), rw * 256, &sm.fullw[w], pol);
       }
+    };
+    // (slice, tile) after (sl, jj) in this CTA's order
+    auto next_of = [&](int& sl, int& jj) {
+      if (++jj >= ntl) {
+        jj = 0;
+        sl += static_cast<int>(gridDim.y);
+      }
+    };
+    if (ntl > 0 && static_cast<int>(blockIdx.y) < nslice) {
+      load(blockIdx.y, 0);
+      int sp = blockIdx.y, jp = 0;
+      next_of(sp, jp);
+      if (sp < nslice && lane == 0 && rows_of(jp) > 0) bulk_prefetch_l2(src_of(sp, jp), rows_of(jp) * 256);
+    }
+    for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
+      const int g0 = it * ntl;
       for (int j = 0; j < ntl; ++j) {
-        const int g = g0 + j, buf = g % kSnapAcc;
-        const int rows = min(128, n_loc - j * 128);
-        mbar_wait(&sm.full, g & 1);
-        SNAP_TR(ptid == 0, it * 64 + j * 2);
-        uint4 v[kRowsPT][4];
+        const int g = g0 + j;
+        const int rw = rows_of(j);
+        uint4 v[8];
+        if (rw > 0) {
+          mbar_wait(&sm.fullw[w], nld & 1);
+          ++nld;
+          SNAP_TR(w == 0 && lane == 0, it * 64 + j * 2);
 #pragma unroll
-        for (int i = 0; i < kRowsPT; ++i) {
-          const int row = rbase + kSnapProd * 8 * i;
+          for (int i = 0; i < 8; ++i) v[i] = 2 * i + sub < rw ? slot[(2 * i + sub) * 16 + ch] : make_uint4(0, 0, 0, 0);
+        } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) v[i][u] = row < rows ? sm.stage[row * 16 + q4 * 4 + u] : make_uint4(0, 0, 0, 0);
+          for (int i = 0; i < 8; ++i) v[i] = make_uint4(0, 0, 0, 0);
         }
         uint32_t mx2 = 0;
 #pragma unroll
-        for (int i = 0; i < kRowsPT; ++i)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            mx2 = __vmaxu2(mx2, v[i][u].x & 0x7fff7fffu);
-            mx2 = __vmaxu2(mx2, v[i][u].y & 0x7fff7fffu);
-            mx2 = __vmaxu2(mx2, v[i][u].z & 0x7fff7fffu);
-            mx2 = __vmaxu2(mx2, v[i][u].w & 0x7fff7fffu);
-          }
-        const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));
-        if (lane == 0) sm.amax[warp] = wmx;
-        named_bar_sync(1, kSnapProd * 32);  // stage consumed into registers, amax complete
-        if (ptid == 0 && j + 1 < ntl) {  // prefetch the next tile
-          const int nrows = min(128, n_loc - (j + 1) * 128);
-          fence_async_smem();
-          mbar_expect_tx(&sm.full, nrows * 256);
-          bulk_g2s_hint(sm.stage, Ks + static_cast<size_t>(j + 1) * 128 * 16, nrows * 256, &sm.full, l2_evict_first());
+        for (int i = 0; i < 8; ++i) {
+          mx2 = __vmaxu2(mx2, v[i].x & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i].y & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i].z & 0x7fff7fffu);
+          mx2 = __vmaxu2(mx2, v[i].w & 0x7fff7fffu);
         }
-        if (ptid == 0) {  // the tile after that into L2 (this slice's, or the next slice's first)
-          if (j + 2 < ntl) {
-            bulk_prefetch_l2(Ks + static_cast<size_t>(j + 2) * 128 * 16, min(128, n_loc - (j + 2) * 128) * 256);
-          } else if (j + 2 - ntl < ntl && slice + static_cast<int>(gridDim.y) < nslice) {
-            const int jn = j + 2 - ntl;
-            bulk_prefetch_l2(K + (static_cast<size_t>(slice + gridDim.y) * T + t_lo + jn * 128) * 16,
-                             min(128, n_loc - jn * 128) * 256);
+        const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));  // slot fully read
+        {  // the next tile's rows into the slot, the one after that into L2
+          int sn = slice, jn = j;
+          next_of(sn, jn);
+          if (sn < nslice) {
+            load(sn, jn);
+            int sp = sn, jp = jn;
+            next_of(sp, jp);
+            if (sp < nslice && lane == 0 && rows_of(jp) > 0) bulk_prefetch_l2(src_of(sp, jp), rows_of(jp) * 256);
           }
         }
-        uint32_t mx = 0;
-#pragma unroll
-        for (int w = 0; w < kSnapProd; ++w) mx = max(mx, sm.amax[w]);
-        const float Af = bf2f(mx);
+        const float Af = bf2f(wmx);
         const float inv = Af > 0.0f ? __fdiv_rn(127.0f, Af) : 0.0f;
         if (SnapSmem::KB == 2) {
           if (g >= 2) mbar_wait(&sm.tfull[(g - 2) % kSnapAcc], ((g - 2) / kSnapAcc) & 1);  // MMA g - 2 done with k8[g & 1]
         } else if (g >= 1) {
           mbar_wait(&sm.tfull[(g - 1) % kSnapAcc], ((g - 1) / kSnapAcc) & 1);  // MMA of tile g - 1 done reading k8
         }
+        if (lane == 0) sm.tau_st[g & 1][w] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;  // slot g & 1 copied at MMA g - 2
         uint8_t* k8 = sm.k8[SnapSmem::KB == 2 ? (g & 1) : 0];
 #pragma unroll
-        for (int i = 0; i < kRowsPT; ++i) {
-          const int row = rbase + kSnapProd * 8 * i;
-          uint32_t wq[8];
+        for (int i = 0; i < 8; ++i) {
+          const int row = kSnapKGrp * w + 2 * i + sub;  // tile row (token)
+          const uint32_t ww[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          uint32_t wq[2];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t ww[4] = {v[i][u].x, v[i][u].y, v[i][u].z, v[i][u].w};
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              // rint of the exact product x * inv (fused rounding, oracle quant_i8)
-              const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
-                                           make_float2(12582912.0f, 12582912.0f));
-              const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])),
-                                           make_float2(inv, inv), make_float2(12582912.0f, 12582912.0f));
-              const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
-              const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
-              wq[2 * u + h2] = __byte_perm(lo, hi, 0x5410);
-            }
+          for (int h2 = 0; h2 < 2; ++h2) {
+            // rint of the exact product x * inv (fused rounding, oracle quant_i8)
+            const float2 y0 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2]), bf_hi(ww[2 * h2])), make_float2(inv, inv),
+                                         make_float2(12582912.0f, 12582912.0f));
+            const float2 y1 = __ffma2_rn(make_float2(bf_lo(ww[2 * h2 + 1]), bf_hi(ww[2 * h2 + 1])),
+                                         make_float2(inv, inv), make_float2(12582912.0f, 12582912.0f));
+            const uint32_t lo = __byte_perm(__float_as_uint(y0.x), __float_as_uint(y0.y), 0x0040);
+            const uint32_t hi = __byte_perm(__float_as_uint(y1.x), __float_as_uint(y1.y), 0x0040);
+            wq[h2] = __byte_perm(lo, hi, 0x5410);
           }
-          const int c0 = q4 * 2;  // 16-byte chunks c0, c0 + 1 of the row (SW128 K-major)
-          *reinterpret_cast<uint4*>(k8 + row * 128 + ((c0 ^ (row & 7)) << 4)) = make_uint4(wq[0], wq[1], wq[2], wq[3]);
-          *reinterpret_cast<uint4*>(k8 + row * 128 + (((c0 + 1) ^ (row & 7)) << 4)) =
-              make_uint4(wq[4], wq[5], wq[6], wq[7]);
+          // channels 8ch .. 8ch + 7: half (ch & 1) of 16-byte chunk ch / 2 (SW128 K-major)
+          *reinterpret_cast<uint2*>(k8 + row * 128 + (((ch >> 1) ^ (row & 7)) << 4) + (ch & 1) * 8) =
+              make_uint2(wq[0], wq[1]);
         }
         fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-        named_bar_sync(1, kSnapProd * 32);
-        if (ptid == 0) {
-          if (j == 0) mbar_wait(&sm.qbar, it & 1);  // this slice's Q8 tile landed
-          if (g >= kSnapAcc) mbar_wait(&sm.tempty[buf], ((g / kSnapAcc) - 1) & 1);  // consumers drained acc[buf] (and read its tau)
-          sm.tau[buf] = Af > 0.0f ? __fdiv_rn(Af, 127.0f) : 0.0f;
-          tc_fence_after();
-          mbar_arrive(&sm.tfull[buf]);  // release: sm.tau visible to the consumers
-          const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(k8);
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, ks > 0);
-          umma_commit(&sm.tfull[buf]);
-          SNAP_TR(true, it * 64 + j * 2 + 1);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.kfull[g & 1]);
       }
     }
-  } else {
+  } else if (warp < kSnapCtl) {
     // ================= consumers: epilogue of every tile, then the slice's tail
     const int ctid = tid - kSnapProd * 32;  // 0 .. 511
     const int cw = warp - kSnapProd;
@@ -881,9 +893,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         uint32_t X[32];
         const uint32_t ta = t_warp + buf * 128;
         tmem_ld32(ta, X);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) X[i] += kSnapBias;  // X = 0x4B400000 + I: as fp32, 12582912 + I exactly
-        const float tau = sm.tau[buf];
+        const float2 tau2 = *reinterpret_cast<const float2*>(&sm.tau[buf][2 * cb]);  // this block's two K groups
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[buf]);  // accumulator read out: the MMA of tile g + kSnapAcc may overwrite it
@@ -896,19 +906,20 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         uint32_t L = 0;
         uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (nv > 0) {  // warp-uniform (one 32-token block per warp)
-          const float a = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau, sig_r), kSnapC0)) & ~3u);
-          float c;
+          const float a0 = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau2.x, sig_r), kSnapC0)) & ~3u);
+          const float a1 = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau2.y, sig_r), kSnapC0)) & ~3u);
+          float c0, c1;
           bool nc;
           int32_t Mb;
-          if (nv == 32) snap_block_stats<false>(X, nv, a, Mb, c, nc);
-          else snap_block_stats<true>(X, nv, a, Mb, c, nc);
+          if (nv == 32) snap_block_stats<false>(X, nv, a0, a1, Mb, c0, c1, nc);
+          else snap_block_stats<true>(X, nv, a0, a1, Mb, c0, c1, nc);
           const bool act = r < R;
           const bool fast = __all_sync(0xffffffffu, nc || !act) && !SNAP_DBG(1);
           if (act) {
             M = Mb;
-            if (nv < 32) L = snap_block_e<true, true>(X, nv, a, c, pk);
-            else if (fast) L = snap_block_e<false, false>(X, nv, a, c, pk);
-            else L = snap_block_e<false, true>(X, nv, a, c, pk);
+            if (nv < 32) L = snap_block_e<true, true>(X, nv, a0, a1, c0, c1, pk);
+            else if (fast) L = snap_block_e<false, false>(X, nv, a0, a1, c0, c1, pk);
+            else L = snap_block_e<false, true>(X, nv, a0, a1, c0, c1, pk);
           }
         }
         if (EG) {
@@ -1142,6 +1153,41 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         for (int t = P + ctid; t < T; t += kCT) out[t] = INFINITY;  // window tokens always kept
       named_bar_sync(2, kCT);  // vote / halos / E / mb / lb free for the next slice
       SNAP_TR(ctid == 0, it * 64 + 38);
+    }
+  } else if (lane == 0) {
+    // ================= control thread: the slice's Q8 tile, then per tile:
+    // every quantiser warp's rows in k8 -> the accumulator drained -> scales
+    // into sm.tau[buf] -> MMA
+    constexpr uint32_t kIdesc = idesc_i8(128, 128);
+    const uint64_t dbias = umma_desc_none(sm.bias, 128, 256);
+    for (int it = 0, slice = blockIdx.y; slice < nslice; ++it, slice += gridDim.y) {
+      if (ntl == 0) continue;
+      const int g0 = it * ntl;
+      // q8 / sig are free once the previous slice's last MMA has completed
+      if (g0 >= 1) mbar_wait(&sm.tfull[(g0 - 1) % kSnapAcc], ((g0 - 1) / kSnapAcc) & 1);
+      mbar_expect_tx(&sm.qbar, kSnapQBytes);
+      bulk_g2s_hint(sm.q8, qbuf + static_cast<size_t>(slice) * kSnapQBytes, 128 * 128, &sm.qbar,
+                    l2_evict_last());  // the Q8 tiles serve every chunk
+      bulk_g2s(sm.sig, qbuf + static_cast<size_t>(slice) * kSnapQBytes + 128 * 128, 512, &sm.qbar);
+      for (int j = 0; j < ntl; ++j) {
+        const int g = g0 + j, buf = g % kSnapAcc;
+        if (g >= kSnapAcc) mbar_wait(&sm.tempty[buf], ((g / kSnapAcc) - 1) & 1);  // consumers drained acc[buf] (and read its tau)
+        // the accumulator restarts from the bias: tcgen05.cp runs before the
+        // MMAs this thread issues after it (in-order tcgen05 pipeline)
+#pragma unroll
+        for (int c8 = 0; c8 < 16; ++c8) tmem_cp_128x256b(tmem + buf * 128 + c8 * 8, dbias);
+        mbar_wait(&sm.kfull[g & 1], (g >> 1) & 1);  // all 16-token groups of tile g quantised
+        if (j == 0) mbar_wait(&sm.qbar, it & 1);     // this slice's Q8 tile landed
+        *reinterpret_cast<float4*>(&sm.tau[buf][0]) = *reinterpret_cast<const float4*>(&sm.tau_st[g & 1][0]);
+        *reinterpret_cast<float4*>(&sm.tau[buf][4]) = *reinterpret_cast<const float4*>(&sm.tau_st[g & 1][4]);
+        tc_fence_after();
+        mbar_arrive(&sm.tfull[buf]);  // release: sm.tau visible to the consumers
+        const uint64_t dq = umma_desc_sw128(sm.q8), dk = umma_desc_sw128(sm.k8[SnapSmem::KB == 2 ? (g & 1) : 0]);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) umma_i8(tmem + buf * 128, dq + 2 * ks, dk + 2 * ks, kIdesc, true);  // onto the bias
+        umma_commit(&sm.tfull[buf]);
+        SNAP_TR(true, it * 64 + j * 2 + 1);
+      }
     }
   }
   // Peers' remote arrives and DSMEM reads of this CTA's smem are all done

@@ -104,6 +104,7 @@ SNAP_C0 = np.float32(0.12751743082459868)  # log2(e) / sqrt(128)
 SNAP_E = [np.float32(float.fromhex(x)) for x in ("0x1.ffec2ep+6", "0x1.683ef2p+6", "0x1.f22ab4p+4")]
 # 2^7 * 2^f on [-1/2, 1/2], degree 2 (spec v3)
 SNAP_LSH = 24  # block sums scaled by 2^24 in the row sum
+SNAP_KGRP = 16  # tokens per K int8 scale (spec v4)
 SNAP_VOTE_SCALE = np.float32(2.0 ** -37)
 
 
@@ -155,7 +156,7 @@ def snap_exp_u8(d):
 
 
 def snapkv_scores(k, q, W, G, pool):
-    """Exact-integer snapkv v3, vectorised numpy, float32 ops."""
+    """Exact-integer snapkv v4, vectorised numpy, float32 ops."""
     L, H, T, D = k.shape
     P = T - W
     out = np.full((L, H, T), np.inf, np.float32)
@@ -170,22 +171,21 @@ def snapkv_scores(k, q, W, G, pool):
             kx = bf2f(k[l, h, :P])
             k8 = np.zeros((P, D), np.int64)
             tau = np.zeros(P, np.float32)
-            for t0 in range(0, P, 128):
-                c, sc = quant_i8(kx[t0:t0 + 128], None)
-                k8[t0:t0 + 128] = c
-                tau[t0:t0 + 128] = sc.reshape(())
+            for t0 in range(0, P, SNAP_KGRP):  # spec v4: one K scale per 16-token group
+                c, sc = quant_i8(kx[t0:t0 + SNAP_KGRP], None)
+                k8[t0:t0 + SNAP_KGRP] = c
+                tau[t0:t0 + SNAP_KGRP] = sc.reshape(())
             I = q8 @ k8.T  # exact integers [R, P]
             a = ((tau[None, :] * sig[:, None]).astype(np.float32) * SNAP_C0).astype(np.float32)  # per (r, t)
             a = (a.view(np.uint32) & np.uint32(0xFFFFFFFC)).view(np.float32)  # 22-bit mantissa: exact offsets
             blk = np.arange(P) // 32
-            Ipad = np.full((G * W, nblk * 32), np.iinfo(np.int64).min, np.int64)
-            Ipad[:, :P] = I
-            mx = Ipad.reshape(G * W, nblk, 32).max(-1)
-            ab = a[:, ::32]  # a is constant within a block (blocks never cross tiles)
-            M = np.ceil((mx.astype(np.float32) * ab).astype(np.float32)).astype(np.int64)
-            cb = ((-M).astype(np.float32) - (np.float32(12582912) * ab).astype(np.float32)).astype(np.float32)
+            y = (I.astype(np.float32) * a).astype(np.float32)  # fl(I * a): monotone in I for one group's a
+            ypad = np.full((G * W, nblk * 32), -np.inf, np.float32)
+            ypad[:, :P] = y
+            M = np.ceil(ypad.reshape(G * W, nblk, 32).max(-1)).astype(np.int64)  # ceil of the block's largest fl(I a)
+            cb = ((-M[:, blk]).astype(np.float32) - (np.float32(12582912) * a).astype(np.float32)).astype(np.float32)
             X = ((I + 0x4B400000).astype(np.uint32)).view(np.float32)
-            E = snap_exp_u8(fma32(X, a, cb[:, blk]))
+            E = snap_exp_u8(fma32(X, a, cb))
             Lb = np.add.reduceat(E, np.arange(0, P, 32), axis=1).astype(np.uint64)
             m = M.max(1, keepdims=True)
             sh = (m - M)
