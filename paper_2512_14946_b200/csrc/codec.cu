@@ -289,6 +289,17 @@ __device__ __forceinline__ void kd_fix_add(const uint4& v, float c, uint32_t (&a
     acc[2 * q + 1] += __float_as_uint(y.y);
   }
 }
+// the same 8 biased words, returned
+__device__ __forceinline__ void kd_fix_words(const uint4& v, float c, uint32_t (&y)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 z = __ffma2_rn(make_float2(bf_lo(w[q]), bf_hi(w[q])), make_float2(c, c),
+                                make_float2(12582912.0f, 12582912.0f));
+    y[2 * q] = __float_as_uint(z.x);
+    y[2 * q + 1] = __float_as_uint(z.y);
+  }
+}
 constexpr int kKdTokens = 256;  // tokens per block (16 half-warps x 16)
 
 // keydiff pass 1: S[slice][d] += sum_t rint(x_td * inv_t * 2^21) (exact int64)
@@ -375,22 +386,25 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
   const uint4* Ks = K + (static_cast<size_t>(slice) * T + t_lo) * 16;
   uint32_t seq = 0;
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint32_t cnt = 0;  // <= per / 16 tokens per lane: the biased u32 sums cannot wrap for T < 2^16
+  uint32_t cnt = 0;  // rows added per lane (incl. zero rows): < 2^9, so sum v < 2^31 and the wrap-add is exact
   stream_rows4(Ks, n_loc, ring, full, seq, [&](const int (&t)[4], const bool (&live)[4], const uint4 (&v)[4]) {
     float q[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) q[u] = chunk_sumsq(v[u]);
     // lanes 4u .. 4u + 3 get row u's |k|^2: one sqrt + reciprocal per lane
     const float mine = kd_inv(half_butterfly4(q));
+    // all four rows go into the sums (a dead row is zero: its biased words
+    // add 0), two rows per 3-input add
+    uint32_t y[4][8];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float inv = __shfl_sync(0xffffffffu, mine, (threadIdx.x & 16) + 4 * u);
-      if (live[u]) {
-        kd_fix_add(v[u], __fmul_rn(inv, kKdFx), acc);
-        ++cnt;
-        if (l16 == 0) kinv[t[u]] = inv;
-      }
+      kd_fix_words(v[u], __fmul_rn(inv, kKdFx), y[u]);
+      if (live[u] && l16 == 0) kinv[t[u]] = inv;
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += y[0][i] + y[1][i] + y[2][i] + y[3][i];
+    cnt += 4;
   }, l2_evict_last());  // pass 2 re-reads these rows: keep them in L2
 #pragma unroll
   for (int i = 0; i < 8; ++i) {  // the warp's two half-warps first (|sum| < 2^31: <= per / 16 rows each)
