@@ -950,6 +950,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
       }
       named_bar_sync(2, kCT);  // every tile's E, mb, lb in place
       SNAP_TR(ctid == 0, it * 64 + 32);
+#ifdef KVT_SNAP_TRACE
+      if (ctid == 0 && blockIdx.y == 0 && it < 16) g_snap_trace[2048 + it * 16 + rank] = gtimer();  // every rank's tiles_done
+#endif
 
       // ---- row shift and sum across the cluster. Every CTA pushes its per-row
       // values into every CTA's mglob / lglob with red.async (max / add),

@@ -75,6 +75,14 @@ def main():
     print(json.dumps({k_: v_ for k_, v_ in out.items() if k_ != "slices"}))
     for sl in out["slices"][: args.slices]:
         print(json.dumps(sl))
+    # cluster 0's CTAs: when each finished its tiles (skew the first round waits for)
+    skew = []
+    for it in range(min(16, len(out["slices"]))):
+        ts = [buf[2048 + it * 16 + r] for r in range(16)]
+        ts = [t for t in ts if t >= t0 and t]
+        if ts:
+            skew.append(round((max(ts) - min(ts)) / 1e3, 2))
+    print(json.dumps({"tiles_done_skew_us": skew}))
     # per-slice durations
     ends = [sl["end"] for sl in out["slices"]]
     print(json.dumps({"n_slices": len(ends), "slice_period_us": [round(b - a, 2) for a, b in zip(ends, ends[1:])]}))
