@@ -10,7 +10,7 @@
  * tests/test_codec_oracle.py, not by reference vectors.
  *
  * Every rounding step is spelled out so the CUDA path can match it
- * bit-for-bit (spec v2): fp32 dot products with explicit
+ * bit-for-bit (spec v2; snapkv v4): fp32 dot products with explicit
  * fmaf chains in the canonical chunk-then-butterfly order, 2^-21
  * fixed-point int64 accumulation for keydiff's mean direction, snapkv as
  * exact int8 x int8 logits with an integer-shift softmax, fp32 IEEE ops

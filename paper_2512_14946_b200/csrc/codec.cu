@@ -445,33 +445,36 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
 
 static size_t kd_cluster_smem(int T) { return kRingBytes + al256(4LL * ((T + kKdC - 1) / kKdC)); }
 
-// snapkv on the integer tensor cores, exact-integer spec v3
+// snapkv on the integer tensor cores, exact-integer spec v4
 // of DESIGN.md §4.2 (oracle/orc_codec.c snapkv_slice): window queries
-// quantised to int8 per row, prefix keys to int8 per 128-token tile, so every
+// quantised to int8 per row, prefix keys to int8 per 16-token group, so every
 // logit is an exact s8 x s8 -> s32 dot product I (tcgen05.mma kind::i8,
-// M = N = K = 128) times a per-(tile, row) factor a. The softmax shift is per
-// (row, 32-token block): M = ceil(max y), E = round(2^7 * 2^(y - M)), an
-// 8-bit value, by a fixed degree-2 FMA polynomial; blocks are combined with
-// exact integer shifts; the votes sum_r E * W (W: the row's 30-bit weight of
+// M = N = K = 128) times a per-(group, row) factor a. The softmax shift is per
+// (row, 32-token block): M = ceil(max fl(I a)), E = round(2^7 * 2^(y - M)),
+// an 8-bit value, by a fixed degree-2 FMA polynomial; blocks are combined
+// with exact integer shifts; the votes sum_r E * W (W: the row's weight of
 // the token's block) run on the integer tensor cores too.
 //
 // A thread-block cluster (<= 16 CTAs) works on one (layer, kv-head) slice
 // at a time; the clusters are persistent (as many as fit, each looping over
-// slices). CTA `rank` owns up to 4 tiles (512 tokens) of a slice. Producer
-// warps bulk-copy each tile (bf16) into smem, quantise it to int8 (SW128
-// K-major UMMA layout) and multiply it against the slice's Q8 tile into a
-// double-buffered TMEM accumulator; the 16 consumer warps (lane quadrant x
-// 32-token block) turn their 32 logits into u8 E values stored in smem as
-// the A operand of the vote MMA ([row][token], MN-major SW128). The
-// consumers then run the slice's tail while the producers already load and
-// multiply the next slice's first tiles: row shifts and row sums are
-// all-reduced by red.async (max / add) from every CTA into every CTA,
-// completing bytes on the receiver's mbarrier; the block weights are split
-// into four bytes (the B operand: n = block x limb, K = rows) and ONE
-// elected thread issues u8 x u8 -> s32 MMAs D[token][block, limb] = sum_r
-// E[r][token] * W_limb[r][block] into TMEM; each token's vote is its own
-// block's four limbs recombined; boundary votes go to the neighbours by
-// st.async; pooling.
+// slices). CTA `rank` owns up to TPC tiles (128 tokens each) of a slice.
+// Eight quantiser warps each own 16 tokens of every tile: a bulk copy of
+// their rows into their own 4 KB stage slot (issued one tile ahead), absmax,
+// int8 quantisation into the SW128 K-major k8 tile, arrive on kfull — no
+// barrier between them. A control thread waits for kfull, resets the
+// accumulator to the bias (tcgen05.cp), and issues the MMA against the
+// slice's Q8 tile into one of three TMEM accumulators. The 16 consumer
+// warps (lane quadrant x 32-token block) turn their 32 logits into u8 E
+// values stored in smem as the A operand of the vote MMA ([row][token],
+// MN-major SW128). The consumers then run the slice's tail while the
+// quantisers and the control thread already work on the next slice's first
+// tiles: row shifts and row sums are all-reduced by red.async (max / add)
+// from every CTA into every CTA, completing bytes on the receiver's
+// mbarrier; the block weights are split into four bytes (the B operand: n =
+// block x limb, K = rows) and one thread per tile issues u8 x u8 -> s32 MMAs
+// D[token][block, limb] = sum_r E[r][token] * W_limb[r][block] into TMEM;
+// each token's vote is its own block's four limbs recombined; boundary votes
+// go to the neighbours by st.async; pooling.
 constexpr int kSnapMaxC = 16;          // CTAs per cluster (non-portable above 8)
 constexpr int kSnapProd = 8;           // quantiser warps: 16 tokens of every K tile each (own bulk copy, absmax, int8)
 constexpr int kSnapCons = 16;          // consumer warps: TMEM epilogue (lane quadrant x 32-token block)
