@@ -142,15 +142,16 @@ class Codec:
         return sum(int(e.abi.launch_count(e.h)) for e in self.lanes)
 
 
-# Per 8,192-token chunk of the bench model, in µs (profiles/r1z: ncu and
-# bench per-kernel averages): scoring by method (snapkv on 112 SMs), and
-# K + V pack per unit of kept ratio by code width.
-_SCORE_US = {"snapkv": 494.0, "keydiff": 180.0, "knorm": 107.0}
+# Per 8,192-token chunk of the bench model, in µs (profiles/r2j-r2n codec
+# probe): scoring by method (snapkv on 120 SMs), and K + V pack per unit of
+# kept ratio by code width.
+_SNAP_REF_SMS = 120
+_SCORE_US = {"snapkv": 331.0, "keydiff": 176.0, "knorm": 108.0}
 _PACK_US = {16: 325.0, 8: 230.0, 4: 210.0, 2: 210.0}
 
 
 def split_plan(methods: Sequence[str], ratios: Sequence[float], Ts: Sequence[int], n_lanes: int,
-               snap_sms: int = 112) -> List[Tuple[Optional[int], int]]:
+               snap_sms: int = 120) -> List[Tuple[Optional[int], int]]:
     """(score lane, pack lane) of each context for Codec.compress_split.
     snapkv scoring is issue-bound and runs as persistent clusters on
     `snap_sms` SMs (KVT_SNAP_SMS): it goes alone on lane 0 (None = no split), so one snapkv
@@ -166,7 +167,7 @@ def split_plan(methods: Sequence[str], ratios: Sequence[float], Ts: Sequence[int
         score = T / 8192.0 * _SCORE_US.get(base, 0.0) if r < 1.0 else 0.0
         li = min(range(1, n_lanes), key=load.__getitem__) if n_lanes > 1 else 0
         if base == "snapkv" and r < 1.0:
-            load[0] += score * 112.0 / snap_sms
+            load[0] += score * _SNAP_REF_SMS / snap_sms
             load[li] += pack
             out.append((0, li))
         else:
