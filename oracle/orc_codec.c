@@ -376,6 +376,7 @@ static void keydiff_slice(void* a, int64_t sl) {
 #define SNAP_VOTE_SCALE 0x1p-37f      /* vote = 2^37 x sum of probabilities */
 #define SNAP_BLK 32   /* tokens per softmax shift block */
 #define SNAP_KGRP 16  /* tokens per K int8 scale (spec v4) */
+#define SNAP_AMAX 0.25f /* cap of the logit factor a (v4): keeps -M - 12582912 a exact */
 
 static uint32_t f2u(float f) {
   uint32_t u;
@@ -460,9 +461,12 @@ static void snapkv_slice(void* a, int64_t sl) {
     const int8_t* qr = q8 + (size_t)r * D_HEAD;
     for (int b = 0; b < nblk; ++b) {
       const int t0 = b * SNAP_BLK, n = (P - t0 < SNAP_BLK ? P - t0 : SNAP_BLK);
-      /* log2 units per unit of I for each token's 16-group, low 2 mantissa
-       * bits cleared: then 12582912 * a and -M - 12582912 * a are exact, and
-       * the fma below is the single correctly rounded value of I * a - M */
+      /* log2 units per unit of I for each token's 16-group, capped at 1/4
+       * and with the low 2 mantissa bits cleared: then 12582912 * a and
+       * -M - 12582912 * a are exact (|M| <= 2^21 a), and the fma below is the
+       * single correctly rounded value of I * a - M. (A factor of 1/4 log2
+       * units per unit of I already makes the softmax one-hot; without the
+       * cap the offset rounds and E could exceed 8 bits.) */
       float a_t[SNAP_BLK];
       float ymax = -INFINITY;
       for (int i = 0; i < n; ++i) {
@@ -470,7 +474,8 @@ static void snapkv_slice(void* a, int64_t sl) {
         const int8_t* kt = k8 + (size_t)(t0 + i) * D_HEAD;
         for (int d = 0; d < D_HEAD; ++d) acc += (int32_t)qr[d] * (int32_t)kt[d];
         I[i] = acc;
-        a_t[i] = u2f(f2u((tau[(t0 + i) / SNAP_KGRP] * sig[r]) * SNAP_C0) & ~3u);
+        const float araw = (tau[(t0 + i) / SNAP_KGRP] * sig[r]) * SNAP_C0;
+        a_t[i] = u2f(f2u(araw < SNAP_AMAX ? araw : SNAP_AMAX) & ~3u);
         const float y = (float)acc * a_t[i];
         ymax = y > ymax ? y : ymax;
       }

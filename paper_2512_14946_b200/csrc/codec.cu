@@ -482,6 +482,7 @@ constexpr int kSnapCtl = kSnapProd + kSnapCons;  // control warp: Q8 loads, logi
 constexpr int kSnapThreads = (kSnapCtl + 1) * 32;
 constexpr int kSnapKGrp = 16;          // tokens per K int8 scale (spec v4)
 constexpr float kSnapC0 = 0.12751743082459868f;  // log2(e) / sqrt(128)
+constexpr float kSnapAMax = 0.25f;  // cap of the logit factor a (spec v4, oracle SNAP_AMAX)
 constexpr int kSnapQBytes = 128 * 128 + 128 * 4;  // per slice: Q8 tile (SW128) + sigma[128]
 // Two configurations of one kernel: prefixes up to 16 x 8 tiles (16384
 // tokens) keep the u8 E matrix in smem (TPC = 8: 1,024 tokens per CTA, so a
@@ -923,8 +924,11 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         uint32_t L = 0;
         uint32_t pk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (nv > 0) {  // warp-uniform (one 32-token block per warp)
-          const float a0 = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau2.x, sig_r), kSnapC0)) & ~3u);
-          const float a1 = __uint_as_float(__float_as_uint(__fmul_rn(__fmul_rn(tau2.y, sig_r), kSnapC0)) & ~3u);
+          // a capped at 1/4 (spec v4: keeps -M - 12582912 a exact), low 2 mantissa bits cleared
+          const float a0 =
+              __uint_as_float(__float_as_uint(fminf(__fmul_rn(__fmul_rn(tau2.x, sig_r), kSnapC0), kSnapAMax)) & ~3u);
+          const float a1 =
+              __uint_as_float(__float_as_uint(fminf(__fmul_rn(__fmul_rn(tau2.y, sig_r), kSnapC0), kSnapAMax)) & ~3u);
           float c0, c1;
           bool nc;
           int32_t Mb;

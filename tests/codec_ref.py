@@ -105,6 +105,7 @@ SNAP_E = [np.float32(float.fromhex(x)) for x in ("0x1.ffec2ep+6", "0x1.683ef2p+6
 # 2^7 * 2^f on [-1/2, 1/2], degree 2 (spec v3)
 SNAP_LSH = 24  # block sums scaled by 2^24 in the row sum
 SNAP_KGRP = 16  # tokens per K int8 scale (spec v4)
+SNAP_AMAX = np.float32(0.25)  # cap of the logit factor a (spec v4)
 SNAP_VOTE_SCALE = np.float32(2.0 ** -37)
 
 
@@ -177,6 +178,7 @@ def snapkv_scores(k, q, W, G, pool):
                 tau[t0:t0 + SNAP_KGRP] = sc.reshape(())
             I = q8 @ k8.T  # exact integers [R, P]
             a = ((tau[None, :] * sig[:, None]).astype(np.float32) * SNAP_C0).astype(np.float32)  # per (r, t)
+            a = np.minimum(a, SNAP_AMAX)  # v4 cap: keeps -M - 12582912 a exact
             a = (a.view(np.uint32) & np.uint32(0xFFFFFFFC)).view(np.float32)  # 22-bit mantissa: exact offsets
             blk = np.arange(P) // 32
             y = (I.astype(np.float32) * a).astype(np.float32)  # fl(I * a): monotone in I for one group's a

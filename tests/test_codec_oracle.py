@@ -155,6 +155,42 @@ def test_snapkv_caller_queries_match_numpy(lib):
     assert not np.array_equal(out, _scores(lib, s, cfg, k))
 
 
+def _snap_groups_k(L, H, T, seed=8):
+    """Keys that exercise snapkv spec v4's per-16-token K scales: an all-zero
+    group (scale 0), a group with one huge outlier row (a large logit factor:
+    the clamped E path next to clamp-free blocks), a group of tiny values, a
+    constant group, -0, and a ragged last group and block (P = T - 32)."""
+    k, _ = _kv(L, H, T, seed=seed)
+    x = R.bf2f(k).copy()
+    x[:, :, 16:32] = 0.0                                   # group 1: all zero -> tau = 0
+    x[:, :, 37] *= np.float32(4e3)                         # group 2: one huge row
+    x[:, :, 48:64] *= np.float32(1e-20)                    # group 3: tiny
+    x[:, :, 64:80] = np.float32(0.75)                      # group 4: constant
+    x[:, :, 81, 3] = np.float32(-0.0)
+    x[:, :, 100:108] *= np.float32(-300.0)                 # half of group 6 large and negated
+    to_bf = lambda a: (a.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    return to_bf(x)
+
+
+def _snap_queries(s, cfg, seed=11, spread=3.0):
+    rng = np.random.default_rng(seed)
+    qf = rng.standard_normal((s.L, s.H * cfg.q_heads, cfg.window, 128)).astype(np.float32) * np.float32(spread)
+    return (qf.view(np.uint32) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("T", [32 + 300, 32 + 129])
+def test_snapkv_k_groups_match_numpy(lib, T):
+    """spec v4 K groups (zero, outlier, tiny, constant, ragged): oracle == numpy."""
+    s = shape(1, 2, T)
+    k = _snap_groups_k(1, 2, T)
+    cfg = plan(lib, "snapkv", 0.5, s)
+    q = _snap_queries(s, cfg)
+    out = np.zeros((1, 2, T), np.float32)
+    lib.check(lib.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(q), A.ptr(out)))
+    want = R.snapkv_scores(k, q, cfg.window, cfg.q_heads, cfg.pool)
+    assert np.array_equal(out.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
+
+
 def test_knorm_keep_low_flag(lib):
     s = shape(1, 2, 100)
     k, _ = _kv(1, 2, 100)

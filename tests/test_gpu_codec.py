@@ -182,6 +182,27 @@ def test_snapkv_caller_queries_bitexact(gpu, orc, si, spread):
     assert np.array_equal(bg.cpu().numpy(), bo)
 
 
+@pytest.mark.parametrize("T", [32 + 300, 32 + 129, 32 + 8192])
+@pytest.mark.parametrize("spread", [3.0, 30.0])
+def test_snapkv_k_groups_bitexact(gpu, orc, T, spread):
+    """spec v4 per-16-token K scales on structured keys (an all-zero group, a
+    huge outlier row whose logit factor hits the 1/4 cap, tiny and constant
+    groups, -0, ragged last group and block) with caller queries: scores
+    equal the oracle bit for bit, through the clamped and clamp-free E paths."""
+    from test_codec_oracle import _snap_groups_k, _snap_queries
+    s = A.KvShape(1, 2, T, 128)
+    k = _snap_groups_k(1, 2, T)
+    cfg = plan(orc.abi, "snapkv", 0.5, s)
+    q = _snap_queries(s, cfg, spread=spread)
+    want = np.zeros(2 * T, np.float32)
+    orc.abi.check(orc.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(q), A.ptr(want)))
+    kg, qg = dev(k.reshape(-1).view(np.int16)), dev(q.reshape(-1).view(np.int16))
+    out = torch.empty(2 * T, dtype=torch.float32, device="cuda")
+    gpu.abi.check(gpu.abi.token_scores(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), A.ptr(qg), A.ptr(out)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
 @pytest.mark.parametrize("si", range(len(SHAPES)))
 def test_knorm_keep_low_flag(gpu, orc, si):
     """KVT_CODEC_KNORM_KEEP_LOW (the cited knorm paper keeps low-norm keys;
