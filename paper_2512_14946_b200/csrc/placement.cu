@@ -30,7 +30,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "kvt_common.cuh"
 
@@ -1665,8 +1664,6 @@ struct kvt_store {
   int* ops_buf = nullptr;
   long long* ops_l = nullptr;
   long long ops_cap = 0;
-  void* sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
   std::vector<std::string> names;
   bool has_space = false;
   DevSpace S{};
@@ -1768,7 +1765,6 @@ extern "C" int kvt_store_destroy(kvt_store* s) {
   cudaFree(s->act);
   cudaFree(s->ops_buf);
   cudaFree(s->ops_l);
-  cudaFree(s->sort_tmp);
   delete s;
   return KVT_OK;
 }
@@ -2161,24 +2157,109 @@ extern "C" int kvt_least_drop_update(kvt_store* s, const kvt_pset* p, const kvt_
   return store_status_error(s, c);
 }
 
-static int ensure_sort_tmp(kvt_store* s, size_t bytes) {
-  if (bytes <= s->sort_tmp_bytes) return KVT_OK;
-  cudaFree(s->sort_tmp);
-  s->sort_tmp = nullptr;
-  KVT_CUDA_TRY(cudaMalloc(&s->sort_tmp, bytes));
-  s->sort_tmp_bytes = bytes;
-  return KVT_OK;
+// Stable LSD radix sort of (u64 key, int value) pairs, ascending, in one
+// 1024-thread CTA (rearrange / placement_utility: one sort of <= the store's
+// contexts per call, off the bench's hot loop). Eight 8-bit passes ping-pong
+// between the two buffers; a pass whose digit is the same for every key is
+// skipped. Per 1,024-element tile: a thread's rank among equal digits of
+// its warp (__match_any_sync), per-(warp, digit) counts prefix-summed over
+// the warps in smem, plus the digit's running base over earlier tiles —
+// stable by construction. The sorted pairs end in (k_out, v_out); k_in /
+// v_in are scratch.
+constexpr int kSortT = 1024;
+__global__ void __launch_bounds__(kSortT) k_sort_pairs(unsigned long long* __restrict__ k_in, int* __restrict__ v_in,
+                                                       unsigned long long* __restrict__ k_out,
+                                                       int* __restrict__ v_out, int n) {
+  __shared__ int wcnt[kSortT / 32][256];
+  __shared__ int base[256], tot[256];
+  __shared__ int skip;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long* sk = k_in;
+  int* sv = v_in;
+  unsigned long long* dk = k_out;
+  int* dv = v_out;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int sh = 8 * pass;
+    if (tid < 256) base[tid] = 0;
+    if (tid == 0) skip = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kSortT) atomicAdd(&base[static_cast<int>((sk[i] >> sh) & 255)], 1);
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 256 digit counts: 8 bins per lane + a warp scan
+      int c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = base[8 * lane + j];
+        if (c[j] == n) skip = 1;  // every key has this digit: the pass is the identity
+        sum += c[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        base[8 * lane + j] = run;
+        run += c[j];
+      }
+    }
+    __syncthreads();
+    if (skip) continue;  // block-uniform
+    for (int t0 = 0; t0 < n; t0 += kSortT) {
+      const int i = t0 + tid;
+      const bool live = i < n;
+      const unsigned long long key = live ? sk[i] : 0ull;
+      const int val = live ? sv[i] : 0;
+      const int d = live ? static_cast<int>((key >> sh) & 255) : 256;
+      for (int j = tid; j < (kSortT / 32) * 256; j += kSortT) (&wcnt[0][0])[j] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int lower = __popc(peers & ((1u << lane) - 1u));
+      if (live && lower == 0) wcnt[warp][d] = __popc(peers);
+      __syncthreads();
+      if (tid < 256) {  // per digit: exclusive prefix over the warps, and the tile's total
+        int acc = 0;
+        for (int w = 0; w < kSortT / 32; ++w) {
+          const int c = wcnt[w][tid];
+          wcnt[w][tid] = acc;
+          acc += c;
+        }
+        tot[tid] = acc;
+      }
+      __syncthreads();
+      if (live) {
+        const int pos = base[d] + wcnt[warp][d] + lower;
+        dk[pos] = key;
+        dv[pos] = val;
+      }
+      __syncthreads();
+      if (tid < 256) base[tid] += tot[tid];
+      __syncthreads();
+    }
+    unsigned long long* tk = sk;
+    sk = dk;
+    dk = tk;
+    int* tv = sv;
+    sv = dv;
+    dv = tv;
+    __syncthreads();  // this pass's scatter visible to the whole CTA before the next reads it
+  }
+  if (sk != k_out)  // the result is in the scratch pair: copy it out
+    for (int i = tid; i < n; i += kSortT) {
+      k_out[i] = sk[i];
+      v_out[i] = sv[i];
+    }
 }
 
 // keys/vals double buffers for the radix sorts (n each)
 static int sort_pairs(kvt_store* s, unsigned long long* k_in, unsigned long long* k_out, int* v_in, int* v_out,
                       int n) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, k_in, k_out, v_in, v_out, n, 0, 64, s->h->stream);
-  int rc = ensure_sort_tmp(s, tmp);
-  if (rc) return rc;
-  KVT_CUDA_TRY(cub::DeviceRadixSort::SortPairs(s->sort_tmp, tmp, k_in, k_out, v_in, v_out, n, 0, 64, s->h->stream));
-  s->h->launches += 4;
+  k_sort_pairs<<<1, kSortT, 0, s->h->stream>>>(k_in, v_in, k_out, v_out, n);
+  s->h->launches++;
+  KVT_CUDA_TRY(cudaGetLastError());
   return KVT_OK;
 }
 
