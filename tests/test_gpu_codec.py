@@ -203,6 +203,31 @@ def test_snapkv_k_groups_bitexact(gpu, orc, T, spread):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("method", ["knorm", "keydiff"])
+def test_scores_denormal_keys_bitexact(gpu, orc, method):
+    """bf16 subnormal, zero and -0 keys (rows of them, and rows mixing them
+    with normal channels): scores equal the oracle's bit for bit (no flush
+    to zero anywhere on the path)."""
+    s = A.KvShape(1, 2, 300, 128)
+    k, _ = gen(orc, s, on_gpu=False)
+    x = k.reshape(2, 300, 128).copy()
+    rng = np.random.default_rng(3)
+    sub = rng.integers(1, 0x80, size=(2, 100, 128)).astype(np.uint16)  # bf16 subnormals: exponent 0
+    sub |= (rng.integers(0, 2, size=sub.shape).astype(np.uint16) << 15)
+    x[:, 50:150] = sub
+    x[:, 160:170] = 0x8000  # -0 rows
+    x[:, 170:180, :64] = sub[:, :10, :64]
+    x = x.reshape(-1)
+    cfg = plan(orc.abi, method, 0.3, s)
+    want = np.zeros(2 * 300, np.float32)
+    orc.abi.check(orc.abi.token_scores(None, C.byref(s), C.byref(cfg), A.ptr(x), None, A.ptr(want)))
+    kg = dev(x.view(np.int16))
+    out = torch.empty(2 * 300, dtype=torch.float32, device="cuda")
+    gpu.abi.check(gpu.abi.token_scores(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), None, A.ptr(out)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
 @pytest.mark.parametrize("si", range(len(SHAPES)))
 def test_knorm_keep_low_flag(gpu, orc, si):
     """KVT_CODEC_KNORM_KEEP_LOW (the cited knorm paper keeps low-norm keys;
