@@ -116,14 +116,15 @@ def topk(eng, s, cfg, sc, on_gpu):
     return out
 
 
-# snapkv prefix lengths: one tile, 1 token, several tiles in one CTA, a
-# 16-CTA (non-portable) cluster (T = 8192), a 9-CTA cluster with a ragged
-# last tile and block, the longest smem-E prefix (8192 tokens, 16 full CTAs),
-# the global-E configuration (8193 tokens: 5 CTAs x 13 tiles; 16352: 8 x 16),
-# and prefixes of length 0 (all window)
+# snapkv prefix lengths (8 tiles = 1,024 tokens per cluster CTA in the
+# smem-E configuration): one tile, 1 token, several tiles in one CTA, an
+# 8-CTA cluster (T = 8192), ragged last tiles and blocks, a 9-CTA cluster
+# (8225), 16 CTAs (16384: the longest smem-E prefix is 16,384 tokens), the
+# global-E configuration (T = 20000: 10 CTAs x 16 tiles, E in per-SM L2
+# slots, votes on the CUDA cores), and prefixes of length 0 (all window)
 SNAP_SHAPES = SHAPES + [A.KvShape(1, 1, 33, 128), A.KvShape(1, 2, 8192, 128), A.KvShape(2, 1, 4097, 128),
                         A.KvShape(1, 1, 8224, 128), A.KvShape(1, 1, 8225, 128), A.KvShape(1, 2, 16384, 128),
-                        A.KvShape(1, 2, 32, 128), A.KvShape(1, 1, 20, 128)]
+                        A.KvShape(1, 2, 32, 128), A.KvShape(1, 1, 20, 128), A.KvShape(1, 2, 20000, 128)]
 
 
 @pytest.mark.parametrize("si", range(len(SNAP_SHAPES)))
@@ -147,7 +148,7 @@ def window_queries(s, cfg, seed, spread=1.0):
     return (q.view(np.uint32) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("si", [0, 1, 4, 5, 7, 9])
+@pytest.mark.parametrize("si", [0, 1, 4, 5, 7, 9, 11])
 @pytest.mark.parametrize("spread", [1.0, 30.0])
 def test_snapkv_caller_queries_bitexact(gpu, orc, si, spread):
     """snapkv over the caller's observation-window queries
