@@ -20,7 +20,6 @@
 #include <string>
 
 #include <cooperative_groups.h>
-#include <cub/block/block_scan.cuh>
 
 #include "codec_common.cuh"
 #include "sm100.cuh"
@@ -1423,21 +1422,25 @@ __device__ __forceinline__ void select_bucket(const int* hist, int rem, int* b_o
 }
 
 constexpr int kTopkThreads = 512;
-using TopkScan = cub::BlockScan<int, kTopkThreads>;
 
 // Per (layer, head): the `keep` largest scores, ties -> lower index,
 // indices ascending. MSB-first 8-bit radix select on orderable keys held in
-// shared memory, then an order-preserving block compaction.
+// shared memory, starting at the highest bit where the slice's keys differ.
+// Then an order-preserving compaction: warp w owns a run of consecutive 32-token
+// groups (lane = token); one ballot of "above the k-th key" and one of
+// "equal to it" per group rank the kept tokens, and each group's indices go
+// out as one coalesced store.
 __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__ scores, int32_t* __restrict__ idx,
                                                        int T, int k, int keys_in_smem) {
-  extern __shared__ uint32_t skeys[];  // key t at skeys[t + t / 16]: conflict-free per-thread segments
+  extern __shared__ uint32_t skeys[];  // key t at skeys[t + t / 16]
   __shared__ int hist[256];
   __shared__ uint32_t s_prefix, s_mask;
   __shared__ int s_remaining, s_bucket, s_remaining_next;
-  __shared__ typename TopkScan::TempStorage scan_tmp;
   __shared__ uint32_t s_and[kTopkThreads / 32], s_or[kTopkThreads / 32];
-  const int slice = blockIdx.x, tid = threadIdx.x;
+  const int slice = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const float* sc = scores + static_cast<size_t>(slice) * T;
+  auto key_at = [&](int t) { return keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]); };
   // the bits every key shares need no radix pass (and would pile the first
   // histogram into one bin): start at the highest bit where keys differ
   uint32_t kand = ~0u, kor = 0u;
@@ -1450,9 +1453,9 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   }
   kand = __reduce_and_sync(0xffffffffu, kand);
   kor = __reduce_or_sync(0xffffffffu, kor);
-  if ((tid & 31) == 0) {
-    s_and[tid >> 5] = kand;
-    s_or[tid >> 5] = kor;
+  if (lane == 0) {
+    s_and[warp] = kand;
+    s_or[warp] = kor;
   }
   __syncthreads();
   kand = ~0u;
@@ -1477,7 +1480,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
     __syncthreads();
     const uint32_t prefix = s_prefix, mask = s_mask;
     for (int t = tid; t < T; t += kTopkThreads) {
-      const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
+      const uint32_t key = key_at(t);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
     }
     __syncthreads();
@@ -1493,29 +1496,38 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   }
   const uint32_t kth = s_prefix;
   const int ties = s_remaining;  // equal-to-kth keys to take (lowest indices)
-  const int seg = (T + kTopkThreads - 1) / kTopkThreads;
-  const int t0 = tid * seg, t1 = min(T, t0 + seg);
-  int above = 0, eq = 0;
-  for (int t = t0; t < t1; ++t) {
-    const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
-    above += key > kth;
-    eq += key == kth;
+  constexpr int kW = kTopkThreads / 32;
+  const int ngrp = (T + 31) / 32, gpw = (ngrp + kW - 1) / kW;
+  const int g0 = warp * gpw, g1 = min(ngrp, g0 + gpw);
+  int na = 0, ne = 0;
+  for (int g = g0; g < g1; ++g) {
+    const int t = g * 32 + lane;
+    const uint32_t key = t < T ? key_at(t) : 0u;
+    na += __popc(__ballot_sync(0xffffffffu, t < T && key > kth));
+    ne += __popc(__ballot_sync(0xffffffffu, t < T && key == kth));
   }
-  int above_before, eq_before;
-  TopkScan(scan_tmp).ExclusiveSum(above, above_before);
+  if (lane == 0) {
+    s_and[warp] = static_cast<uint32_t>(na);  // (the key-bit reductions are done with these)
+    s_or[warp] = static_cast<uint32_t>(ne);
+  }
   __syncthreads();
-  TopkScan(scan_tmp).ExclusiveSum(eq, eq_before);
-  int pos = above_before + min(eq_before, ties);
-  int eq_seen = eq_before;
+  int a_before = 0, e_before = 0;
+  for (int w = 0; w < warp; ++w) {
+    a_before += static_cast<int>(s_and[w]);
+    e_before += static_cast<int>(s_or[w]);
+  }
+  int pos = a_before + min(e_before, ties), eq_seen = e_before;
   int32_t* out = idx + static_cast<size_t>(slice) * k;
-  for (int t = t0; t < t1; ++t) {
-    const uint32_t key = keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]);
-    if (key > kth) {
-      out[pos++] = t;
-    } else if (key == kth) {
-      if (eq_seen < ties) out[pos++] = t;
-      ++eq_seen;
-    }
+  for (int g = g0; g < g1; ++g) {
+    const int t = g * 32 + lane;
+    const uint32_t key = t < T ? key_at(t) : 0u;
+    const bool gt = t < T && key > kth, eq = t < T && key == kth;
+    const unsigned be = __ballot_sync(0xffffffffu, eq);
+    const bool keep = gt || (eq && eq_seen + __popc(be & lt) < ties);
+    const unsigned bk = __ballot_sync(0xffffffffu, keep);
+    if (keep) out[pos + __popc(bk & lt)] = t;
+    pos += __popc(bk);
+    eq_seen += __popc(be);
   }
 }
 
