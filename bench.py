@@ -403,6 +403,12 @@ def _alias(ptr, n):
     return torch.as_tensor(_Cai(), device="cuda")
 
 
+# snapkv's SM budget in the split schedule, per workload: A/B on one B200
+# (alternating runs, same box): c2 48 SMs 3,507 / 56 3,475 / 64 3,453 GB/s;
+# c5 (varied lengths, up to 16-CTA clusters) 48 3,278 / 64 3,323 GB/s.
+SNAP_SMS = {"c5": 64}
+
+
 def north_star_pass(args):
     """BASELINE configs[4] beside the headline config: the full compress +
     score + place pass over 13,889 varied-length contexts x 72 candidates =
@@ -411,7 +417,7 @@ def north_star_pass(args):
     placement is the reference's own, bit for bit
     (tests/test_large_placement.py, fixture from the reference greedy)."""
     cmd = [sys.executable, os.path.abspath(__file__), "--config", "c5", "--steps", str(args.n1_steps), "--warmup", "1",
-           "--no-cpu-baseline", "--tiered-steps", "0", "--no-n1", "--snap-sms", str(args.snap_sms),
+           "--no-cpu-baseline", "--tiered-steps", "0", "--no-n1", "--snap-sms", str(SNAP_SMS.get("c5", 48)),
            "--streams", str(args.streams), "--lanes", args.lanes]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
@@ -975,8 +981,9 @@ def main():
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
     ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
-    ap.add_argument("--snap-sms", type=int, default=64,
-                    help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS)")
+    ap.add_argument("--snap-sms", type=int, default=None,
+                    help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS); default "
+                         "per workload (SNAP_SMS: measured best for its mix of context lengths)")
     ap.add_argument("--tiered-steps", type=int, default=2, help="steps of the e2e_tiered leg (PCIe-bound); 0 = skip")
     ap.add_argument("--no-n1", dest="n1", action="store_false",
                     help="skip the north-star pass (c5: 1,000,008 chunk-configs) reported beside the headline line")
@@ -988,6 +995,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.snap_sms is None:
+        args.snap_sms = SNAP_SMS.get(args.config, 48)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch(args)
     if args.impl == "reference":
