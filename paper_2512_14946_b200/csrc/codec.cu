@@ -545,15 +545,14 @@ constexpr uint32_t kSnapBias = 0x4B400000u;
 // Two E values: x = 12582912 + I (exact), d = fma(x, a, c) = rint-exact
 // I * a - M; E = round(2^7 * 2^max(d, -16)) (oracle snap_exp_u8), packed
 // fp32x2 ops (each lane rounds like the scalar op). Returns the raw
-// float-as-int words 0x4B000000 + E, E <= 128. kClamp = false when every d
-// of the block is >= -120: then n = rint(d) >= -120 keeps the exponent add
-// in range and E (0 for any d < -9) equals the clamped value bit for bit.
-template <bool kClamp>
+// float-as-int words 0x4B000000 + E, E <= 128. (Skipping the clamp for
+// blocks whose smallest d is >= -120 is bit-identical but cost more than it
+// saved: the block minimum took as many instructions, r2 measurement.)
 __device__ __forceinline__ void snap_exp_pair(uint32_t x0, uint32_t x1, float a, float c, uint32_t& u0,
                                               uint32_t& u1) {
   const float2 x = make_float2(__uint_as_float(x0), __uint_as_float(x1));
   const float2 d = __ffma2_rn(x, make_float2(a, a), make_float2(c, c));
-  const float2 dc = kClamp ? make_float2(fmaxf(d.x, -16.0f), fmaxf(d.y, -16.0f)) : d;
+  const float2 dc = make_float2(fmaxf(d.x, -16.0f), fmaxf(d.y, -16.0f));
   const float2 t = __fadd2_rn(dc, make_float2(12582912.0f, 12582912.0f));
   const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(dc, make_float2(-n.x, -n.y));
@@ -568,25 +567,18 @@ __device__ __forceinline__ void snap_exp_pair(uint32_t x0, uint32_t x1, float a,
 
 // One (row, 32-token block), phase 1. Tokens 0-15 and 16-31 are two K
 // scale groups (a0, a1): block shift M = ceil(max over tokens of fl(I * a))
-// (per group fl(max I * a): fl is monotone), the fma offsets c0, c1, and
-// whether the block's smallest d is >= -120 (no clamp needed). Ragged blocks
-// only look at tokens < nv.
+// (per group fl(max I * a): fl is monotone) and the fma offsets c0, c1.
+// Ragged blocks only look at tokens < nv.
 template <bool kRagged>
 __device__ __forceinline__ void snap_block_stats(const uint32_t (&X)[32], int nv, float a0, float a1, int32_t& M,
-                                                 float& c0, float& c1, bool& noclamp) {
-  uint32_t mx0 = 0, mn0 = 0xffffffffu, mx1 = 0, mn1 = 0xffffffffu;
+                                                 float& c0, float& c1) {
+  uint32_t mx0 = 0, mx1 = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i)
-    if (!kRagged || i < nv) {
-      mx0 = max(mx0, X[i]);
-      mn0 = min(mn0, X[i]);
-    }
+    if (!kRagged || i < nv) mx0 = max(mx0, X[i]);
 #pragma unroll
   for (int i = 16; i < 32; ++i)
-    if (!kRagged || i < nv) {
-      mx1 = max(mx1, X[i]);
-      mn1 = min(mn1, X[i]);
-    }
+    if (!kRagged || i < nv) mx1 = max(mx1, X[i]);
   const bool h1 = !kRagged || nv > 16;  // the second group has tokens
   // X - 12582912 is exact (both in [2^23, 2^24)): the int32 max I as fp32
   const float y0 = __fmul_rn(__fsub_rn(__uint_as_float(mx0), 12582912.0f), a0);
@@ -595,13 +587,11 @@ __device__ __forceinline__ void snap_block_stats(const uint32_t (&X)[32], int nv
   const float fm = __int2float_rn(-M);
   c0 = __fsub_rn(fm, __fmul_rn(12582912.0f, a0));
   c1 = __fsub_rn(fm, __fmul_rn(12582912.0f, a1));
-  noclamp = __fmaf_rn(__uint_as_float(mn0), a0, c0) >= -120.0f &&
-            (!h1 || __fmaf_rn(__uint_as_float(mn1), a1, c1) >= -120.0f);
 }
 
 // Phase 2: the 32 E bytes packed 4 per word (token order); returns the
 // block sum L. Ragged blocks mask tokens >= nv (E = 0).
-template <bool kRagged, bool kClamp>
+template <bool kRagged>
 __device__ __forceinline__ uint32_t snap_block_e(const uint32_t (&X)[32], int nv, float a0, float a1, float c0,
                                                  float c1, uint32_t (&pk)[8]) {
   uint32_t L = 0;
@@ -609,8 +599,8 @@ __device__ __forceinline__ uint32_t snap_block_e(const uint32_t (&X)[32], int nv
   for (int i = 0; i < 32; i += 4) {
     const float a = i < 16 ? a0 : a1, c = i < 16 ? c0 : c1;
     uint32_t u[4];
-    snap_exp_pair<kClamp>(X[i], X[i + 1], a, c, u[0], u[1]);
-    snap_exp_pair<kClamp>(X[i + 2], X[i + 3], a, c, u[2], u[3]);
+    snap_exp_pair(X[i], X[i + 1], a, c, u[0], u[1]);
+    snap_exp_pair(X[i + 2], X[i + 3], a, c, u[2], u[3]);
     if (kRagged) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -711,15 +701,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                       \
     if ((cond) && blockIdx.y == 0 && rank == 0 && (idx) < 4096) g_snap_trace[(idx)] = gtimer(); \
   } while (0)
-__device__ int g_snap_dbg;  // bit 0: force the clamped E path
-extern "C" int kvt_debug_snap_set(int v) { return cudaMemcpyToSymbol(g_snap_dbg, &v, sizeof v) == cudaSuccess ? 0 : -1; }
-#define SNAP_DBG(bit) (g_snap_dbg & (bit))
 extern "C" int kvt_debug_snap_trace(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, g_snap_trace, sizeof(unsigned long long) * (n < 4096 ? n : 4096)) == cudaSuccess ? 0 : -1;
 }
 #else
 #define SNAP_TR(cond, idx) do {} while (0)
-#define SNAP_DBG(bit) 0
 #endif
 
 template <int TPC, bool EG>
@@ -928,18 +914,15 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
               __uint_as_float(__float_as_uint(fminf(__fmul_rn(__fmul_rn(tau2.x, sig_r), kSnapC0), kSnapAMax)) & ~3u);
           const float a1 =
               __uint_as_float(__float_as_uint(fminf(__fmul_rn(__fmul_rn(tau2.y, sig_r), kSnapC0), kSnapAMax)) & ~3u);
-          float c0, c1;
-          bool nc;
-          int32_t Mb;
-          if (nv == 32) snap_block_stats<false>(X, nv, a0, a1, Mb, c0, c1, nc);
-          else snap_block_stats<true>(X, nv, a0, a1, Mb, c0, c1, nc);
-          const bool act = r < R;
-          const bool fast = __all_sync(0xffffffffu, nc || !act) && !SNAP_DBG(1);
-          if (act) {
-            M = Mb;
-            if (nv < 32) L = snap_block_e<true, true>(X, nv, a0, a1, c0, c1, pk);
-            else if (fast) L = snap_block_e<false, false>(X, nv, a0, a1, c0, c1, pk);
-            else L = snap_block_e<false, true>(X, nv, a0, a1, c0, c1, pk);
+          if (r < R) {
+            float c0, c1;
+            if (nv == 32) {
+              snap_block_stats<false>(X, nv, a0, a1, M, c0, c1);
+              L = snap_block_e<false>(X, nv, a0, a1, c0, c1, pk);
+            } else {
+              snap_block_stats<true>(X, nv, a0, a1, M, c0, c1);
+              L = snap_block_e<true>(X, nv, a0, a1, c0, c1, pk);
+            }
           }
         }
         if (EG) {
