@@ -818,15 +818,22 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = make_uint4(0, 0, 0, 0);
         }
-        uint32_t mx2 = 0;
+        // |x| max = max(max x, -min x): packed bf16 max / min chains (3-input
+        // VHMNMX), no per-word abs mask; NaN ignored, as the oracle's compare
+        auto bf2 = [](uint32_t w) { return *reinterpret_cast<__nv_bfloat162*>(&w); };
+        __nv_bfloat162 hi2 = bf2(v[0].x), lo2 = bf2(v[0].x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          mx2 = __vmaxu2(mx2, v[i].x & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i].y & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i].z & 0x7fff7fffu);
-          mx2 = __vmaxu2(mx2, v[i].w & 0x7fff7fffu);
+          const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+          for (int q = (i == 0 ? 1 : 0); q < 4; ++q) {
+            hi2 = __hmax2(hi2, bf2(w4[q]));
+            lo2 = __hmin2(lo2, bf2(w4[q]));
+          }
         }
-        const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mx2 & 0xffffu, mx2 >> 16));  // slot fully read
+        const __nv_bfloat162 m2 = __hmax2(hi2, __hneg2(lo2));  // per half: max |x|
+        const uint32_t mu = *reinterpret_cast<const uint32_t*>(&m2) & 0x7fff7fffu;  // (-0 -> +0)
+        const uint32_t wmx = __reduce_max_sync(0xffffffffu, max(mu & 0xffffu, mu >> 16));  // slot fully read
         {  // the next tile's rows into the slot, the one after that into L2
           int sn = slice, jn = j;
           next_of(sn, jn);
