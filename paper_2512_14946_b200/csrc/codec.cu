@@ -812,8 +812,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           mbar_wait(&sm.fullw[w], nld & 1);
           ++nld;
           SNAP_TR(w == 0 && lane == 0, it * 64 + j * 2);
+          if (rw == kSnapKGrp) {  // full group (every tile but a prefix's last)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 2 * i + sub < rw ? slot[(2 * i + sub) * 16 + ch] : make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < 8; ++i) v[i] = slot[(2 * i + sub) * 16 + ch];
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = 2 * i + sub < rw ? slot[(2 * i + sub) * 16 + ch] : make_uint4(0, 0, 0, 0);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = make_uint4(0, 0, 0, 0);
