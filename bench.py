@@ -270,9 +270,9 @@ def unpack_rate(eng, stream, codec, pool, snap, arrays, names, L, H, D, bpt, lo,
 # kernels whose limit is instruction issue, not HBM (ncu captures in profiles/)
 ISSUE_BOUND = {
     "k_snapkv_tc": "issue-bound: the exp epilogue (FMA + ALU pipes, 1 exp per logit, 268 M logits per chunk) "
-                   "and the per-slice cluster tail; DRAM 548 MB/launch = 1.00x algorithmic; ncu issue active 65 %, "
-                   "180 M warp-instructions per launch (profiles/r2n_ncu_snapkv_raw.csv, "
-                   "r2n_ncu_snapkv_source_summary.txt, DESIGN.md §5)",
+                   "and the per-slice cluster tail; DRAM 548 MB/launch = 1.00x algorithmic; ncu issue active 66 %, "
+                   "173 M warp-instructions per launch (profiles/r3d_ncu_snapkv_raw.csv, "
+                   "r3d_ncu_snapkv_source_summary.txt, DESIGN.md §5)",
     "k_keydiff_cluster": "issue/latency-bound: K is read from HBM once (574 MB/launch with the L2 hints); "
                          "ncu issue active 60 %, 97 M warp-instructions (profiles/r2m_ncu_keydiff_raw.csv)",
 }
