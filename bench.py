@@ -418,7 +418,7 @@ def north_star_pass(args):
     (tests/test_large_placement.py, fixture from the reference greedy)."""
     cmd = [sys.executable, os.path.abspath(__file__), "--config", "c5", "--steps", str(args.n1_steps), "--warmup", "1",
            "--no-cpu-baseline", "--tiered-steps", "0", "--no-n1", "--snap-sms", str(SNAP_SMS.get("c5", 48)),
-           "--streams", str(args.streams), "--lanes", args.lanes]
+           "--streams", str(args.streams), "--lanes", args.lanes, "--group-slices", str(args.group_slices)]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
         d = json.loads(r.stdout.strip().splitlines()[-1])
@@ -578,7 +578,7 @@ def run_b200(args):
         for c, m, r, T, (sl, pl) in zip(cs, ms, rs, Ts, plan):
             k, v = pool.chunk(c)
             if args.lanes == "split":
-                out_b += (codec.compress(m, r, k, v, T, c, pl) if sl is None
+                out_b += (codec.compress(m, r, k, v, T, c, pl, group=args.group_slices) if sl is None
                           else codec.compress_split(m, r, k, v, T, c, sl, pl))
             else:
                 out_b += codec.compress(m, r, k, v, T, c)
@@ -976,6 +976,9 @@ def main():
     ap.add_argument("--n-ctx", type=int, default=None)
     ap.add_argument("--pool", type=int, default=8, help="distinct resident KV chunks")
     ap.add_argument("--streams", type=int, default=3, help="codec CUDA streams")
+    ap.add_argument("--group-slices", type=int, default=0,
+                    help="knorm / keydiff chunks compressed this many (layer, head) slices at a time "
+                         "(kvt_compress_slices: K read from HBM once per group); 0 = whole chunks")
     ap.add_argument("--lanes", choices=["split", "rr"], default="split",
                     help="split: snapkv scoring alone on stream 0 (--snap-sms SM budget), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "

@@ -316,6 +316,14 @@ typedef struct {
 
 KVT_DECLARE_CODEC(kvt_)
 
+/* kvt_compress over slices (layer, head) [s0, s0 + ns) of the chunk only,
+ * same workspace and blob: compressing a chunk as a sequence of slice groups
+ * gives the blob kvt_compress gives. knorm / keydiff (and keep == T) only;
+ * the scoring pass leaves K in L2 for the pack of the same group, so groups
+ * of <= ~64 MB of K are read from HBM once. snapkv: KVT_EINVAL. */
+int kvt_compress_slices(kvt_handle* h, const kvt_kv_shape* shape, const kvt_codec_cfg* cfg, const uint16_t* k,
+                        const uint16_t* v, int32_t s0, int32_t ns, void* workspace, void* blob);
+
 /* ------------------------------------------------------------------------
  * Tier-move executor: turns placement decisions
  * (PlacementAction, proj/include/kvtier/core.hpp:96-103; built at

@@ -163,6 +163,7 @@ PRODUCT_EXTRA_SIGS = {
     "launch_count": (i64, [P]),
     "tier_host_alloc": (C.c_int, [i64, PP]),
     "tier_host_free": (C.c_int, [P]),
+    "compress_slices": (C.c_int, [P, C.POINTER(KvShape), C.POINTER(CodecCfg), P, P, i32, i32, P, P]),
 }
 TIER_SIGS = {"tier_moves": (C.c_int, [P, C.POINTER(Move), i64])}
 FILE_SIGS = {"tier_file_open": (C.c_int, [C.c_char_p, i64, PP]),

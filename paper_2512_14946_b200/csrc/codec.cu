@@ -244,8 +244,10 @@ constexpr int kUnroll = 4;
 
 // knorm: squared L2 norm of every key (larger = keep).
 // KVT_CODEC_KNORM_KEEP_LOW: the negated norm (low norms rank first).
+// keep_l2: K is loaded at normal L2 priority instead of evict-first (the
+// slice-group path of kvt_compress_slices re-reads the kept rows in pack).
 __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, float* __restrict__ out, long long ntok,
-                                               float sign) {
+                                               float sign, int keep_l2) {
   const int l16 = threadIdx.x & 15;
   const long long hw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 4;
   const long long nhw = (gridDim.x * (long long)blockDim.x) >> 4;
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const long long t = t0 + u * nhw;
-      v[u] = t < ntok ? __ldcs(K + t * 16 + l16) : make_uint4(0, 0, 0, 0);
+      v[u] = t < ntok ? (keep_l2 ? __ldg(K + t * 16 + l16) : __ldcs(K + t * 16 + l16)) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
 // products. Bit-identical to k_keydiff_sum + k_keydiff_score.
 constexpr int kKdC = 8;
 __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
-    k_keydiff_cluster(const uint4* __restrict__ K, float* __restrict__ out, int T) {
+    k_keydiff_cluster(const uint4* __restrict__ K, float* __restrict__ out, int T, int keep_l2) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
   const int slice = blockIdx.y, tid = threadIdx.x, l16 = tid & 15, hw = tid >> 4;
@@ -438,7 +440,7 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
     const int tu = u == 0 ? t[0] : (u == 1 ? t[1] : (u == 2 ? t[2] : t[3]));
     const bool lu = u == 0 ? live[0] : (u == 1 ? live[1] : (u == 2 ? live[2] : live[3]));
     if (lu && (l16 & 3) == 0) o[tu] = -__fmul_rn(p, kinv[tu]);
-  }, l2_evict_first());  // last use
+  }, keep_l2 ? l2_evict_normal() : l2_evict_first());  // last use here (keep_l2: pack reads the kept rows next)
   cluster_sync_smem();  // no CTA exits while a peer may still read its sfix
 }
 
@@ -1325,8 +1327,11 @@ static int launch_snapkv(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
   return KVT_OK;
 }
 
+// keep_l2 (knorm / keydiff only): leave K at normal L2 priority for a pack
+// that re-reads it right after (kvt_compress_slices).
 static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                         const uint16_t* q, float* scores, uint8_t* snapq, unsigned long long* fixed) {
+                         const uint16_t* q, float* scores, uint8_t* snapq, unsigned long long* fixed,
+                         int keep_l2 = 0) {
   const int S = s->L * s->H, T = s->T;
   cudaStream_t st = h->stream;
   if (c->scorer == KVT_SCORER_KNORM) {
@@ -1334,12 +1339,13 @@ static int launch_scores(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_c
     const long long want = (ntok * 16 + 255) / 256;
     const int blocks = static_cast<int>(std::min<long long>(want, num_sms() * 16LL));
     k_knorm<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), scores, ntok,
-                                     (c->flags & KVT_CODEC_KNORM_KEEP_LOW) ? -1.0f : 1.0f);
+                                     (c->flags & KVT_CODEC_KNORM_KEEP_LOW) ? -1.0f : 1.0f, keep_l2);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_KEYDIFF && kd_cluster_smem(T) <= 100 * 1024 && T <= kKdC * 16000) {
     KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(k_keydiff_cluster), h->device,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-    k_keydiff_cluster<<<dim3(kKdC, S), 256, kd_cluster_smem(T), st>>>(reinterpret_cast<const uint4*>(k), scores, T);
+    k_keydiff_cluster<<<dim3(kKdC, S), 256, kd_cluster_smem(T), st>>>(reinterpret_cast<const uint4*>(k), scores, T,
+                                                                                       keep_l2);
     LAUNCHED(h);
   } else if (c->scorer == KVT_SCORER_KEYDIFF) {
     KVT_CUDA_TRY(cudaMemsetAsync(fixed, 0, 8LL * S * kD, st));
@@ -1814,36 +1820,45 @@ __global__ void __launch_bounds__(256, 4) k_pack_kv(const uint4* __restrict__ K,
 
 template <int BITS>
 static void launch_pack_bits(cudaStream_t st, const kvt_blob_map& m, char* b, const uint16_t* k, const uint16_t* v,
-                             const int32_t* idx, int S, int T, int kk) {
+                             const int32_t* idx, int s0, int ns, int T, int kk) {
   const int nk = (kk + KVT_QGROUP - 1) / KVT_QGROUP, nv = (kk + 16 * kVRows - 1) / (16 * kVRows);
-  k_pack_kv<BITS><<<dim3(nk + nv, S), 256, 0, st>>>(
+  constexpr size_t wpr = kD * BITS / 32;
+  const size_t r0 = static_cast<size_t>(s0) * kk;  // first kept row of slice s0
+  k_pack_kv<BITS><<<dim3(nk + nv, ns), 256, 0, st>>>(
       reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
-      reinterpret_cast<int32_t*>(b + m.idx_off), reinterpret_cast<uint32_t*>(b + m.kcode_off),
-      reinterpret_cast<uint16_t*>(b + m.kscale_off), reinterpret_cast<uint16_t*>(b + m.kzero_off),
-      reinterpret_cast<uint32_t*>(b + m.vcode_off), reinterpret_cast<uint16_t*>(b + m.vscale_off),
-      reinterpret_cast<uint16_t*>(b + m.vzero_off), T, kk, nk);
+      reinterpret_cast<int32_t*>(b + m.idx_off) + r0, reinterpret_cast<uint32_t*>(b + m.kcode_off) + r0 * wpr,
+      reinterpret_cast<uint16_t*>(b + m.kscale_off) + static_cast<size_t>(s0) * nk * kD,
+      reinterpret_cast<uint16_t*>(b + m.kzero_off) + static_cast<size_t>(s0) * nk * kD,
+      reinterpret_cast<uint32_t*>(b + m.vcode_off) + r0 * wpr, reinterpret_cast<uint16_t*>(b + m.vscale_off) + r0,
+      reinterpret_cast<uint16_t*>(b + m.vzero_off) + r0, T, kk, nk);
 }
 
+// Slices [s0, s0 + ns) of the chunk (the whole chunk: s0 = 0, ns = L * H):
+// k / v / idx point at slice s0 (the kernels index from there); the blob
+// sections are offset to the same slice, so a chunk packed in slice groups
+// is byte-identical to one packed at once.
 static int launch_pack(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
-                       const uint16_t* v, const int32_t* idx, void* blob) {
+                       const uint16_t* v, const int32_t* idx, void* blob, int s0 = 0, int ns = -1) {
   kvt_blob_map m;
   blob_map(*s, *c, &m);
   char* b = static_cast<char*>(blob);
-  const int S = s->L * s->H, kk = c->keep;
+  const int kk = c->keep;
+  if (ns < 0) ns = s->L * s->H;
   cudaStream_t st = h->stream;
   if (m.identity) return KVT_OK;  // nothing to write: the source KV is the blob
   if (c->bits == 16) {
-    dim3 rows_grid((kk + 16 * kGRows - 1) / (16 * kGRows), S);
+    const size_t r0 = static_cast<size_t>(s0) * kk;
+    dim3 rows_grid((kk + 16 * kGRows - 1) / (16 * kGRows), ns);
     k_gather16<<<rows_grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(k), reinterpret_cast<const uint4*>(v), idx,
-                                          reinterpret_cast<int32_t*>(b + m.idx_off),
-                                          reinterpret_cast<uint4*>(b + m.kcode_off),
-                                          reinterpret_cast<uint4*>(b + m.vcode_off), s->T, kk);
+                                          reinterpret_cast<int32_t*>(b + m.idx_off) + r0,
+                                          reinterpret_cast<uint4*>(b + m.kcode_off) + r0 * 16,
+                                          reinterpret_cast<uint4*>(b + m.vcode_off) + r0 * 16, s->T, kk);
     LAUNCHED(h);
     return KVT_OK;
   }
-  if (c->bits == 8) launch_pack_bits<8>(st, m, b, k, v, idx, S, s->T, kk);
-  else if (c->bits == 4) launch_pack_bits<4>(st, m, b, k, v, idx, S, s->T, kk);
-  else launch_pack_bits<2>(st, m, b, k, v, idx, S, s->T, kk);
+  if (c->bits == 8) launch_pack_bits<8>(st, m, b, k, v, idx, s0, ns, s->T, kk);
+  else if (c->bits == 4) launch_pack_bits<4>(st, m, b, k, v, idx, s0, ns, s->T, kk);
+  else launch_pack_bits<2>(st, m, b, k, v, idx, s0, ns, s->T, kk);
   LAUNCHED(h);
   KVT_CUDA_TRY(cudaGetLastError());
   return KVT_OK;
@@ -2017,4 +2032,40 @@ extern "C" int kvt_compress(kvt_handle* h, const kvt_kv_shape* s, const kvt_code
   if ((rc = launch_scores(h, s, c, k, q, scores, snapq, fixed))) return rc;
   if ((rc = launch_topk(h, s, c, scores, idx))) return rc;
   return launch_pack(h, s, c, k, v, idx, blob);
+}
+
+// kvt_compress over slices [s0, s0 + ns) of the chunk only, into the same
+// workspace and blob: a chunk compressed as a sequence of slice groups is
+// byte-identical to kvt_compress. For knorm / keydiff the scoring pass
+// leaves K at normal L2 priority, so with groups of a few tens of MB the
+// pack's reads of the kept rows hit L2 instead of HBM. snapkv scores the
+// whole chunk from its shared window queries (KVT_EINVAL here).
+extern "C" int kvt_compress_slices(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const uint16_t* k,
+                                   const uint16_t* v, int s0, int ns, void* workspace, void* blob) {
+  KVT_ON_DEVICE(h);
+  int rc;
+  if ((rc = check_shape(s, c))) return rc;
+  const int S = s->L * s->H, T = s->T;
+  if (s0 < 0 || ns < 0 || s0 > S || ns > S - s0) return set_error(KVT_EINVAL, "slice range outside the chunk");
+  if (c->keep == T && c->bits == 16) return KVT_OK;  // identity
+  if (ns == 0) return KVT_OK;
+  const size_t rows = static_cast<size_t>(s0) * T * kD;  // bf16 elements before slice s0
+  const uint16_t* ks = k + rows;
+  const uint16_t* vs = v + rows;
+  char* w = static_cast<char*>(workspace);
+  float* scores = reinterpret_cast<float*>(w) + static_cast<size_t>(s0) * T;
+  auto* fixed = reinterpret_cast<unsigned long long*>(w + ws_scores(s) + ws_snapq(s)) + static_cast<size_t>(s0) * kD;
+  int32_t* idx = reinterpret_cast<int32_t*>(w + ws_scores(s) + ws_snapq(s) + ws_fixed(s)) +
+                 static_cast<size_t>(s0) * c->keep;
+  const kvt_kv_shape sub{1, ns, T, s->D};  // the scoring and top-k kernels see only S = L * H and T
+  if (c->keep == T) {
+    const long long n = static_cast<long long>(ns) * T;
+    k_iota<<<static_cast<int>(std::min<long long>((n + 255) / 256, num_sms() * 8LL)), 256, 0, h->stream>>>(idx, T, n);
+    LAUNCHED(h);
+    return launch_pack(h, s, c, ks, vs, idx, blob, s0, ns);
+  }
+  if (c->scorer == KVT_SCORER_SNAPKV) return set_error(KVT_EINVAL, "snapkv compresses whole chunks (kvt_compress)");
+  if ((rc = launch_scores(h, &sub, c, ks, nullptr, scores, nullptr, fixed, 1))) return rc;
+  if ((rc = launch_topk(h, &sub, c, scores, idx))) return rc;
+  return launch_pack(h, s, c, ks, vs, idx, blob, s0, ns);
 }

@@ -84,12 +84,24 @@ class Codec:
                      for _ in self.lanes]
         self.ws, self.out = self._ws[0], self._out[0]
 
-    def compress(self, method: str, ratio: float, k, v, T: int, slot: int, lane: Optional[int] = None) -> int:
+    def compress(self, method: str, ratio: float, k, v, T: int, slot: int, lane: Optional[int] = None,
+                 group: int = 0) -> int:
+        """`group` > 0: knorm / keydiff chunks are compressed `group` slices
+        at a time (kvt_compress_slices: each group's K is read from HBM once,
+        its pack hits L2); the blob is the same."""
         cfg, m, _ = self.plan(method, ratio, T)
         s = A.KvShape(self.L, self.H, T, self.D)
         li = slot % len(self.lanes) if lane is None else lane
         eng, outs = self.lanes[li], self._out[li]
         out = outs[(slot // len(self.lanes)) % len(outs)]
+        S = self.L * self.H
+        if group > 0 and cfg.scorer != 2 and not m.identity and group < S:
+            ws, ob = A.ptr(self._ws[li]), A.ptr(out)
+            for s0 in range(0, S, group):
+                eng.abi.check(eng.abi.compress_slices(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), s0,
+                                                      min(group, S - s0), ws, ob))
+            self.last = (li, out.data_ptr(), m)
+            return self.retained_bytes(m, T)
         eng.abi.check(eng.abi.compress(eng.h, C.byref(s), C.byref(cfg), A.ptr(k), A.ptr(v), None, A.ptr(self._ws[li]),
                                        A.ptr(out)))
         self.last = (li, out.data_ptr(), m)

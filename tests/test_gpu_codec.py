@@ -370,6 +370,48 @@ def test_compress_unpack_bitexact(gpu, orc, si, method, ratio):
     assert np.array_equal(host(kug, np.uint16), kuo) and np.array_equal(host(vug, np.uint16), vuo)
 
 
+@pytest.mark.parametrize("shape,group", [((2, 3, 300), 1), ((2, 3, 300), 4), ((1, 4, 8192), 3),
+                                         ((3, 1, 129), 2), ((2, 2, 4097), 5)])
+@pytest.mark.parametrize("method,ratio", [("knorm-q8", 0.3), ("keydiff-q4", 0.2), ("knorm", 0.4),
+                                          ("keydiff-q2", 1.0), ("knorm-q4", 0.02), ("keydiff", 1.0)])
+def test_compress_slices_bitexact(gpu, orc, shape, group, method, ratio):
+    """kvt_compress_slices over slice groups (ragged last group) writes the
+    blob the oracle's whole-chunk compress writes, byte for byte."""
+    s = A.KvShape(*shape, 128)
+    S = s.L * s.H
+    kg, vg = gen(gpu, s)
+    ko, vo = gen(orc, s, on_gpu=False)
+    cfg = plan(orc.abi, method, ratio, s)
+    m = A.BlobMap()
+    gpu.abi.check(gpu.abi.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
+    ws = torch.empty(gpu.abi.compress_workspace_bytes(C.byref(s), C.byref(cfg)), dtype=torch.uint8, device="cuda")
+    bg = torch.zeros(max(1, m.total_bytes), dtype=torch.uint8, device="cuda")
+    l0 = gpu.abi.launch_count(gpu.h)
+    for s0 in range(0, S, group):
+        gpu.abi.check(gpu.abi.compress_slices(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), A.ptr(vg), s0,
+                                              min(group, S - s0), A.ptr(ws), A.ptr(bg)))
+    gpu.abi.check(gpu.abi.sync(gpu.h))
+    if m.identity:
+        assert gpu.abi.launch_count(gpu.h) == l0
+        return
+    bo, _ = compress(orc, s, cfg, ko, vo, False)
+    sg, so = blob_sections(bg, m, cfg.bits), blob_sections(bo, m, cfg.bits)
+    for name in so:
+        assert np.array_equal(sg[name], so[name]), name
+
+
+def test_compress_slices_rejects(gpu):
+    s = A.KvShape(2, 2, 300, 128)
+    kg, vg = gen(gpu, s)
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    blob = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    for method, s0, ns in (("snapkv-q4", 0, 2), ("knorm-q4", 3, 2), ("knorm-q4", -1, 1), ("knorm-q4", 0, -1)):
+        cfg = plan(gpu.abi, method, 0.2, s)
+        with pytest.raises(A.AbiError):
+            gpu.abi.check(gpu.abi.compress_slices(gpu.h, C.byref(s), C.byref(cfg), A.ptr(kg), A.ptr(vg), s0, ns,
+                                                  A.ptr(ws), A.ptr(blob)))
+
+
 def test_full_llama_chunk_knorm_q4_properties(gpu, orc):
     """One full Llama-3.1-8B chunk (32 L x 8 H x 8192 T x 128, 1 GiB):
     knorm scores bit-exact to the oracle, top-k sorted and sized, and the
