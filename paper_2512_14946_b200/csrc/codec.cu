@@ -1422,15 +1422,20 @@ __device__ __forceinline__ void select_bucket(const int* hist, int rem, int* b_o
   }
 }
 
+// k_topk's dynamic smem: key t at word t + t / 16, the staged indices from
+// word topk_stage_off(T) (16-byte aligned)
+__host__ __device__ constexpr size_t topk_stage_off(int T) {
+  return (static_cast<size_t>(T) + static_cast<size_t>(T) / 16 + 1 + 3) & ~size_t(3);
+}
+
 constexpr int kTopkThreads = 512;
 
 // Per (layer, head): the `keep` largest scores, ties -> lower index,
 // indices ascending. MSB-first 8-bit radix select on orderable keys held in
 // shared memory, starting at the highest bit where the slice's keys differ.
-// Then an order-preserving compaction: warp w owns a run of consecutive 32-token
-// groups (lane = token); one ballot of "above the k-th key" and one of
-// "equal to it" per group rank the kept tokens, and each group's indices go
-// out as one coalesced store.
+// Then an order-preserving compaction: each thread owns a run of consecutive
+// tokens; a block scan of its (above the k-th key, equal to it) counts ranks
+// its kept tokens.
 __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__ scores, int32_t* __restrict__ idx,
                                                        int T, int k, int keys_in_smem) {
   extern __shared__ uint32_t skeys[];  // key t at skeys[t + t / 16]
@@ -1439,18 +1444,45 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   __shared__ int s_remaining, s_bucket, s_remaining_next;
   __shared__ uint32_t s_and[kTopkThreads / 32], s_or[kTopkThreads / 32];
   const int slice = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned lt = (1u << lane) - 1u;
   const float* sc = scores + static_cast<size_t>(slice) * T;
   auto key_at = [&](int t) { return keys_in_smem ? skeys[t + (t >> 4)] : score_key(sc[t]); };
   // the bits every key shares need no radix pass (and would pile the first
   // histogram into one bin): start at the highest bit where keys differ
   uint32_t kand = ~0u, kor = 0u;
+  if (keys_in_smem && (T & 3) == 0 && (reinterpret_cast<uintptr_t>(sc) & 15) == 0) {
+    // 16-byte loads, 4 per thread in flight (T = 8192: all of a thread's keys at once)
+    const float4* sc4 = reinterpret_cast<const float4*>(sc);
+    const int n4 = T >> 2;
+    for (int b = tid; b < n4; b += 4 * kTopkThreads) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = b + u * kTopkThreads;
+        x[u] = i < n4 ? __ldcs(sc4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = b + u * kTopkThreads;
+        if (i < n4) {
+          const uint32_t k4[4] = {score_key(x[u].x), score_key(x[u].y), score_key(x[u].z), score_key(x[u].w)};
+          const int t = 4 * i, o = t + (t >> 4);  // t .. t + 3 share t >> 4
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            skeys[o + e] = k4[e];
+            kand &= k4[e];
+            kor |= k4[e];
+          }
+        }
+      }
+    }
+  } else {
 #pragma unroll 4
-  for (int t = tid; t < T; t += kTopkThreads) {
-    const uint32_t key = score_key(sc[t]);
-    if (keys_in_smem) skeys[t + (t >> 4)] = key;
-    kand &= key;
-    kor |= key;
+    for (int t = tid; t < T; t += kTopkThreads) {
+      const uint32_t key = score_key(sc[t]);
+      if (keys_in_smem) skeys[t + (t >> 4)] = key;
+      kand &= key;
+      kor |= key;
+    }
   }
   kand = __reduce_and_sync(0xffffffffu, kand);
   kor = __reduce_or_sync(0xffffffffu, kor);
@@ -1497,45 +1529,58 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk(const float* __restrict__
   }
   const uint32_t kth = s_prefix;
   const int ties = s_remaining;  // equal-to-kth keys to take (lowest indices)
-  constexpr int kW = kTopkThreads / 32;
-  const int ngrp = (T + 31) / 32, gpw = (ngrp + kW - 1) / kW;
-  const int g0 = warp * gpw, g1 = min(ngrp, g0 + gpw);
+  // thread tid owns tokens [t0, t1) (consecutive: with the 1-in-17 padding
+  // its smem reads are bank-conflict free); one block scan of the (above,
+  // equal) counts gives every thread its first output slot
+  const int per = (T + kTopkThreads - 1) / kTopkThreads;
+  const int t0 = min(T, tid * per), t1 = min(T, t0 + per);
   int na = 0, ne = 0;
-  for (int g = g0; g < g1; ++g) {
-    const int t = g * 32 + lane;
-    const uint32_t key = t < T ? key_at(t) : 0u;
-    na += __popc(__ballot_sync(0xffffffffu, t < T && key > kth));
-    ne += __popc(__ballot_sync(0xffffffffu, t < T && key == kth));
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t key = key_at(t);
+    na += key > kth;
+    ne += key == kth;
   }
-  if (lane == 0) {
-    s_and[warp] = static_cast<uint32_t>(na);  // (the key-bit reductions are done with these)
-    s_or[warp] = static_cast<uint32_t>(ne);
+  int ia = na, ie = ne;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, ia, off), e = __shfl_up_sync(0xffffffffu, ie, off);
+    if (lane >= off) {
+      ia += a;
+      ie += e;
+    }
+  }
+  if (lane == 31) {
+    s_and[warp] = static_cast<uint32_t>(ia);  // (the key-bit reductions are done with these)
+    s_or[warp] = static_cast<uint32_t>(ie);
   }
   __syncthreads();
-  int a_before = 0, e_before = 0;
+  int a_before = ia - na, e_before = ie - ne;
   for (int w = 0; w < warp; ++w) {
     a_before += static_cast<int>(s_and[w]);
     e_before += static_cast<int>(s_or[w]);
   }
   int pos = a_before + min(e_before, ties), eq_seen = e_before;
   int32_t* out = idx + static_cast<size_t>(slice) * k;
-  for (int g = g0; g < g1; ++g) {
-    const int t = g * 32 + lane;
-    const uint32_t key = t < T ? key_at(t) : 0u;
-    const bool gt = t < T && key > kth, eq = t < T && key == kth;
-    const unsigned be = __ballot_sync(0xffffffffu, eq);
-    const bool keep = gt || (eq && eq_seen + __popc(be & lt) < ties);
-    const unsigned bk = __ballot_sync(0xffffffffu, keep);
-    if (keep) out[pos + __popc(bk & lt)] = t;
-    pos += __popc(bk);
-    eq_seen += __popc(be);
+  // with the keys in smem the indices are staged there too (after the keys)
+  // and leave as coalesced stores: a thread's own run of slots would touch a
+  // different sector per lane per store
+  int32_t* stage = keys_in_smem ? reinterpret_cast<int32_t*>(skeys + topk_stage_off(T)) : out;
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t key = key_at(t);
+    const bool eq = key == kth;
+    if (key > kth || (eq && eq_seen < ties)) stage[pos++] = t;
+    eq_seen += eq;
+  }
+  if (keys_in_smem) {
+    __syncthreads();
+    for (int j = tid; j < k; j += kTopkThreads) out[j] = stage[j];
   }
 }
 
 static int launch_topk(kvt_handle* h, const kvt_kv_shape* s, const kvt_codec_cfg* c, const float* scores,
                        int32_t* idx) {
   const int S = s->L * s->H;
-  const size_t smem = sizeof(uint32_t) * (size_t(s->T) + size_t(s->T) / 16 + 1);
+  const size_t smem = sizeof(uint32_t) * (topk_stage_off(s->T) + size_t(c->keep));  // keys, then staged indices
   const int in_smem = smem <= 160 * 1024;
   KVT_CUDA_TRY(func_attr(reinterpret_cast<const void*>(k_topk), h->device, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          160 * 1024));

@@ -58,9 +58,9 @@ def main():
         ab.check(ab.blob_layout(C.byref(s), C.byref(cfg), C.byref(m)))
         S = s.L * s.H
         sc = torch.empty(S * s.T, dtype=torch.float32, device="cuda")
-        idx = torch.empty(S * cfg.keep, dtype=torch.int32, device="cuda")
+        idx = torch.zeros(S * cfg.keep, dtype=torch.int32, device="cuda")
         blob = torch.empty(m.total_bytes, dtype=torch.uint8, device="cuda")
-        ws = torch.empty(ab.compress_workspace_bytes(C.byref(s), C.byref(cfg)), dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(ab.compress_workspace_bytes(C.byref(s), C.byref(cfg)), dtype=torch.uint8, device="cuda")
         kk = cfg.keep
         alg = {
             "scores": S * s.T * 256 + S * s.T * 4,

@@ -279,14 +279,15 @@ def test_topk_bitexact_with_ties(gpu, orc, keep_ratio):
 
 # top-k key distributions for the adaptive first radix digit: every key
 # equal, keys differing only in the last mantissa bits, +inf window scores
-# mixed in, the full signed range, and a slice too long for smem keys
-TOPK_CASES = ["equal", "ulps", "inf", "wide", "long"]
+# mixed in, the full signed range, a slice too long for smem keys, and an
+# odd-length slice whose keys + staged indices fit smem at small keep only
+TOPK_CASES = ["equal", "ulps", "inf", "wide", "long", "odd"]
 
 
 @pytest.mark.parametrize("case", TOPK_CASES)
 @pytest.mark.parametrize("keep_ratio", [0.01, 0.37, 0.9])
 def test_topk_key_distributions(gpu, orc, case, keep_ratio):
-    T = 41000 if case == "long" else 3000
+    T = {"long": 41000, "odd": 30001}.get(case, 3000)
     s = A.KvShape(1, 2, T, 128)
     rng = np.random.default_rng(7)
     n = s.L * s.H * s.T
@@ -297,6 +298,8 @@ def test_topk_key_distributions(gpu, orc, case, keep_ratio):
     elif case == "inf":
         sc = rng.standard_normal(n).astype(np.float32)
         sc[rng.random(n) < 0.05] = np.inf
+    elif case == "odd":
+        sc = rng.standard_normal(n).astype(np.float32)
     else:
         sc = (rng.standard_normal(n) * np.float32(1e30)).astype(np.float32)
         sc[::13] = -0.0
