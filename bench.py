@@ -636,6 +636,37 @@ def run_b200(args):
     ms_step = ms / args.steps
     value = total_bytes / (ms_step / 1e3) / 1e9
 
+    if args.lane_trace:  # diagnostic only (stderr): where the codec streams wait on each other in one step
+        barrier()
+        codec.trace = []
+        marks = []
+        for ls in lane_streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(ls)
+            marks.append(e)
+        run_steps(1, False, exchange_value)
+        ends = []
+        for ls in lane_streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(ls)
+            ends.append(e)
+        barrier()
+        t0 = marks[0]
+        rel = lambda e: t0.elapsed_time(e)  # noqa: E731
+        n = len(lane_streams)
+        stall = [0.0] * n
+        ring_stall = score_busy = 0.0
+        for sl, pl, ev in codec.trace:
+            ring_stall += ev[0].elapsed_time(ev[1])
+            score_busy += ev[1].elapsed_time(ev[2])
+            stall[pl] += ev[3].elapsed_time(ev[4])
+        print(json.dumps({"lane_trace": {
+            "lane_end_ms": [round(rel(e), 2) for e in ends],
+            "pack_lane_wait_on_scores_ms": [round(x, 2) for x in stall],
+            "score_lane_wait_on_ring_ms": round(ring_stall, 2), "score_lane_scoring_ms": round(score_busy, 2),
+            "split_contexts": len(codec.trace)}}), file=sys.stderr)
+        codec.trace = None
+
     # ---- e2e: through the C ABI with host buffers, copies inside the timed region
     e2e_ms, (_, _, _, _, acts, snap_full) = timed(lambda: run_steps(args.steps, True, True))
     h2d = rp.h2d_bytes
@@ -983,6 +1014,8 @@ def main():
                     help="split: snapkv scoring alone on stream 0 (--snap-sms SM budget), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
+    ap.add_argument("--lane-trace", action="store_true",
+                    help="diagnostic: one extra step with per-context stream events; stream waits to stderr")
     ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
     ap.add_argument("--snap-sms", type=int, default=None,
                     help="split mode: SM budget of snapkv's persistent clusters (sets KVT_SNAP_SMS); default "

@@ -54,6 +54,7 @@ class Codec:
         self._ws: List[torch.Tensor] = []
         self._out: List[List[torch.Tensor]] = []
         self.last = None  # (lane, blob address, BlobMap) of the latest compress: the tier executor's source
+        self.trace = None  # a list: compress_split appends (score lane, pack lane, events) (lane-stall probe)
 
     def plan(self, method: str, ratio: float, T: int):
         key = (method, ratio, T)
@@ -137,10 +138,22 @@ class Codec:
         self._ri = (j + 1) % len(self._ring)
         se, pe = self.lanes[score_lane], self.lanes[pack_lane]
         ss, ps = self._streams[score_lane], self._streams[pack_lane]
+        tr = self.trace
+        if tr is not None:  # lane-stall probe: when each stream reaches / passes its cross-stream wait
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev[0].record(ss)
         ss.wait_event(self._free[j])  # the ring slot's previous top-k has read it
+        if tr is not None:
+            ev[1].record(ss)
         se.abi.check(se.abi.token_scores(se.h, C.byref(s), C.byref(cfg), A.ptr(k), None, A.ptr(self._ring[j])))
         self._ready[j].record(ss)
+        if tr is not None:
+            ev[2].record(ss)
+            ev[3].record(ps)
         ps.wait_event(self._ready[j])
+        if tr is not None:
+            ev[4].record(ps)
+            tr.append((score_lane, pack_lane, ev))
         idx = self._idx[pack_lane]
         pe.abi.check(pe.abi.topk(pe.h, C.byref(s), C.byref(cfg), A.ptr(self._ring[j]), A.ptr(idx)))
         self._free[j].record(ps)
