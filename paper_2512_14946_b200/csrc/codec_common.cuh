@@ -122,7 +122,7 @@ __device__ __forceinline__ uint32_t quant_exact(float x, float zf, float inv, in
 // Fast path of quant_exact for 8 channels (one 16-byte bf16 chunk, words
 // q = channel pairs (2q, 2q+1)): one packed fp32x2 subtract and one fused
 // multiply-add with 1.5 * 2^23 (= rint of the exact product, |y| < 2^22),
-// then both codes clamped as int16 lanes. Lane word q: code 2q in bits
+// then both codes clamped as int16 lanes (min + relu, one op). Lane word q: code 2q in bits
 // 0..15, code 2q+1 in bits 16..31. Exact when QParam::fast holds.
 template <int BITS>
 __device__ __forceinline__ void quant8_fast(const uint4& v, const float2 (&nz)[4], const float2 (&iv)[4],
@@ -133,9 +133,8 @@ __device__ __forceinline__ void quant8_fast(const uint4& v, const float2 (&nz)[4
   for (int q = 0; q < 4; ++q) {
     const float2 d = __fadd2_rn(make_float2(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)), nz[q]);
     const float2 r = __ffma2_rn(d, iv[q], make_float2(12582912.0f, 12582912.0f));
-    uint32_t c = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x5410);
-    c = __vmaxs2(c, 0u);
-    p[q] = __vminu2(c, hi2);
+    const uint32_t c = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x5410);
+    p[q] = __vimin_s16x2_relu(c, hi2);  // max(min(c, 2^b - 1), 0) per int16 lane, one instruction
   }
 }
 // same lane layout through quant_exact (any parameters)
@@ -155,16 +154,17 @@ __device__ __forceinline__ void quant8_exact(const uint4& v, const float (&z)[8]
 template <int BITS>
 __device__ __forceinline__ uint2 pack8(const uint32_t (&p)[4]) {
   if (BITS == 8) return make_uint2(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420));
+  // codes sit in 16-bit lanes (code 2q in bits 0.., code 2q+1 in bits 16..):
+  // shifted adds interleave them without overlapping bits (LEA), then one
+  // x + (x >> k) (LEA.HI) folds the high lanes down next to the low ones
   if (BITS == 4) {
-    uint32_t t[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) t[q] = p[q] | (p[q] >> 12);  // byte 0 = code 2q | code 2q+1 << 4
-    return make_uint2(__byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410), 0u);
+    const uint32_t x = p[0] + (p[1] << 8), y = p[2] + (p[3] << 8);  // codes 0,2 | 1,3 (and 4,6 | 5,7)
+    const uint32_t xs = x + (x >> 12), ys = y + (y >> 12);          // low 16 bits: nibbles 0..3 (4..7)
+    return make_uint2(__byte_perm(xs, ys, 0x5410), 0u);
   }
-  uint32_t t[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) t[q] = p[q] | (p[q] >> 14);  // bits 0..3 = code 2q | code 2q+1 << 2
-  return make_uint2((t[0] | (t[1] << 4) | (t[2] << 8) | (t[3] << 12)) & 0xffffu, 0u);
+  const uint32_t x = p[0] + (p[1] << 4), y = p[2] + (p[3] << 4);
+  const uint32_t z = x + (y << 8);  // codes 0,2,4,6 at bits 0,4,8,12; 1,3,5,7 at 16,20,24,28
+  return make_uint2((z + (z >> 14)) & 0xffffu, 0u);
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }

@@ -34,6 +34,13 @@ __global__ void kern(float* out, long long* cyc, float a, float b) {
       if (MODE == 7) u[i] = max(u[i], u[(i + 1) & 7]);                            // VIMNMX
       if (MODE == 8) u[i] = u[i] + (u[(i + 1) & 7] << 10);                        // LEA / IMAD.SHL + IADD
       if (MODE == 9) h[i] = __hfma2(h[i], h[(i + 1) & 7], hd);                     // HFMA2 r, r, r (dep)
+      if (MODE == 10) {                                                           // FHFMA.BF16: bf16 x bf16 + f32
+        float r;
+        asm("{.reg .b16 l, h; mov.b32 {l, h}, %1; fma.rn.f32.bf16 %0, h, l, %2;}" : "=f"(r) : "r"(u[i]), "f"(x[i].x));
+        x[i].x = r;
+        u[i] ^= __float_as_uint(r);
+      }
+      if (MODE == 11) u[i] = __vimin_s16x2_relu(u[i], u[(i + 3) & 7]);            // VIMNMX.S16x2 relu
     }
   }
   long long t1 = clock64();
@@ -48,10 +55,10 @@ int main() {
   float* out; long long* cyc;
   cudaMalloc(&out, 1 << 24); cudaMalloc(&cyc, 8 * 1024);
   const char* names[] = {"HFMA2", "HADD2 imm", "HMNMX2", "F2FP f32x2->f16x2", "LOP3", "FMNMX", "IDP.4A", "VIMNMX",
-                         "shift+add", "HFMA2 r,r,r"};
-  void (*fn[])(float*, long long*, int) = {run<0>, run<1>, run<2>, run<3>, run<4>, run<5>, run<6>, run<7>, run<8>, run<9>};
+                         "shift+add", "HFMA2 r,r,r", "FHFMA.BF16 (+LOP3)", "VIMNMX.S16x2.RELU"};
+  void (*fn[])(float*, long long*, int) = {run<0>, run<1>, run<2>, run<3>, run<4>, run<5>, run<6>, run<7>, run<8>, run<9>, run<10>, run<11>};
   for (int warps = 8; warps <= 32; warps *= 2)
-    for (int m = 0; m < 10; ++m) {
+    for (int m = 0; m < 12; ++m) {
       fn[m](out, cyc, warps); cudaDeviceSynchronize(); fn[m](out, cyc, warps);
       long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       const double per = double(c) / (double(N) * 8 * (warps / 4));
