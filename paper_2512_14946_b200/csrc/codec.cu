@@ -1667,10 +1667,15 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
   const int32_t* ix = idx + static_cast<size_t>(slice) * k + j0;
   const uint4* Ks = K + static_cast<size_t>(slice) * T * 16 + cg;
   uint4 v[8];
+  if (nr == KVT_QGROUP) {  // every group but a slice's last: no row masks
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = rs * 8 + i;
-    v[i] = r < nr ? __ldcs(Ks + static_cast<uint32_t>(ix[r]) * 16u) : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < 8; ++i) v[i] = __ldcs(Ks + static_cast<uint32_t>(ix[rs * 8 + i]) * 16u);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = rs * 8 + i;
+      v[i] = r < nr ? __ldcs(Ks + static_cast<uint32_t>(ix[r]) * 16u) : make_uint4(0, 0, 0, 0);
+    }
   }
   const uint32_t kInf2 = 0x7f807f80u, kNInf2 = 0xff80ff80u;
   uint32_t mn[4] = {kInf2, kInf2, kInf2, kInf2}, mx[4] = {kNInf2, kNInf2, kNInf2, kNInf2};
@@ -1782,11 +1787,18 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
   const uint4* Vs = V + static_cast<size_t>(slice) * T * 16 + l16;
   int tok[kVRows];
   uint4 v[kVRows];
+  if (j_first + kVRows <= k) {  // all rows live (half-warp uniform)
 #pragma unroll
-  for (int i = 0; i < kVRows; ++i) tok[i] = j_first + i < k ? ix[j_first + i] : 0;
+    for (int i = 0; i < kVRows; ++i) tok[i] = ix[j_first + i];
 #pragma unroll
-  for (int i = 0; i < kVRows; ++i)
-    v[i] = j_first + i < k ? __ldcs(Vs + static_cast<uint32_t>(tok[i]) * 16u) : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < kVRows; ++i) v[i] = __ldcs(Vs + static_cast<uint32_t>(tok[i]) * 16u);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kVRows; ++i) tok[i] = j_first + i < k ? ix[j_first + i] : 0;
+#pragma unroll
+    for (int i = 0; i < kVRows; ++i)
+      v[i] = j_first + i < k ? __ldcs(Vs + static_cast<uint32_t>(tok[i]) * 16u) : make_uint4(0, 0, 0, 0);
+  }
   static_assert(kVRows == 8, "transpose-reduce below is written for 8 rows per half-warp");
   // (min, max) of each row's 128 channels as a bf16 pair, reduced over the
   // half-warp for all 8 rows at once: at each butterfly level a lane keeps
@@ -1819,11 +1831,12 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
   }
   constexpr int wpr = kD * BITS / 32;
   const int fast_mine = p.fast ? 1 : 0;
+  const bool all_fast = __all_sync(0xffffffffu, p.fast);  // every row of both half-warps (the common case)
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
     const int j = j_first + i;
     const float zf = __shfl_sync(0xffffffffu, p.zf, base + 2 * i), inv = __shfl_sync(0xffffffffu, p.inv, base + 2 * i);
-    const int fast = __shfl_sync(0xffffffffu, fast_mine, base + 2 * i);
+    const int fast = all_fast ? 1 : __shfl_sync(0xffffffffu, fast_mine, base + 2 * i);
     uint32_t lanes[4];
     if (fast) {
       const float2 nz[4] = {make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf), make_float2(-zf, -zf)};
