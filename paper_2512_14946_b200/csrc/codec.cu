@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(256) k_keydiff_score(const uint4* __restrict__
 // the same rows (~18 slices x 2 MiB in flight: L2 hits) for the dot
 // products. Bit-identical to k_keydiff_sum + k_keydiff_score.
 constexpr int kKdC = 8;
-__global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 4)
+__global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 3)
     k_keydiff_cluster(const uint4* __restrict__ K, float* __restrict__ out, int T, int keep_l2) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = static_cast<int>(cl.block_rank());
@@ -375,9 +375,7 @@ __global__ void __cluster_dims__(kKdC, 1, 1) __launch_bounds__(256, 4)
   extern __shared__ __align__(16) uint8_t kd_raw[];
   uint4* ring = reinterpret_cast<uint4*>(kd_raw);
   float* kinv = reinterpret_cast<float*>(kd_raw + kRingBytes);
-  // warp partials of pass 1 live in the ring (idle between the passes): 4 KB
-  // less static smem, so 4 CTAs fit on an SM
-  int32_t (*part)[kD] = reinterpret_cast<int32_t (*)[kD]>(ring);
+  __shared__ int32_t part[8][kD];
   __shared__ long long sfix[kD];
   __shared__ float sdir[kD];
   __shared__ __align__(8) uint64_t full[kRingStages];
