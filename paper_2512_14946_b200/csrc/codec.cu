@@ -260,12 +260,15 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
       const long long t = t0 + u * nhw;
       v[u] = t < ntok ? (keep_l2 ? __ldg(K + t * 16 + l16) : __ldcs(K + t * 16 + l16)) : make_uint4(0, 0, 0, 0);
     }
+    // the 4 rows' butterflies at once (bit-identical to one per row): lanes
+    // 4u .. 4u + 3 of the half-warp end with row u's sum
+    static_assert(kUnroll == 4, "half_butterfly4 reduces 4 rows");
+    float q[4];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const long long t = t0 + u * nhw;
-      const float n2 = half_butterfly(chunk_sumsq(v[u]));
-      if (t < ntok && l16 == 0) out[t] = sign * n2;
-    }
+    for (int u = 0; u < 4; ++u) q[u] = chunk_sumsq(v[u]);
+    const float n2 = half_butterfly4(q);
+    const long long t = t0 + (l16 >> 2) * nhw;
+    if (t < ntok && (l16 & 3) == 0) out[t] = sign * n2;
   }
 }
 
