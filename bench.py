@@ -405,8 +405,10 @@ def _alias(ptr, n):
 
 # snapkv's SM budget in the split schedule, per workload: A/B on one B200
 # (alternating runs, same box): c2 48 SMs 3,507 / 56 3,475 / 64 3,453 GB/s;
-# c5 (varied lengths, up to 16-CTA clusters) 48 3,278 / 64 3,323 GB/s.
-SNAP_SMS = {"c5": 64}
+# c5 (varied lengths, up to 16-CTA clusters) 48 3,278 / 64 3,323 GB/s;
+# r2z, after the pack cuts: c3 48 / 56 / 64 3,446 / 3,507 / 3,477; c4 48 /
+# 64 / 80 3,689 / 3,743 / 3,687 (profiles/r2z_c34_sms_sweep.txt).
+SNAP_SMS = {"c3": 56, "c4": 64, "c5": 64}
 
 
 def north_star_pass(args):
