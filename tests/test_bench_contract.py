@@ -55,3 +55,19 @@ def test_b200_arm_contract():
     c = d["clocks"]
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in c, k
+
+
+@pytest.mark.gpu
+def test_b200_lane_trace_diagnostic():
+    """--lane-trace adds one traced step and reports the cross-stream waits on
+    stderr; stdout keeps exactly one JSON line."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--n-ctx", "16", "--steps", "1", "--warmup",
+                        "3", "--no-n1", "--tiered-steps", "0", "--no-cpu-baseline", "--lane-trace"],
+                       capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert len([l for l in r.stdout.strip().splitlines() if l.startswith("{")]) == 1
+    tr = [json.loads(l)["lane_trace"] for l in r.stderr.splitlines() if l.startswith('{"lane_trace"')]
+    assert len(tr) == 1
+    t = tr[0]
+    assert len(t["lane_end_ms"]) == len(t["pack_lane_wait_on_scores_ms"]) >= 2
+    assert all(x >= 0 for x in t["pack_lane_wait_on_scores_ms"]) and t["score_lane_scoring_ms"] >= 0
