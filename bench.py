@@ -536,7 +536,11 @@ def run_b200(args):
 
     max_T = int(mine.orig.max() // bpt)
     pool = KVPool(eng, L, H, max_T, D, n_chunks=args.pool)
-    lane_streams = [torch.cuda.Stream() for _ in range(args.streams)]
+    # stream priorities (lower = higher priority): "snap" favours the snapkv
+    # stream's launches, "mem" the memory streams'; default none
+    prio = {"none": [0] * args.streams, "snap": [-1] + [0] * (args.streams - 1),
+            "mem": [0] + [-1] * (args.streams - 1)}[args.lane_priority]
+    lane_streams = [torch.cuda.Stream(priority=p_) for p_ in prio]
     lanes = [Engine(pkg.product(), device=local, stream=ls.cuda_stream) for ls in lane_streams]
     codec = Codec(lanes, L, H, D)
     codec.reserve(max_T, n_out=2)
@@ -1016,6 +1020,8 @@ def main():
                     help="split: snapkv scoring alone on stream 0 (--snap-sms SM budget), every other codec "
                          "kernel on streams 1.. (pipeline.split_plan); rr: contexts round-robin, one kvt_compress "
                          "each")
+    ap.add_argument("--lane-priority", choices=["none", "snap", "mem"], default="none",
+                    help="CUDA stream priorities of the codec streams (diagnostic)")
     ap.add_argument("--lane-trace", action="store_true",
                     help="diagnostic: one extra step with per-context stream events; stream waits to stderr")
     ap.add_argument("--ring", type=int, default=8, help="split mode: score buffers between the streams")
