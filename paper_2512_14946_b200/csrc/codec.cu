@@ -1835,6 +1835,7 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
   constexpr int wpr = kD * BITS / 32;
   const int fast_mine = p.fast ? 1 : 0;
   const bool all_fast = __all_sync(0xffffffffu, p.fast);  // every row of both half-warps (the common case)
+  uint32_t* const out0 = vc + (static_cast<size_t>(slice) * k + j_first) * wpr;  // row j_first; row i at + i * wpr
 #pragma unroll
   for (int i = 0; i < kVRows; ++i) {
     const int j = j_first + i;
@@ -1850,7 +1851,7 @@ __device__ __forceinline__ void pack_v_rows(const uint4* __restrict__ V, const i
       quant8_exact<BITS>(v[i], z8, i8, lanes);
     }
     const uint2 c = pack8<BITS>(lanes);
-    uint32_t* out = vc + (static_cast<size_t>(slice) * k + j) * wpr;
+    uint32_t* out = out0 + i * wpr;
     const bool live = j < k;
     if (BITS == 8) {
       if (live) __stcs(reinterpret_cast<uint2*>(out) + l16, c);
