@@ -1650,7 +1650,7 @@ __global__ void __launch_bounds__(256) k_gather16(const uint4* __restrict__ K, c
 struct PackKSmem {
   uint32_t red[8][16][8];  // [warp][cg][4 min | 4 max] bf16x2
   float zf[kD], inv[kD];
-  int fast[kD];
+  alignas(8) uint8_t fast[kD];  // 0 / 1 per channel: a thread's 8 channels are one 8-byte load
 };
 
 __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
@@ -1730,7 +1730,7 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
     const QParam p = make_param(hi ? bf_hi(a) : bf_lo(a), hi ? bf_hi(b) : bf_lo(b), BITS);
     sm.zf[tid] = p.zf;
     sm.inv[tid] = p.inv;
-    sm.fast[tid] = p.fast;
+    sm.fast[tid] = p.fast ? 1 : 0;
     const size_t po = (static_cast<size_t>(slice) * ng + g) * kD + tid;
     ks[po] = p.s16;
     kz[po] = p.z16;
@@ -1742,7 +1742,10 @@ __device__ __forceinline__ void pack_k_group(const uint4* __restrict__ K, const 
   for (int e = 0; e < 8; ++e) {
     z[e] = sm.zf[cg * 8 + e];
     iv[e] = sm.inv[cg * 8 + e];
-    fast &= sm.fast[cg * 8 + e] != 0;
+  }
+  {
+    const uint2 f8 = *reinterpret_cast<const uint2*>(&sm.fast[cg * 8]);
+    fast = (f8.x & f8.y) == 0x01010101u;
   }
   constexpr int wpr = kD * BITS / 32;
   uint32_t* out = kc + static_cast<size_t>(slice) * k * wpr;
