@@ -217,6 +217,26 @@ __device__ __forceinline__ float chunk_sumsq(const uint4& v) {
   }
   return __fadd_rn(acc.x, acc.y);
 }
+// chunk_sumsq on the raw bf16 words: fma.rn.f32.bf16 (FHFMA.BF16, half
+// select) squares each element exactly and adds in fp32, so the two chains
+// (low / high halves) and their final add are chunk_sumsq's, bit for bit,
+// in 8 instructions instead of 8 unpacks + 4 FFMA2
+__device__ __forceinline__ float fma_bf16_sq(uint32_t w, bool hi, float c) {
+  float r;
+  if (hi) asm("{.reg .b16 l, h; mov.b32 {l, h}, %1; fma.rn.f32.bf16 %0, h, h, %2;}" : "=f"(r) : "r"(w), "f"(c));
+  else asm("{.reg .b16 l, h; mov.b32 {l, h}, %1; fma.rn.f32.bf16 %0, l, l, %2;}" : "=f"(r) : "r"(w), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float chunk_sumsq_raw(const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  float lo = 0.0f, hi = 0.0f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    lo = fma_bf16_sq(w[q], false, lo);
+    hi = fma_bf16_sq(w[q], true, hi);
+  }
+  return __fadd_rn(lo, hi);
+}
 // butterfly over the 16 chunk sums of a half-warp (strides 8, 4, 2, 1);
 // warp-uniform (full-mask shuffles; both half-warps call)
 __device__ __forceinline__ float half_butterfly(float p) {
@@ -265,7 +285,7 @@ __global__ void __launch_bounds__(256) k_knorm(const uint4* __restrict__ K, floa
     static_assert(kUnroll == 4, "half_butterfly4 reduces 4 rows");
     float q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = chunk_sumsq(v[u]);
+    for (int u = 0; u < 4; ++u) q[u] = chunk_sumsq_raw(v[u]);
     const float n2 = half_butterfly4(q);
     const long long t = t0 + (l16 >> 2) * nhw;
     if (t < ntok && (l16 & 3) == 0) out[t] = sign * n2;
